@@ -1,0 +1,338 @@
+"""Generate tests/golden/*.npz from the LIVE reference (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python -m oracle.gen_golden
+
+Imports the reference package read-only from /root/reference/pkg/src and records its
+outputs on seeded inputs.  The fixtures travel with the repo (the reference does
+not exist on the GPU box).  Cases (reference file:line they exercise):
+
+  philox.npz    rng.stream f32/f64 draws + derive_seed          rng.py:27-39
+  exp.npz       numpy float32 exp on the hot-path input range    prediction.py:156
+  predict_*.npz predict() hyp indices, per-step counts, float32 positions, layers
+                                                                prediction.py:223-255
+  belief.npz    update_belief() chains incl. masked/zero-prior/fallback
+                                                                belief.py:159-198
+  smooth.npz    smooth_values() on random layers                occupancy.py:139-154
+  multi.npz     sim-style per-human predict + union_max + time union
+                                                                sim.py:489-504
+  exact.npz     exact_predict() on the lattice instance         prediction.py:303-377
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def _ref():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import gridcast  # noqa: F401
+    return gridcast
+
+
+def gen_philox(G):
+    from gridcast import rng
+    r = np.random.default_rng(123)
+    seeds, paths, f32, f64, derived = [], [], [], [], []
+    for i in range(64):
+        seed = int(r.integers(0, 2**63)) if i % 3 else int(r.integers(0, 2**20))
+        plen = int(r.integers(0, 6))
+        path = [int(r.integers(0, 2**32)) if j % 2 else int(r.integers(0, 300)) for j in range(plen)]
+        seeds.append(seed)
+        paths.append(path)
+        f32.append(rng.stream(seed, *path).random(24, dtype=np.float32))
+        f64.append(rng.stream(seed, *path).random(12))
+        derived.append(rng.derive_seed(seed, *path))
+    np.savez_compressed(
+        os.path.join(OUT, "philox.npz"),
+        meta=json.dumps(dict(seeds=seeds, paths=paths, derived=[str(d) for d in derived])),
+        f32=np.stack(f32), f64=np.stack(f64),
+    )
+
+
+def gen_exp():
+    r = np.random.default_rng(7)
+    x = np.concatenate([
+        r.uniform(-110, 0, 60000), r.uniform(-2, 0, 20000), np.linspace(-104.0, -86.0, 20000),
+        np.array([0.0, -0.0, -1e-30, -87.33654, -103.972, -103.97208404541015625, -104.0]),
+    ]).astype(np.float32)
+    np.savez_compressed(os.path.join(OUT, "exp.npz"), x=x, y=np.exp(x))
+
+
+def _spec(G, case):
+    cs = G.ControlSet([G.ControlAction(float(v), float(t)) for v, t in zip(case["v"], case["theta"])])
+    space = G.HypothesisSpace(G.RationalitySet(tuple(case["betas"])), G.GoalSet(np.array(case["goals"])))
+    fam = case["q"]
+    if fam["family"] == "goal_progress":
+        q = G.q_goal_progress(fam["tau"], (fam["w_v"], fam["w_th"]))
+    else:
+        q = G.q_default((fam["w_v"], fam["w_th"]))
+    if fam.get("v_threshold") is not None:
+        from gridcast.belief import mask_stationary
+        q = mask_stationary(q, cs, fam["v_threshold"])
+    g = case["grid"]
+    spec = G.GridSpec(g[0], g[1], g[2], tuple(g[3]))
+    return cs, space, q, spec
+
+
+def _grid_cs():
+    from oracle.model import control_grid
+    v, th = control_grid(4, 24, 1.4)
+    return v.tolist(), th.tolist()
+
+
+def predict_cases():
+    v, th = _grid_cs()
+    lat_th = [0.0, math.pi / 2, -math.pi / 2, -math.pi] * 2
+    lat_v = [0.0] * 4 + [1.0] * 4
+    gp = dict(family="goal_progress", tau=0.5, w_v=0.0, w_th=0.0, v_threshold=None)
+    cases = {
+        # cfg1 (BASELINE.json configs[0]): 1 human, 2 goals, 5 betas, 1024 particles, T=20,
+        # dt 0.1, 100x100 @ 0.1 m; sigma 0 (count parity) and 0.1 (smoothed layers)
+        "cfg1_s0": dict(v=v, theta=th, betas=list(np.geomspace(0.1, 10, 5)),
+                        goals=[[8.5, 5.0], [1.5, 7.0]], q=gp, grid=[100, 100, 0.1, [0.0, 0.0]],
+                        z0=[5.0, 5.0], n=1024, steps=20, dt=0.1, sigma=0.0, seed=0, prefix=[2, 0],
+                        belief="posterior"),
+        "cfg1_s01": dict(v=v, theta=th, betas=list(np.geomspace(0.1, 10, 5)),
+                         goals=[[8.5, 5.0], [1.5, 7.0]], q=gp, grid=[100, 100, 0.1, [0.0, 0.0]],
+                         z0=[5.0, 5.0], n=1024, steps=20, dt=0.1, sigma=0.1, seed=3, prefix=[],
+                         belief="posterior"),
+        # ragged particle count (partial last chunk), weights, edge clamping near origin
+        "ragged_w": dict(v=v, theta=th, betas=[0.5, 2.0, 8.0], goals=[[-1.0, 0.3], [3.0, 2.9]],
+                         q=dict(family="goal_progress", tau=0.3, w_v=0.2, w_th=0.1, v_threshold=None),
+                         grid=[40, 30, 0.1, [0.0, 0.0]], z0=[0.35, 0.2], n=3333, steps=12, dt=0.1,
+                         sigma=0.0, seed=99, prefix=[2, 5], belief="random"),
+        # stationary-masked Q (mask_stationary drops base_policy -> full base)
+        "masked": dict(v=v, theta=th, betas=list(np.geomspace(0.1, 10, 5)),
+                       goals=[[4.0, 9.0], [9.0, 1.0], [0.5, 0.5], [6.0, 6.0]],
+                       q=dict(family="goal_progress", tau=0.5, w_v=0.0, w_th=0.0, v_threshold=0.5),
+                       grid=[100, 100, 0.1, [0.0, 0.0]], z0=[5.0, 5.0], n=2048, steps=10, dt=0.1,
+                       sigma=0.0, seed=5, prefix=[2, 1], belief="random"),
+        # q_default with weights (position-independent policy)
+        "qdefault": dict(v=v, theta=th, betas=[0.3, 1.0, 3.0],
+                         goals=[[1.0, 1.0], [2.0, 3.0]],
+                         q=dict(family="default", tau=0.5, w_v=0.3, w_th=2.0, v_threshold=None),
+                         grid=[64, 48, 0.05, [-0.5, 0.25]], z0=[1.1, 1.3], n=1500, steps=8, dt=0.05,
+                         sigma=0.0, seed=11, prefix=[], belief="uniform"),
+        # cfg2 shape (65,536 particles, 4 goals, dt 0.02, 200x200) truncated to 30 steps
+        "cfg2_t30": dict(v=v, theta=th, betas=list(np.geomspace(0.1, 10, 5)),
+                        goals=[[17.0, 10.0], [10.0, 17.0], [3.0, 10.0], [10.0, 3.0]], q=gp,
+                        grid=[200, 200, 0.1, [0.0, 0.0]], z0=[10.0, 10.0], n=65536, steps=30, dt=0.02,
+                        sigma=0.0, seed=2, prefix=[2, 0], belief="posterior"),
+        # the reference's lattice instance (test_prediction.py:32-50)
+        "lattice": dict(v=lat_v, theta=lat_th, betas=[0.5, 2.0], goals=[[8.5, 4.5], [0.5, 4.5]],
+                        q=dict(family="goal_progress", tau=1.0, w_v=0.0, w_th=0.0, v_threshold=None),
+                        grid=[10, 10, 1.0, [0.0, 0.0]], z0=[4.5, 4.5], n=8192, steps=3, dt=1.0,
+                        sigma=0.1, seed=11, prefix=[], belief="uniform"),
+    }
+    return cases
+
+
+def _belief_for(G, space, cs, kind, seed):
+    if kind == "uniform":
+        return G.init_belief(space)
+    r = np.random.default_rng(seed)
+    if kind == "random":
+        return G.JointBelief.from_probs(r.dirichlet(np.ones(space.size)))
+    # posterior after 10 synthetic observations of a Boltzmann walker
+    from gridcast.belief import update_belief
+    b = G.init_belief(space)
+    q = G.q_goal_progress(0.5)
+    goals = space.goals.positions
+    z = G.HumanState(float(np.mean(goals[:, 0])), float(np.mean(goals[:, 1])))
+    for _ in range(10):
+        p = G.boltzmann_policy(z, 10.0, goals[0], cs, q)
+        j = min(int(np.searchsorted(np.cumsum(p), r.random(), side="right")), len(cs) - 1)
+        z2 = G.human_step(z, cs[j], 0.1)
+        b = update_belief(b, z, z2, 0.1, cs, q, space, snap_tol=math.inf)
+        z = z2
+    return b
+
+
+def gen_predict(G):
+    from gridcast.prediction import PredictionConfig, predict, sample_hypotheses, propagate_step, ParticleBatch
+    from oracle import model
+    for name, case in predict_cases().items():
+        cs, space, q, spec = _spec(G, case)
+        b = _belief_for(G, space, cs, case["belief"], 17)
+        cfg = PredictionConfig(n=case["n"], steps=case["steps"], dt=case["dt"],
+                               smoothing_sigma=case["sigma"], seed=case["seed"])
+        pre = tuple(case["prefix"])
+        stack = predict(G.HumanState(*case["z0"]), b, cfg, cs, q, space, spec, prefix=pre)
+        hyp = sample_hypotheses(b, cfg.n, cfg.seed, prefix=pre)
+        # per-step float32 positions through the public propagate_step
+        batch = ParticleBatch.duplicated(G.HumanState(*case["z0"]), hyp)
+        xy_steps = []
+        counts = []
+        from gridcast.occupancy import emplace_counts
+        for t in range(1, cfg.steps + 1):
+            batch = propagate_step(batch, cs, q, space, cfg.dt, cfg.seed, step=t, prefix=pre)
+            xy_steps.append(batch.xy.copy())
+            counts.append(emplace_counts(batch.xy, spec).astype(np.int64))
+        counts = np.stack(counts)
+        nz = np.nonzero(counts)
+        qs = case["q"]
+        tb = model.make_tables(cs.v, cs.theta, cfg.dt,
+                               model.QSpec(qs["family"], qs["tau"], qs["w_v"], qs["w_th"], qs["v_threshold"]))
+        keep_steps = sorted({0, cfg.steps // 2, cfg.steps - 1})
+        payload = dict(
+            meta=json.dumps(case),
+            log_w=b.log_weights,
+            hyp=hyp,
+            count_idx=np.stack(nz, axis=1).astype(np.int32),
+            count_val=counts[nz].astype(np.int32),
+            xy_first=xy_steps[0], xy_last=xy_steps[-1],
+            layer_steps=np.array(keep_steps),
+            layers=stack.layers[keep_steps],
+            layer_sums=stack.layers.sum(axis=(1, 2)),
+            # tables as the reference host computes them (float32), so the GPU box
+            # need not recompute numpy cos/sin
+            sx=tb.sx, sy=tb.sy, at=tb.at, pen=tb.pen, dispx=tb.dispx, dispy=tb.dispy,
+            keep=tb.keep, q_kind=np.int32(tb.q_kind),
+            ref_disp=cs.displacements(cfg.dt).astype(np.float32),
+        )
+        np.savez_compressed(os.path.join(OUT, f"predict_{name}.npz"), **payload)
+        print("predict", name, "nnz", len(nz[0]))
+
+
+def gen_belief(G):
+    from gridcast.belief import update_belief, mask_stationary, ControlSnapMismatch
+    from oracle.model import control_grid
+    v, th = control_grid(4, 24, 1.4)
+    cs = G.ControlSet([G.ControlAction(float(a), float(b)) for a, b in zip(v, th)])
+    r = np.random.default_rng(5)
+    goals = r.uniform(0, 10, (4, 2))
+    space = G.HypothesisSpace(G.RationalitySet.log_spaced(5), G.GoalSet(goals))
+    chains = []
+    specs = [
+        dict(family="goal_progress", tau=0.5, w_v=0.0, w_th=0.0, v_threshold=None),
+        dict(family="goal_progress", tau=0.5, w_v=0.0, w_th=0.0, v_threshold=0.5),
+        dict(family="goal_progress", tau=0.4, w_v=0.1, w_th=0.05, v_threshold=None),
+        dict(family="default", tau=0.5, w_v=1.0, w_th=1.0, v_threshold=None),
+    ]
+    for ci, qsd in enumerate(specs):
+        if qsd["family"] == "goal_progress":
+            q = G.q_goal_progress(qsd["tau"], (qsd["w_v"], qsd["w_th"]))
+        else:
+            q = G.q_default((qsd["w_v"], qsd["w_th"]))
+        if qsd["v_threshold"] is not None:
+            q = mask_stationary(q, cs, qsd["v_threshold"])
+        if ci == 2:
+            lw0 = np.log(r.dirichlet(np.ones(space.size)))
+            lw0[[3, 7]] = -np.inf
+            b = G.JointBelief(lw0 - np.log(np.exp(lw0).sum()))
+        else:
+            b = G.init_belief(space)
+        z = (5.0, 5.0)
+        heading = 0.3
+        rows = []
+        for k in range(30):
+            if k % 7 == 3:
+                zn = z  # stationary observation -> fallback heading
+            elif k % 11 == 5:
+                zn = (z[0] + 0.9, z[1] - 0.4)  # beyond the set: snap mismatch
+            else:
+                zn = (z[0] + r.uniform(-0.15, 0.15), z[1] + r.uniform(-0.15, 0.15))
+            try:
+                nb = update_belief(b, G.HumanState(*z), G.HumanState(*zn), 0.1, cs, q, space,
+                                   fallback_theta=heading)
+                status = 0
+            except ControlSnapMismatch:
+                nb = update_belief(b, G.HumanState(*z), G.HumanState(*zn), 0.1, cs, q, space,
+                                   fallback_theta=heading, snap_tol=math.inf)
+                status = 1
+            rows.append(dict(z=list(z), zn=list(zn), heading=heading, status=status,
+                             prior=b.log_weights.tolist(), post=nb.log_weights.tolist()))
+            if math.hypot(zn[0] - z[0], zn[1] - z[1]) > 1e-9:
+                heading = math.atan2(zn[1] - z[1], zn[0] - z[0])
+            b, z = nb, zn
+        chains.append(dict(q=qsd, rows=rows))
+    np.savez_compressed(os.path.join(OUT, "belief.npz"),
+                        meta=json.dumps(dict(goals=goals.tolist(), betas=list(G.RationalitySet.log_spaced(5).betas),
+                                             dt=0.1, chains=chains)))
+
+
+def gen_smooth(G):
+    from gridcast.occupancy import GridSpec, smooth_values
+    r = np.random.default_rng(9)
+    items = []
+    arrs = []
+    outs = []
+    for (w, h, res, sig) in [(37, 23, 0.1, 0.1), (50, 50, 0.1, 0.15), (16, 40, 0.25, 0.3), (9, 9, 1.0, 0.7), (30, 30, 0.1, 0.0)]:
+        v = r.integers(0, 50, (h, w)).astype(float)
+        v[r.random((h, w)) < 0.6] = 0
+        v /= max(v.sum(), 1.0)
+        spec = GridSpec(w, h, res)
+        items.append([w, h, res, sig])
+        arrs.append(v.ravel())
+        outs.append(smooth_values(v, spec, sig).ravel())
+    np.savez_compressed(os.path.join(OUT, "smooth.npz"), meta=json.dumps(items),
+                        x=np.concatenate(arrs), y=np.concatenate(outs))
+
+
+def gen_multi(G):
+    """sim.py:489-504 pattern: per-human predict with prefix (2, i), union_max, time union."""
+    from gridcast import rng
+    from gridcast.prediction import PredictionConfig, predict
+    from gridcast.occupancy import union_max
+    from oracle.model import control_grid
+    v, th = control_grid(4, 24, 1.4)
+    cs = G.ControlSet([G.ControlAction(float(a), float(b)) for a, b in zip(v, th)])
+    starts = [(3.0, 3.0), (6.0, 3.0), (3.0, 6.0)]
+    humans = []
+    stacks = []
+    seed = rng.derive_seed(0, 7, 4)
+    cfg = PredictionConfig(n=1500, steps=8, dt=0.1, smoothing_sigma=0.1, seed=seed)
+    spec = G.GridSpec(100, 100, 0.1)
+    for i, s in enumerate(starts):
+        goals = np.array([[s[0] + 2.0 * math.cos(a), s[1] + 2.0 * math.sin(a)] for a in (0.0, 1.6, 3.1, 4.7)])
+        space = G.HypothesisSpace(G.RationalitySet.log_spaced(5), G.GoalSet(goals))
+        b = _belief_for(G, space, cs, "random", 100 + i)
+        q = G.q_goal_progress(0.5)
+        st = predict(G.HumanState(*s), b, cfg, cs, q, space, spec, prefix=(2, i))
+        stacks.append(st)
+        humans.append(dict(start=list(s), goals=goals.tolist(), log_w=b.log_weights.tolist()))
+    layers = np.stack([union_max([s.grid(k) for s in stacks]).values for k in range(cfg.steps)])
+    tu = np.maximum.accumulate(layers, axis=0)
+    np.savez_compressed(os.path.join(OUT, "multi.npz"),
+                        meta=json.dumps(dict(humans=humans, seed=str(seed), n=cfg.n, steps=cfg.steps,
+                                             dt=cfg.dt, sigma=cfg.smoothing_sigma)),
+                        union=layers.astype(np.float64), time_union=tu)
+
+
+def gen_exact(G):
+    from gridcast.prediction import exact_predict
+    case = predict_cases()["lattice"]
+    cs, space, q, spec = _spec(G, case)
+    b = G.JointBelief.from_probs([0.35, 0.35, 0.15, 0.15])
+    st = exact_predict(G.HumanState(4.5, 4.5), b, 3, 1.0, cs, q, space, spec)
+    np.savez_compressed(os.path.join(OUT, "exact.npz"), log_w=b.log_weights, layers=st.layers)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    G = _ref()
+    gen_philox(G)
+    gen_exp()
+    gen_predict(G)
+    gen_belief(G)
+    gen_smooth(G)
+    gen_multi(G)
+    gen_exact(G)
+    import platform
+    with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
+        f.write(f"generated by oracle/gen_golden.py from {REF}\n")
+        f.write(f"numpy {np.__version__}; python {platform.python_version()}; {platform.machine()}\n")
+
+
+if __name__ == "__main__":
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    main()

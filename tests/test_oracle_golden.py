@@ -1,0 +1,126 @@
+"""CPU: pin the oracle restatement against the golden vectors of the live reference.
+
+The fixtures (tests/golden/*.npz) were produced by oracle/gen_golden.py from
+/root/reference/pkg/src; these tests need neither the reference nor a GPU.
+"""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+import golden_io
+from oracle import cstep, model, philox
+from oracle import predict as OP
+
+
+def test_philox_streams_match_reference():
+    z = golden_io.load("philox.npz")
+    meta = json.loads(str(z["meta"]))
+    for i, (seed, path) in enumerate(zip(meta["seeds"], meta["paths"])):
+        np.testing.assert_array_equal(philox.stream_random_f32(seed, path, 24), z["f32"][i])
+        np.testing.assert_array_equal(philox.stream_random_f64(seed, path, 12), z["f64"][i])
+        assert philox.derive_seed(seed, *path) == int(meta["derived"][i])
+
+
+def test_numpy_exp_restatement_bit_exact():
+    z = golden_io.load("exp.npz")
+    y = cstep.exp_np_f32(z["x"])
+    assert np.array_equal(y.view(np.uint32), z["y"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", golden_io.predict_case_names())
+def test_tables_match_reference_displacements(name):
+    c = golden_io.PredictCase(name)
+    np.testing.assert_array_equal(np.stack([c.dispx, c.dispy], 1), c.ref_disp)
+    m = c.meta
+    q = m["q"]
+    tb = model.make_tables(m["v"], m["theta"], c.dt,
+                           model.QSpec(q["family"], q["tau"], q["w_v"], q["w_th"], q["v_threshold"]))
+    for k in ("sx", "sy", "at", "pen", "dispx", "dispy", "keep"):
+        np.testing.assert_array_equal(getattr(tb, k), getattr(c, k))
+
+
+@pytest.mark.parametrize("name", golden_io.predict_case_names())
+def test_oracle_predict_bit_exact(name):
+    c = golden_io.PredictCase(name)
+    if c.n * c.steps > 400_000:
+        pytest.skip("large case covered by test_oracle_predict_positions")
+    W, H, res, org = c.grid
+    out = OP.predict(c.z0, c.log_w, c.n, c.steps, c.dt, c.sigma, c.seed, c.tables(),
+                     c.beta_of, c.goal_xy_of, OP.Grid(W, H, res, org), prefix=c.prefix, keep_xy=True)
+    np.testing.assert_array_equal(out["hyp"], c.hyp)
+    np.testing.assert_array_equal(out["counts"], c.counts())
+    np.testing.assert_array_equal(out["xy"][0], c.xy_first)
+    np.testing.assert_array_equal(out["xy"][-1], c.xy_last)
+    np.testing.assert_array_equal(out["layers"][c.layer_steps], c.layers)
+
+
+def test_oracle_predict_positions_cfg2():
+    c = golden_io.PredictCase("cfg2_t30")
+    W, H, res, org = c.grid
+    out = OP.predict(c.z0, c.log_w, c.n, c.steps, c.dt, c.sigma, c.seed, c.tables(),
+                     c.beta_of, c.goal_xy_of, OP.Grid(W, H, res, org), prefix=c.prefix, keep_xy=True)
+    np.testing.assert_array_equal(out["counts"], c.counts())
+    np.testing.assert_array_equal(out["xy"][-1], c.xy_last)
+
+
+def test_unsmoothed_layers_are_counts_over_n():
+    c = golden_io.PredictCase("cfg1_s0")
+    cnt = c.counts()
+    np.testing.assert_array_equal(cnt[c.layer_steps].astype(float) / c.n, c.layers)
+
+
+def test_smoothing_restatements():
+    z = golden_io.load("smooth.npz")
+    items = json.loads(str(z["meta"]))
+    off = 0
+    for w, h, res, sig in items:
+        x = z["x"][off:off + w * h].reshape(h, w)
+        y = z["y"][off:off + w * h].reshape(h, w)
+        off += w * h
+        g = OP.Grid(w, h, res)
+        np.testing.assert_array_equal(OP.smooth_dense(x, g, sig), y)
+        np.testing.assert_allclose(OP.smooth_banded(x, g, sig), y, rtol=0, atol=1e-15)
+
+
+def test_belief_chains():
+    z = golden_io.load("belief.npz")
+    meta = json.loads(str(z["meta"]))
+    v, th = model.control_grid(4, 24, 1.4)
+    beta_of, goal_xy_of = model.hypothesis_tables(meta["betas"], meta["goals"])
+    for chain in meta["chains"]:
+        qd = chain["q"]
+        qs = model.QSpec(qd["family"], qd["tau"], qd["w_v"], qd["w_th"], qd["v_threshold"])
+        for row in chain["rows"]:
+            prior = np.array(row["prior"])
+            tol = None
+            if row["status"] == 1:
+                with pytest.raises(ValueError):
+                    OP.belief_update(prior, row["z"], row["zn"], meta["dt"], v, th, qs,
+                                     beta_of, goal_xy_of, row["heading"])
+                tol = math.inf
+            post, _ = OP.belief_update(prior, row["z"], row["zn"], meta["dt"], v, th, qs,
+                                       beta_of, goal_xy_of, row["heading"], snap_tol=tol)
+            ref = np.array(row["post"])
+            fin = np.isfinite(ref)
+            np.testing.assert_array_equal(np.isfinite(post), fin)
+            np.testing.assert_allclose(post[fin], ref[fin], rtol=1e-12, atol=1e-12)
+
+
+def test_multi_union_and_time_union():
+    z = golden_io.load("multi.npz")
+    meta = json.loads(str(z["meta"]))
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, meta["dt"], model.QSpec())
+    stacks = []
+    for i, hm in enumerate(meta["humans"]):
+        beta_of, goal_xy_of = model.hypothesis_tables(np.geomspace(0.1, 10, 5), hm["goals"])
+        out = OP.predict(hm["start"], np.array(hm["log_w"]), meta["n"], meta["steps"], meta["dt"],
+                         meta["sigma"], int(meta["seed"]), tb, beta_of, goal_xy_of,
+                         OP.Grid(100, 100, 0.1), prefix=(2, i))
+        stacks.append(out["layers"])
+    u = OP.union_max(stacks)
+    np.testing.assert_array_equal(u, z["union"])
+    np.testing.assert_array_equal(OP.time_union(u), z["time_union"])
