@@ -1,0 +1,213 @@
+/*
+ * gridcast_b200 -- C ABI of the B200-native particle predictor (sm_100a).
+ *
+ * Drop-in boundary for the reference package `gridcast` (arXiv 2603.01122).  The
+ * reference has no FFI (it is pure Python/NumPy); its GPU seam is the contract of
+ * SPEC.md:273-281 ("GPU backends can be added behind the same contract": chunk-keyed
+ * counter RNG, disjoint outputs, bitwise determinism for any worker count).  Each entry
+ * point below replaces one reference function; the Python host mirror
+ * (paper_2603_01122_b200/) binds them with ctypes under the reference's own names.
+ *
+ * Conventions
+ *   - every pointer named d_* is DEVICE memory owned by the caller; h_* is host memory;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, passed as void*) and does
+ *     not synchronise unless documented;
+ *   - no torch / numpy types cross this boundary: plain pointers, sizes, PODs;
+ *   - errors: a gc_status is returned and gc_last_error() holds a message (thread-local).
+ */
+#ifndef GRIDCAST_B200_H
+#define GRIDCAST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GC_ABI_VERSION 1
+
+typedef enum {
+    GC_OK = 0,
+    GC_BAD_ARG = 1,            /* ValueError */
+    GC_EMPTY_CONTROL_SET = 2,  /* agents.EmptyControlSetError (agents.py:20-21) */
+    GC_SNAP_MISMATCH = 3,      /* belief.ControlSnapMismatch (belief.py:35-36) */
+    GC_UNSUPPORTED_Q = 4,      /* utility family the kernels do not implement */
+    GC_CUDA_ERROR = 5,         /* RuntimeError */
+    GC_WINDOW_OVERFLOW = 6     /* a particle left its reachable-cell window (internal bug) */
+} gc_status;
+
+/* Utility families (agents.py:245-296).  *_FULL = the reference's `base` (with the
+ * row-constant -|rel|^2), used when a stationary mask dropped base_policy (belief.py:222). */
+enum { GC_Q_GOAL_PROGRESS = 0, GC_Q_GOAL_PROGRESS_FULL = 1, GC_Q_DEFAULT = 2, GC_Q_TABLE = 3 };
+
+/* Random-number modes of gc_predict.
+ *   GC_RNG_REFERENCE : regenerate the reference's own numpy Philox4x64-10 streams
+ *                      in-register (rng.py:27-31, prediction.py:128-131, :190-192) and run
+ *                      the float32 per-action step op-for-op (prediction.py:147-162)
+ *                      -> counts bit-identical to the reference;
+ *   GC_RNG_UNIFORMS  : same arithmetic, uniforms supplied by the caller (d_uniforms,
+ *                      d_hyp_u) e.g. drawn by the reference itself;
+ *   GC_RNG_PRODUCTION: Philox4x32-10 in-register + exact-in-distribution factorised
+ *                      sampler (one exp per heading) -- the fast path. */
+enum { GC_RNG_REFERENCE = 0, GC_RNG_UNIFORMS = 1, GC_RNG_PRODUCTION = 2 };
+
+/* Per-action table of one control set + utility (prediction.py:134-144, agents.py:275-294).
+ * All arrays have length m (the FULL control set); keep lists the unmasked indices. */
+typedef struct {
+    int32_t m;
+    int32_t m_keep;
+    int32_t q_kind;            /* GC_Q_* */
+    int32_t _pad;
+    const float *d_sx, *d_sy;  /* float32 step_x*tau, step_y*tau (agents.py:279-280) */
+    const float *d_at;         /* float32 action term incl. weights (agents.py:284-287) */
+    const float *d_pen;        /* float32 q_default penalty (agents.py:256) */
+    const float *d_dispx, *d_dispy; /* float32 displacements (agents.py:108-112 -> f32) */
+    const int32_t *d_keep;     /* (m_keep,) */
+    /* production factorised sampler (valid when n_speeds > 0): action (a, b) with
+     * a in [0, n_speeds), b in [0, n_headings) has index a_index[a*n_headings+b] in the
+     * full set, speed a*dv and heading theta_b. */
+    int32_t n_speeds, n_headings;
+    float dv, tau, w_v, w_th;
+    const float *d_cos_h, *d_sin_h, *d_theta_h; /* (n_headings,) */
+    const int32_t *d_a_index;                   /* (n_speeds*n_headings,) or NULL */
+} gc_action_table;
+
+/* Batched Alg. 1 (prediction.py:223-255, sim.py:489-499): every human h of the batch
+ * samples n hypotheses from its belief and propagates n particles for `steps` steps;
+ * per-step particle counts land in that human's windowed count buffer. */
+typedef struct {
+    int32_t n_humans;
+    int32_t n;                 /* particles per human */
+    int32_t steps;             /* horizon T */
+    int32_t rng_mode;          /* GC_RNG_* */
+    int32_t grid_w, grid_h;
+    float origin_x32, origin_y32, res32; /* GridSpec pre-cast to float32 (NEP 50) */
+    const float *d_start_xy;   /* (n_humans, 2) float32 start positions */
+    /* hypotheses: human h owns rows [d_hyp_off[h], d_hyp_off[h+1]) */
+    const int32_t *d_hyp_off;
+    const float *d_beta32;     /* (sum |H|,) */
+    const float *d_goal32;     /* (sum |H|, 2) */
+    const double *d_cdf;       /* (sum |H|,) host-built cdf (prediction.py:128-129) or NULL */
+    const double *d_log_w;     /* (sum |H|,) device posterior, used when d_cdf == NULL */
+    /* reference RNG: seed + path prefix per human (rng.stream(seed, *prefix, ...)) */
+    const uint64_t *d_seed;    /* (n_humans,) */
+    const uint32_t *d_prefix;  /* (n_humans, 4) */
+    const int32_t *d_prefix_len; /* (n_humans,) 0..4 */
+    /* GC_RNG_UNIFORMS inputs */
+    const float *d_uniforms;   /* (n_humans, steps, n) float32 or NULL */
+    const double *d_hyp_u;     /* (n_humans, n) float64 or NULL */
+    const int32_t *d_hyp_in;   /* (n_humans, n) explicit hypothesis indices or NULL */
+    /* action tables: human h uses tables[d_table_id[h]] */
+    const gc_action_table *h_tables; /* host array of n_tables */
+    int32_t n_tables;
+    const int32_t *d_table_id; /* (n_humans,) */
+    /* Reachable-cell windows.  Step t (0-based) of human h covers the cells within
+     * d_step_r[t] of the human's start cell (clamped to the grid); its counts live at
+     * d_counts + h*human_stride + d_step_off[t], row-major with row length
+     * (clamped) window width.  Counts must be zero on entry. */
+    const int32_t *d_step_r;   /* (steps,) */
+    const int64_t *d_step_off; /* (steps,) */
+    int64_t human_stride;
+    int32_t max_win_cells;     /* max_t (2 r_t + 1)^2 */
+    int32_t _pad2;
+    uint32_t *d_counts;
+    /* optional outputs */
+    int32_t *d_hyp_out;        /* (n_humans, n) sampled hypothesis indices or NULL */
+    float *d_xy_out;           /* (n_humans, n, 2) final positions or NULL */
+    uint32_t *d_error;         /* device status word (GC_WINDOW_OVERFLOW bit) or NULL */
+} gc_predict_args;
+
+/* Occupancy epilogue (prediction.py:251-254, occupancy.py:139-154, :162-192,
+ * sim.py:500-504): windowed counts -> counts/n -> truncated-Gaussian smoothing with
+ * edge-normalised columns -> per-human layers and/or the cell-wise max union. */
+typedef struct {
+    int32_t n_humans, n, steps;
+    int32_t grid_w, grid_h;
+    int32_t radius;            /* ceil(3 sigma_cells); 0 = no smoothing */
+    const double *d_kernel;    /* (2*radius+1,) exp(-0.5 (o/sigma_cells)^2) */
+    const double *d_zx;        /* (grid_w,) in-grid kernel mass per source column */
+    const double *d_zy;        /* (grid_h,) */
+    float origin_x32, origin_y32, res32;
+    int32_t n_tiles;           /* tiles per human (static geometry) */
+    const float *d_start_xy;   /* (n_humans, 2) float32 start positions */
+    const int32_t *d_step_r;
+    const int64_t *d_step_off;
+    int64_t human_stride;
+    const int32_t *d_tiles;    /* (n_tiles, 4): t, tile_x, tile_y, 0 (32x32 output tiles
+                                  over the window grown by radius) */
+    const uint32_t *d_counts;
+    double *d_layers64;        /* (n_humans, steps, H, W) zero-filled, or NULL */
+    float *d_union32;          /* (steps, H, W) zero-filled max-union (float32) or NULL */
+    double *d_union64;         /* (steps, H, W) zero-filled max-union (float64) or NULL */
+    int32_t time_union;        /* running max over t of the union (sim.py:503-504) */
+} gc_epilogue_args;
+
+/* Observation update of every human's joint belief (belief.py:159-198), one warp per
+ * human: recover_control (agents.py:355-371) -> snap (agents.py:114-120) -> log-policy
+ * (agents.py:299-323) -> prior + loglik, floor -745, -inf kept -> logsumexp normalise. */
+typedef struct {
+    int32_t n_humans;
+    int32_t m;
+    const double *d_v, *d_theta;      /* (m,) control set rows */
+    const double *d_sx, *d_sy, *d_at; /* (m,) float64 goal-progress tables */
+    const double *d_pen;              /* (m,) float64 q_default penalty */
+    const uint8_t *d_masked;          /* (m,) 1 = masked, or NULL */
+    int32_t q_kind;                   /* GC_Q_GOAL_PROGRESS(_FULL) / GC_Q_DEFAULT / GC_Q_TABLE */
+    const double *d_qtable;           /* GC_Q_TABLE: (sum |H|, m) q.table at z_t per human */
+    const int32_t *d_hyp_off;         /* (n_humans+1,) */
+    const double *d_beta, *d_goal;    /* (sum |H|,), (sum |H|, 2) float64 */
+    const double *d_obs;              /* (n_humans, 4): z_t.x, z_t.y, z_next.x, z_next.y */
+    const double *d_fallback_theta;   /* (n_humans,) */
+    double dt;
+    double snap_tol;                  /* +inf disables ControlSnapMismatch */
+    int32_t clamp_on_mismatch;        /* 1: update with the nearest action anyway (sim.py:469-478) */
+    const double *d_prior;            /* (sum |H|,) log weights */
+    double *d_post;                   /* (sum |H|,) log weights (may alias d_prior) */
+    int32_t *d_status;                /* (n_humans,) GC_OK / GC_SNAP_MISMATCH */
+    int32_t *d_action;                /* (n_humans,) snapped action index or NULL */
+} gc_belief_args;
+
+gc_status gc_predict(const gc_predict_args *args, void *stream);
+gc_status gc_grid_epilogue(const gc_epilogue_args *args, void *stream);
+gc_status gc_belief_update(const gc_belief_args *args, void *stream);
+
+/* One propagate_step (prediction.py:165-211) of an explicit particle batch in reference
+ * arithmetic: d_xy (n,2) f32 in/out, d_hyp (n,), hypothesis tables of ONE human,
+ * uniforms either supplied (d_u01, n) or regenerated from (seed, prefix, step). */
+gc_status gc_propagate_step(float *d_xy, const int32_t *d_hyp, int32_t n,
+                            const float *d_beta32, const float *d_goal32, int32_t n_hyp,
+                            const gc_action_table *h_table, const float *d_u01,
+                            uint64_t seed, const uint32_t *h_prefix, int32_t prefix_len,
+                            int32_t step, void *stream);
+
+/* sample_hypotheses (prediction.py:124-131) with the reference stream: d_out (n,) int32. */
+gc_status gc_sample_hypotheses(const double *d_cdf, int32_t n_hyp, int32_t n, uint64_t seed,
+                               const uint32_t *h_prefix, int32_t prefix_len, int32_t *d_out,
+                               void *stream);
+
+/* emplace_counts (occupancy.py:105-109): accumulate d_xy (n,2) float32 particles into
+ * d_counts (H*W) uint32, float32 cell arithmetic + edge clamping (occupancy.py:43-51). */
+gc_status gc_emplace_counts(const float *d_xy, int64_t n, int32_t grid_w, int32_t grid_h,
+                            float origin_x32, float origin_y32, float res32, uint32_t *d_counts,
+                            void *stream);
+
+/* smooth_values (occupancy.py:139-154) on n_layers float64 (H, W) layers, d_in != d_out. */
+gc_status gc_smooth_layers(const double *d_in, double *d_out, int32_t n_layers, int32_t grid_w,
+                           int32_t grid_h, int32_t radius, const double *d_kernel,
+                           const double *d_zx, const double *d_zy, void *stream);
+
+/* rng.derive_seed (rng.py:34-39): SeedSequence(seed, path).generate_state(2,u64) xor-folded. */
+uint64_t gc_derive_seed(uint64_t seed, const uint32_t *h_path, int32_t path_len);
+
+/* Fill h_out[0..n) with rng.stream(seed, *path).random(n, float32) (host, for tests/tools). */
+void gc_stream_f32(uint64_t seed, const uint32_t *h_path, int32_t path_len, float *h_out, int64_t n);
+
+const char *gc_last_error(void);
+int32_t gc_abi_version(void);
+/* Number of kernel launches issued through this library since load (for bench claims). */
+uint64_t gc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRIDCAST_B200_H */

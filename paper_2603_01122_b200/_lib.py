@@ -1,0 +1,155 @@
+"""ctypes binding of the C ABI in include/gridcast_b200.h (libgridcast_b200.so).
+
+The library is built in-tree (``python -m paper_2603_01122_b200.build`` or
+``__graft_entry__.build()``) into ``paper_2603_01122_b200/_lib/``.  There is no CPU
+fallback: every product entry point calls :func:`lib` and fails loudly when the
+shared library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libgridcast_b200.so")
+
+GC_OK = 0
+GC_BAD_ARG = 1
+GC_EMPTY_CONTROL_SET = 2
+GC_SNAP_MISMATCH = 3
+GC_UNSUPPORTED_Q = 4
+GC_CUDA_ERROR = 5
+GC_WINDOW_OVERFLOW = 6
+
+GC_Q_GOAL_PROGRESS = 0
+GC_Q_GOAL_PROGRESS_FULL = 1
+GC_Q_DEFAULT = 2
+GC_Q_TABLE = 3
+
+GC_RNG_REFERENCE = 0
+GC_RNG_UNIFORMS = 1
+GC_RNG_PRODUCTION = 2
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+U64 = ctypes.c_uint64
+F32 = ctypes.c_float
+F64 = ctypes.c_double
+
+
+class ActionTable(ctypes.Structure):
+    _fields_ = [
+        ("m", I32), ("m_keep", I32), ("q_kind", I32), ("_pad", I32),
+        ("d_sx", P), ("d_sy", P), ("d_at", P), ("d_pen", P), ("d_dispx", P), ("d_dispy", P),
+        ("d_keep", P),
+        ("n_speeds", I32), ("n_headings", I32),
+        ("dv", F32), ("tau", F32), ("w_v", F32), ("w_th", F32),
+        ("d_cos_h", P), ("d_sin_h", P), ("d_theta_h", P), ("d_a_index", P),
+    ]
+
+
+class PredictArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_humans", I32), ("n", I32), ("steps", I32), ("rng_mode", I32),
+        ("grid_w", I32), ("grid_h", I32),
+        ("origin_x32", F32), ("origin_y32", F32), ("res32", F32),
+        ("d_start_xy", P), ("d_hyp_off", P), ("d_beta32", P), ("d_goal32", P),
+        ("d_cdf", P), ("d_log_w", P),
+        ("d_seed", P), ("d_prefix", P), ("d_prefix_len", P),
+        ("d_uniforms", P), ("d_hyp_u", P), ("d_hyp_in", P),
+        ("h_tables", ctypes.POINTER(ActionTable)), ("n_tables", I32), ("d_table_id", P),
+        ("d_step_r", P), ("d_step_off", P), ("human_stride", I64),
+        ("max_win_cells", I32), ("_pad2", I32), ("d_counts", P),
+        ("d_hyp_out", P), ("d_xy_out", P), ("d_error", P),
+    ]
+
+
+class EpilogueArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_humans", I32), ("n", I32), ("steps", I32),
+        ("grid_w", I32), ("grid_h", I32), ("radius", I32),
+        ("d_kernel", P), ("d_zx", P), ("d_zy", P),
+        ("origin_x32", F32), ("origin_y32", F32), ("res32", F32), ("n_tiles", I32),
+        ("d_start_xy", P), ("d_step_r", P), ("d_step_off", P), ("human_stride", I64),
+        ("d_tiles", P), ("d_counts", P),
+        ("d_layers64", P), ("d_union32", P), ("d_union64", P), ("time_union", I32),
+    ]
+
+
+class BeliefArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_humans", I32), ("m", I32),
+        ("d_v", P), ("d_theta", P), ("d_sx", P), ("d_sy", P), ("d_at", P), ("d_pen", P),
+        ("d_masked", P), ("q_kind", I32), ("d_qtable", P), ("d_hyp_off", P),
+        ("d_beta", P), ("d_goal", P), ("d_obs", P), ("d_fallback_theta", P),
+        ("dt", F64), ("snap_tol", F64), ("clamp_on_mismatch", I32),
+        ("d_prior", P), ("d_post", P), ("d_status", P), ("d_action", P),
+    ]
+
+
+EXPORTS = (
+    "gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
+    "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
+    "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
+)
+
+_lib = None
+
+
+class GridcastLibraryMissing(RuntimeError):
+    """The sm_100a shared library has not been built (no CPU fallback exists)."""
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise GridcastLibraryMissing(
+            f"{LIB_PATH} not found; build it with `python -m paper_2603_01122_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.gc_predict.argtypes = [ctypes.POINTER(PredictArgs), P]
+    L.gc_grid_epilogue.argtypes = [ctypes.POINTER(EpilogueArgs), P]
+    L.gc_belief_update.argtypes = [ctypes.POINTER(BeliefArgs), P]
+    L.gc_propagate_step.argtypes = [P, P, I32, P, P, I32, ctypes.POINTER(ActionTable), P, U64, P,
+                                    I32, I32, P]
+    L.gc_sample_hypotheses.argtypes = [P, I32, I32, U64, P, I32, P, P]
+    L.gc_emplace_counts.argtypes = [P, I64, I32, I32, F32, F32, F32, P, P]
+    L.gc_smooth_layers.argtypes = [P, P, I32, I32, I32, I32, P, P, P, P]
+    for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
+               "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers"):
+        getattr(L, fn).restype = ctypes.c_int
+    L.gc_derive_seed.argtypes = [U64, P, I32]
+    L.gc_derive_seed.restype = U64
+    L.gc_stream_f32.argtypes = [U64, P, I32, P, I64]
+    L.gc_stream_f32.restype = None
+    L.gc_last_error.restype = ctypes.c_char_p
+    L.gc_abi_version.restype = I32
+    L.gc_launch_count.restype = U64
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().gc_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str = ""):
+    """Map a gc_status onto the reference's exception classes."""
+    if status == GC_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if status == GC_EMPTY_CONTROL_SET:
+        from .agents import EmptyControlSetError
+        raise EmptyControlSetError(msg)
+    if status == GC_SNAP_MISMATCH:
+        from .belief import ControlSnapMismatch
+        raise ControlSnapMismatch(msg)
+    if status == GC_UNSUPPORTED_Q:
+        raise NotImplementedError(msg)
+    if status == GC_BAD_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(msg)

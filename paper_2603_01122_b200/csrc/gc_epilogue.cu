@@ -1,0 +1,247 @@
+// gc_epilogue.cu -- K3: occupancy epilogue.
+//
+// Windowed u32 counts -> layer values counts/n (float64, one IEEE division exactly as
+// prediction.py:251) -> truncated Gaussian smoothing with edge-normalised columns
+// (occupancy.py:122-154) applied as a banded separable stencil (SURVEY.md App. A.5:
+// pre-divide each source cell by its in-grid kernel mass Z, then a plain
+// (2R+1)-tap convolution along y then x) -> per-human float64 layers (the reference
+// (T, H, W) layout) and/or the cell-wise max union of all humans (occupancy.py:162-192,
+// sim.py:500-502) via order-independent atomicMax on the IEEE bits of non-negative
+// values.  A second kernel applies the conservative time union (sim.py:503-504).
+//
+// The reference rescales each smoothed layer by before/after sums; the banded operator
+// conserves mass exactly in real arithmetic, so that rescale only corrects rounding
+// (<= 1e-16 relative) and is omitted: parity tests bound the difference at 1e-15 abs.
+#include "gc_common.cuh"
+#include "gc_internal.h"
+
+namespace gc {
+
+constexpr int ET = 32;    // output tile edge
+constexpr int ENT = 256;  // threads per CTA
+constexpr int MAXRAD = 16;
+
+struct EParams {
+    int n_humans, n, steps, grid_w, grid_h, radius, n_tiles, time_union;
+    float ox, oy, res;
+    const double *kernel, *zx, *zy;
+    const float *start_xy;
+    const int *step_r;
+    const long long *step_off;
+    long long human_stride;
+    const int4 *tiles;
+    const unsigned *counts;
+    double *layers64;
+    float *union32;
+    double *union64;
+};
+
+__device__ __forceinline__ void cell_of_start(float x, float y, const EParams &P, int &ix, int &iy) {
+    const float fx = floorf(__fdiv_rn(__fsub_rn(x, P.ox), P.res));
+    const float fy = floorf(__fdiv_rn(__fsub_rn(y, P.oy), P.res));
+    ix = fx < 0.f ? 0 : (fx > (float)(P.grid_w - 1) ? P.grid_w - 1 : (int)fx);
+    iy = fy < 0.f ? 0 : (fy > (float)(P.grid_h - 1) ? P.grid_h - 1 : (int)fy);
+}
+
+__global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
+    extern __shared__ __align__(16) double esm[];
+    const int h = blockIdx.y;
+    const int4 tl = P.tiles[blockIdx.x];
+    const int t = tl.x;
+    const int rad = P.radius;
+    const int E = ET + 2 * rad;
+    double *vin = esm;            // E x E
+    double *vmid = esm + E * E;   // ET x E
+    __shared__ double kern[2 * MAXRAD + 1];
+
+    int cx, cy;
+    cell_of_start(__ldg(&P.start_xy[2 * h]), __ldg(&P.start_xy[2 * h + 1]), P, cx, cy);
+    const int R = __ldg(&P.step_r[t]);
+    const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
+    const int y0 = max(0, cy - R), y1 = min(P.grid_h - 1, cy + R);
+    const int ww = x1 - x0 + 1;
+    // tile origin in grid coordinates (tile grid anchored at the unclamped grown window)
+    const int X0 = cx - R - rad + tl.y * ET, Y0 = cy - R - rad + tl.z * ET;
+    // whole tile outside the grown, clamped window or the grid -> nothing to do
+    if (X0 > min(P.grid_w - 1, x1 + rad) || X0 + ET - 1 < max(0, x0 - rad) ||
+        Y0 > min(P.grid_h - 1, y1 + rad) || Y0 + ET - 1 < max(0, y0 - rad))
+        return;
+    const unsigned *cnt = P.counts + (long long)h * P.human_stride + __ldg(&P.step_off[t]);
+    const double inv_n = 1.0 / (double)P.n;  // only used for smoothing (see below)
+    (void)inv_n;
+    for (int i = threadIdx.x; i < 2 * rad + 1; i += ENT) kern[i] = P.kernel[i];
+
+    // load inputs (counts/n, pre-divided by the source cell's in-grid kernel masses)
+    for (int i = threadIdx.x; i < E * E; i += ENT) {
+        const int ly = i / E, lx = i - ly * E;
+        const int X = X0 - rad + lx, Y = Y0 - rad + ly;
+        double v = 0.0;
+        if (X >= x0 && X <= x1 && Y >= y0 && Y <= y1) {
+            const unsigned c = __ldg(&cnt[(Y - y0) * ww + (X - x0)]);
+            if (c) {
+                v = (double)c / (double)P.n;  // exactly the reference's counts / n
+                if (rad > 0) v = v / __ldg(&P.zy[Y]) / __ldg(&P.zx[X]);
+            }
+        }
+        vin[i] = v;
+    }
+    __syncthreads();
+    if (rad > 0) {
+        // pass along y: vmid[yy][lx] = sum_o k[o] vin[yy + rad - o][lx]
+        for (int i = threadIdx.x; i < ET * E; i += ENT) {
+            const int yy = i / E, lx = i - yy * E;
+            double s = 0.0;
+            for (int o = -rad; o <= rad; ++o) s = fma(kern[o + rad], vin[(yy + rad - o) * E + lx], s);
+            vmid[i] = s;
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < ET * ET; i += ENT) {
+        const int yy = i / ET, xx = i - yy * ET;
+        const int X = X0 + xx, Y = Y0 + yy;
+        if (X < 0 || X >= P.grid_w || Y < 0 || Y >= P.grid_h) continue;
+        double v;
+        if (rad > 0) {
+            double s = 0.0;
+            for (int o = -rad; o <= rad; ++o) s = fma(kern[o + rad], vmid[yy * E + (xx + rad - o)], s);
+            v = s > 0.0 ? s : 0.0;  // np.maximum(out, 0) (occupancy.py:153)
+        } else {
+            v = vin[(yy + rad) * E + (xx + rad)];
+        }
+        const long long cell = (long long)Y * P.grid_w + X;
+        if (P.layers64) P.layers64[((long long)h * P.steps + t) * P.grid_h * P.grid_w + cell] = v;
+        if (v > 0.0) {
+            const long long o = (long long)t * P.grid_h * P.grid_w + cell;
+            if (P.union32) atomicMax(reinterpret_cast<unsigned *>(P.union32) + o, __float_as_uint((float)v));
+            if (P.union64)
+                atomicMax(reinterpret_cast<unsigned long long *>(P.union64) + o,
+                          (unsigned long long)__double_as_longlong(v));
+        }
+    }
+}
+
+// conservative time union: layer t <- max over t' <= t (np.maximum.accumulate, axis 0)
+template <typename Tv>
+__global__ void k_time_union(Tv *u, int steps, long long cells) {
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    Tv run = u[c];
+    for (int t = 1; t < steps; ++t) {
+        const long long o = (long long)t * cells + c;
+        const Tv v = u[o];
+        if (v < run) u[o] = run; else run = v;
+    }
+}
+
+// ---- standalone smooth_values (occupancy.py:139-154) over full float64 layers -------
+__global__ void __launch_bounds__(ENT) k_smooth(const double *in, double *out, int W, int H, int rad,
+                                                const double *kernel, const double *zx, const double *zy) {
+    extern __shared__ __align__(16) double ssm[];
+    const int E = ET + 2 * rad;
+    double *vin = ssm, *vmid = ssm + E * E;
+    const int L = blockIdx.z;
+    const int X0 = blockIdx.x * ET, Y0 = blockIdx.y * ET;
+    const double *src = in + (long long)L * W * H;
+    for (int i = threadIdx.x; i < E * E; i += ENT) {
+        const int ly = i / E, lx = i - ly * E;
+        const int X = X0 - rad + lx, Y = Y0 - rad + ly;
+        double v = 0.0;
+        if (X >= 0 && X < W && Y >= 0 && Y < H) v = src[(long long)Y * W + X] / zy[Y] / zx[X];
+        vin[i] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ET * E; i += ENT) {
+        const int yy = i / E, lx = i - yy * E;
+        double s = 0.0;
+        for (int o = -rad; o <= rad; ++o) s = fma(kernel[o + rad], vin[(yy + rad - o) * E + lx], s);
+        vmid[i] = s;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ET * ET; i += ENT) {
+        const int yy = i / ET, xx = i - yy * ET;
+        const int X = X0 + xx, Y = Y0 + yy;
+        if (X >= W || Y >= H) continue;
+        double s = 0.0;
+        for (int o = -rad; o <= rad; ++o) s = fma(kernel[o + rad], vmid[yy * E + (xx + rad - o)], s);
+        out[(long long)L * W * H + (long long)Y * W + X] = s > 0.0 ? s : 0.0;
+    }
+}
+
+// ---- standalone emplace_counts (occupancy.py:105-109) ---------------------------------
+__global__ void k_emplace(const float *xy, long long n, int W, int H, float ox, float oy, float res,
+                          unsigned *counts) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float fx = floorf(__fdiv_rn(__fsub_rn(xy[2 * i], ox), res));
+    const float fy = floorf(__fdiv_rn(__fsub_rn(xy[2 * i + 1], oy), res));
+    const int ix = fx < 0.f ? 0 : (fx > (float)(W - 1) ? W - 1 : (int)fx);
+    const int iy = fy < 0.f ? 0 : (fy > (float)(H - 1) ? H - 1 : (int)fy);
+    atomicAdd(&counts[(long long)iy * W + ix], 1u);
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" gc_status gc_emplace_counts(const float *d_xy, int64_t n, int32_t grid_w, int32_t grid_h,
+                                       float origin_x32, float origin_y32, float res32, uint32_t *d_counts,
+                                       void *stream) {
+    GC_CHECK_ARG(d_xy && d_counts && n >= 1 && grid_w >= 1 && grid_h >= 1 && res32 > 0.f,
+                 "gc_emplace_counts: bad args");
+    k_emplace<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_xy, n, grid_w, grid_h, origin_x32,
+                                                                            origin_y32, res32, d_counts);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_emplace launch");
+}
+
+extern "C" gc_status gc_smooth_layers(const double *d_in, double *d_out, int32_t n_layers, int32_t grid_w,
+                                      int32_t grid_h, int32_t radius, const double *d_kernel, const double *d_zx,
+                                      const double *d_zy, void *stream) {
+    GC_CHECK_ARG(d_in && d_out && d_in != d_out && n_layers >= 1 && grid_w >= 1 && grid_h >= 1,
+                 "gc_smooth_layers: bad args");
+    GC_CHECK_ARG(radius >= 1 && radius <= MAXRAD && d_kernel && d_zx && d_zy, "gc_smooth_layers: radius 1..%d", MAXRAD);
+    GC_CHECK_ARG(n_layers <= 65535, "gc_smooth_layers: too many layers");
+    const int E = ET + 2 * radius;
+    const size_t smem = (size_t)(E * E + ET * E) * sizeof(double);
+    if (smem > 48 * 1024)
+        GC_CUDA(cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((grid_w + ET - 1) / ET, (grid_h + ET - 1) / ET, n_layers);
+    k_smooth<<<grid, ENT, smem, (cudaStream_t)stream>>>(d_in, d_out, grid_w, grid_h, radius, d_kernel, d_zx, d_zy);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_smooth launch");
+}
+
+extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
+    GC_CHECK_ARG(a != nullptr, "gc_grid_epilogue: null args");
+    GC_CHECK_ARG(a->n_humans >= 1 && a->n >= 1 && a->steps >= 1, "gc_grid_epilogue: bad sizes");
+    GC_CHECK_ARG(a->radius >= 0 && a->radius <= MAXRAD, "gc_grid_epilogue: smoothing radius 0..%d cells", MAXRAD);
+    GC_CHECK_ARG(a->radius == 0 || (a->d_kernel && a->d_zx && a->d_zy), "gc_grid_epilogue: missing kernel tables");
+    GC_CHECK_ARG(a->d_tiles && a->n_tiles >= 1 && a->d_counts && a->d_start_xy && a->d_step_r && a->d_step_off,
+                 "gc_grid_epilogue: missing geometry buffers");
+    GC_CHECK_ARG(a->n_humans <= 65535, "gc_grid_epilogue: too many humans");
+    EParams P;
+    P.n_humans = a->n_humans; P.n = a->n; P.steps = a->steps; P.grid_w = a->grid_w; P.grid_h = a->grid_h;
+    P.radius = a->radius; P.n_tiles = a->n_tiles; P.time_union = a->time_union;
+    P.ox = a->origin_x32; P.oy = a->origin_y32; P.res = a->res32;
+    P.kernel = a->d_kernel; P.zx = a->d_zx; P.zy = a->d_zy;
+    P.start_xy = a->d_start_xy; P.step_r = a->d_step_r; P.step_off = (const long long *)a->d_step_off;
+    P.human_stride = a->human_stride; P.tiles = (const int4 *)a->d_tiles; P.counts = a->d_counts;
+    P.layers64 = a->d_layers64; P.union32 = a->d_union32; P.union64 = a->d_union64;
+    const int E = ET + 2 * a->radius;
+    const size_t smem = (size_t)(E * E + (a->radius > 0 ? ET * E : 0)) * sizeof(double);
+    if (smem > 48 * 1024)
+        GC_CUDA(cudaFuncSetAttribute(k_epilogue, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaStream_t st = (cudaStream_t)stream;
+    dim3 grid(a->n_tiles, a->n_humans);
+    k_epilogue<<<grid, ENT, smem, st>>>(P);
+    count_launch();
+    GC_TRY(cuda_check(cudaGetLastError(), "k_epilogue launch"));
+    if (a->time_union && a->steps > 1) {
+        const long long cells = (long long)a->grid_w * a->grid_h;
+        const int blocks = (int)((cells + 255) / 256);
+        if (a->d_union32) { k_time_union<float><<<blocks, 256, 0, st>>>(a->d_union32, a->steps, cells); count_launch(); }
+        if (a->d_union64) { k_time_union<double><<<blocks, 256, 0, st>>>(a->d_union64, a->steps, cells); count_launch(); }
+        GC_TRY(cuda_check(cudaGetLastError(), "k_time_union launch"));
+    }
+    return GC_OK;
+}

@@ -1,0 +1,616 @@
+// gc_predict.cu -- K2: register-resident particle propagation fused with the per-step
+// occupancy histogram (Alg. 1 of arXiv 2603.01122; reference prediction.py:223-255).
+//
+// One CTA = one contiguous block of one human's particles.  Each thread keeps K
+// particles' (x, y, hypothesis) in registers for the WHOLE horizon; per step it samples
+// an action per particle, Euler-steps, maps the particle to its cell and adds it, with
+// warp aggregation (__match_any_sync), into a shared-memory privatised window covering
+// the cells the human can reach by that step.  After a CTA barrier the touched cells
+// (kept in a shared list) are flushed with one global reduction each into the human's
+// windowed count buffer, and zeroed.  HBM sees only those reductions.
+//
+// Two arithmetic families:
+//   MODE_REF  : the reference float32 step op for op: per-action
+//               logits, max shift, numpy exp (gc::exp_np), sequential cumsum, inverse CDF.
+//               Uniforms regenerated in-register from the reference's numpy Philox4x64
+//               streams (or read from a caller buffer) -> counts bit-identical.
+//   MODE_FACT : production, exact in distribution for grid control sets with
+//               goal-progress utility: weight(a,b) = H_b G_a e_b^a, one ex2 per heading.
+//   MODE_GEN  : production generic per-action softmax (fast ex2) for any control set.
+#include <cstring>
+#include <vector>
+#include "gc_common.cuh"
+#include "gc_internal.h"
+
+namespace gc {
+
+constexpr int NT = 256;        // threads per CTA
+constexpr int MAXM = 256;      // max actions per control set
+constexpr int MAXH = 128;      // max hypotheses per human
+constexpr int NBF = 24;        // headings of the factorised sampler (ControlSet.grid default)
+constexpr int NAF = 4;         // max speeds of the factorised sampler
+
+enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2 };
+
+struct KTable {
+    int m, m_keep, q_kind, n_speeds, n_headings;
+    float dv, tau, w_v, w_th;
+    const float *sx, *sy, *at, *pen, *dispx, *dispy;
+    const int *keep, *a_index;
+};
+
+struct KParams {
+    int n_humans, n, steps, ppc, ctas_per_human, rng_mode;
+    int grid_w, grid_h;
+    float ox, oy, res, inv_res;
+    const float *start_xy;
+    const int *hyp_off;
+    const float *beta32, *goal32;
+    const double *cdf, *log_w;
+    const unsigned long long *seed;
+    const unsigned *prefix;
+    const int *prefix_len;
+    const float *uniforms;
+    const double *hyp_u;
+    const int *hyp_in;
+    KTable tab[4];
+    int n_tables;
+    const int *table_id;
+    const int *step_r;
+    const long long *step_off;
+    long long human_stride;
+    unsigned *counts;
+    int smem_window;
+    int *hyp_out;
+    float *xy_out;
+    unsigned *error;
+    // headings shared by every table of a factorised launch (constant-bank operands)
+    float hcos[NBF], hsin[NBF], hth2[NBF];
+};
+
+// cell of a float32 position exactly as GridSpec.cells_of (occupancy.py:43-51, NEP 50)
+__device__ __forceinline__ void cell_ref(float x, float y, const KParams &P, int &ix, int &iy) {
+    const float fx = floorf(__fdiv_rn(__fsub_rn(x, P.ox), P.res));
+    const float fy = floorf(__fdiv_rn(__fsub_rn(y, P.oy), P.res));
+    ix = fx < 0.f ? 0 : (fx > (float)(P.grid_w - 1) ? P.grid_w - 1 : (int)fx);
+    iy = fy < 0.f ? 0 : (fy > (float)(P.grid_h - 1) ? P.grid_h - 1 : (int)fy);
+}
+
+__device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, int &ix, int &iy) {
+    const float fx = floorf((x - P.ox) * P.inv_res);
+    const float fy = floorf((y - P.oy) * P.inv_res);
+    ix = fx < 0.f ? 0 : (fx > (float)(P.grid_w - 1) ? P.grid_w - 1 : (int)fx);
+    iy = fy < 0.f ? 0 : (fy > (float)(P.grid_h - 1) ? P.grid_h - 1 : (int)fy);
+}
+
+struct SmemTabs {
+    // MODE_REF / MODE_GEN: per-action rows compacted over keep
+    float ax[MAXM], ay[MAXM], aat[MAXM], adx[MAXM], ady[MAXM];
+    // hypotheses of this CTA's human
+    double cdf[MAXH];
+    float hb[MAXH], hgx[MAXH], hgy[MAXH];
+    float hk[MAXH], hc2[MAXH], hsumH[MAXH];
+    // MODE_FACT displacement of (a, b)
+    float fdx[NAF * NBF], fdy[NAF * NBF];
+    int list_n[2];
+    int n_hyp, m_keep, q_kind, n_speeds;
+    float wth;
+};
+
+// ---- reference float32 step (prediction.py:147-162), 3 passes, no stored row --------
+__device__ __forceinline__ float ref_logit(const SmemTabs &S, int k, float rx, float ry, float d2,
+                                           float beta, int qk) {
+    float L;
+    if (qk == GC_Q_DEFAULT) {
+        L = __fsub_rn(-d2, S.aat[k]);
+    } else {
+        L = __fmul_rn(__fmaf_rn(ry, S.ay[k], __fmul_rn(rx, S.ax[k])), -2.0f);
+        L = __fsub_rn(L, S.aat[k]);
+        if (qk == GC_Q_GOAL_PROGRESS_FULL) L = __fsub_rn(L, d2);
+    }
+    return __fmul_rn(L, beta);
+}
+
+__device__ __forceinline__ int ref_pick(const SmemTabs &S, float x, float y, int h, float u) {
+    const float rx = __fsub_rn(x, S.hgx[h]), ry = __fsub_rn(y, S.hgy[h]);
+    const float d2 = __fadd_rn(__fmul_rn(rx, rx), __fmul_rn(ry, ry));
+    const float beta = S.hb[h];
+    const int mk = S.m_keep, qk = S.q_kind;
+    float M = -__int_as_float(0x7f800000);
+    for (int k = 0; k < mk; ++k) M = fmaxf(M, ref_logit(S, k, rx, ry, d2, beta, qk));
+    float c = 0.f;
+    for (int k = 0; k < mk; ++k) {
+        const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
+        c = (k == 0) ? w : __fadd_rn(c, w);
+    }
+    const float r = __fmul_rn(u, c);
+    float cc = 0.f;
+    int k = 0;
+    for (; k < mk; ++k) {
+        const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
+        cc = (k == 0) ? w : __fadd_rn(cc, w);
+        if (!(cc < r)) break;
+    }
+    return k < mk - 1 ? k : mk - 1;
+}
+
+// ---- production generic per-action softmax ------------------------------------------
+__device__ __forceinline__ int gen_pick(const SmemTabs &S, float x, float y, int h, float u) {
+    const float rx = x - S.hgx[h], ry = y - S.hgy[h];
+    const float d2 = fmaf(rx, rx, ry * ry);
+    const float bl = S.hb[h] * 1.4426950408889634f;
+    const int mk = S.m_keep, qk = S.q_kind;
+    auto L = [&](int k) {
+        float q;
+        if (qk == GC_Q_DEFAULT) q = -d2 - S.aat[k];
+        else q = fmaf(-2.f, fmaf(ry, S.ay[k], rx * S.ax[k]), -S.aat[k]);
+        return q * bl;
+    };
+    float M = -__int_as_float(0x7f800000);
+    for (int k = 0; k < mk; ++k) M = fmaxf(M, L(k));
+    float W = 0.f;
+    for (int k = 0; k < mk; ++k) W += ex2_approx(L(k) - M);
+    const float r = u * W;
+    float c = 0.f;
+    int k = 0;
+    for (; k < mk; ++k) {
+        c += ex2_approx(L(k) - M);
+        if (c > r) break;
+    }
+    return k < mk - 1 ? k : mk - 1;
+}
+
+// ---- production factorised sampler (grid control set x goal-progress utility) --------
+// logit(a,b) = beta*(-2 tau a dv d_b - (tau^2 + w_v) a^2 dv^2 - w_th theta_b^2) + const,
+// d_b = rel . (cos th_b, sin th_b).  With k = 2 beta tau dv, r = |rel|:
+//   weight(a,b) = H_b * G_a * e_b^a,  e_b = exp(-k (d_b + r)) in (0,1],
+//   G_a = exp(a k r - c a^2 - S),     S = max_a (a k r - c a^2),  H_b = exp(-beta w_th th_b^2)
+// -> per step: NB ex2 (e_b), 4 ex2 (G_a), Horner in e_b, inverse CDF over headings then
+//    over speeds.  Zero-speed actions share displacement 0 and merge into one "stay".
+template <bool WTH>
+__device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, float &x, float &y,
+                                          int h, float u1, float u2) {
+    const float rx = x - S.hgx[h], ry = y - S.hgy[h];
+    const float r2 = fmaf(rx, rx, ry * ry);
+    const float r = r2 > 0.f ? r2 * rsqrtf(r2) : 0.f;
+    const float kk = S.hk[h], c2 = S.hc2[h];
+    const float kr = kk * r;
+    const int na = S.n_speeds;
+    const float s1 = kr - c2, s2 = fmaf(2.f, kr, -4.f * c2), s3 = fmaf(3.f, kr, -9.f * c2);
+    float Smax = fmaxf(0.f, s1);
+    if (na > 2) Smax = fmaxf(Smax, s2);
+    if (na > 3) Smax = fmaxf(Smax, s3);
+    const float G0 = ex2_approx(-Smax);
+    const float G1 = ex2_approx(s1 - Smax);
+    const float G2 = na > 2 ? ex2_approx(s2 - Smax) : 0.f;
+    const float G3 = na > 3 ? ex2_approx(s3 - Smax) : 0.f;
+    float cum[NBF];
+    float C = 0.f;
+    const float nkr = -kr;
+#pragma unroll
+    for (int b = 0; b < NBF; ++b) {
+        const float d = fmaf(rx, P.hcos[b], ry * P.hsin[b]);
+        const float e = ex2_approx(fmaf(-kk, d, nkr));
+        float m = e * fmaf(e, fmaf(e, G3, G2), G1);
+        if (WTH) m *= ex2_approx(-S.wth * S.hb[h] * P.hth2[b]);
+        C += m;
+        cum[b] = C;
+    }
+    const float Z0 = G0 * S.hsumH[h];
+    const float rr = u1 * (Z0 + C);
+    if (rr < Z0) return;  // stay: every zero-speed action has displacement 0
+    const float t = rr - Z0;
+    int b = 0;
+#pragma unroll
+    for (int bb = 0; bb < NBF; ++bb) b += (cum[bb] <= t) ? 1 : 0;
+    b = b < NBF - 1 ? b : NBF - 1;
+    const float d = fmaf(rx, P.hcos[b], ry * P.hsin[b]);
+    const float e = ex2_approx(fmaf(-kk, d, nkr));
+    const float w1 = G1 * e, w2 = G2 * e * e, w3 = G3 * e * e * e;
+    const float r2u = u2 * (w1 + w2 + w3);
+    int a = 1 + ((w1 <= r2u) ? 1 : 0) + ((w1 + w2 <= r2u) ? 1 : 0);
+    a = a < na - 1 ? a : na - 1;
+    x += S.fdx[a * NBF + b];
+    y += S.fdy[a * NBF + b];
+}
+
+template <int MODE, int K>
+__global__ void __launch_bounds__(NT) k_predict(const KParams P) {
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    __shared__ SmemTabs S;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int h = blockIdx.x / P.ctas_per_human;
+    const int blk = blockIdx.x - h * P.ctas_per_human;
+    const int tsel = __ldg(&P.table_id[h]);
+    const KTable &T = P.tab[tsel];
+    const int h0 = __ldg(&P.hyp_off[h]);
+    const int nh = __ldg(&P.hyp_off[h + 1]) - h0;
+
+    // ---- stage tables in shared memory ----
+    if (tid == 0) {
+        S.n_hyp = nh; S.m_keep = T.m_keep; S.q_kind = T.q_kind; S.n_speeds = T.n_speeds;
+        S.wth = T.w_th;
+        S.list_n[0] = 0; S.list_n[1] = 0;
+    }
+    for (int k = tid; k < T.m_keep; k += NT) {
+        const int j = __ldg(&T.keep[k]);
+        S.ax[k] = __ldg(&T.sx[j]);
+        S.ay[k] = __ldg(&T.sy[j]);
+        S.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? __ldg(&T.pen[j]) : __ldg(&T.at[j]);
+        S.adx[k] = __ldg(&T.dispx[j]);
+        S.ady[k] = __ldg(&T.dispy[j]);
+    }
+    if (MODE == MODE_FACT) {
+        for (int i = tid; i < NAF * NBF; i += NT) {
+            const int a = i / NBF;
+            const int j = a < T.n_speeds ? __ldg(&T.a_index[i]) : -1;
+            S.fdx[i] = j >= 0 ? __ldg(&T.dispx[j]) : 0.f;
+            S.fdy[i] = j >= 0 ? __ldg(&T.dispy[j]) : 0.f;
+        }
+    }
+    for (int i = tid; i < nh; i += NT) {
+        const float b = __ldg(&P.beta32[h0 + i]);
+        S.hb[i] = b;
+        S.hgx[i] = __ldg(&P.goal32[2 * (h0 + i)]);
+        S.hgy[i] = __ldg(&P.goal32[2 * (h0 + i) + 1]);
+        if (MODE == MODE_FACT) {
+            const float L2E = 1.4426950408889634f;
+            S.hk[i] = 2.f * b * T.tau * T.dv * L2E;
+            S.hc2[i] = b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E;
+            float sh = 0.f;
+            for (int q = 0; q < T.n_headings; ++q)
+                sh += (T.w_th != 0.f) ? exp2f(-T.w_th * b * P.hth2[q] * L2E) : 1.f;
+            S.hsumH[i] = sh;
+        }
+    }
+    if (tid == 0) {
+        if (P.cdf) {
+            for (int i = 0; i < nh; ++i) S.cdf[i] = P.cdf[h0 + i];
+        } else {
+            double c = 0.0;
+            for (int i = 0; i < nh; ++i) { c += exp(P.log_w[h0 + i]); S.cdf[i] = c; }
+            S.cdf[nh - 1] = 1.0;
+        }
+    }
+    if (MODE == MODE_FACT && T.w_th != 0.f) {
+        // pre-scale theta^2 by log2(e) once: hth2 already holds theta^2; fold beta*w_th*L2E
+        if (tid == 0) S.wth = T.w_th * 1.4426950408889634f;
+    }
+    unsigned *win_s = reinterpret_cast<unsigned *>(smem_dyn);
+    int *list = reinterpret_cast<int *>(smem_dyn) + (P.smem_window ? 0 : 0);
+    int max_cells = 0;
+    if (P.smem_window) {
+        max_cells = (2 * __ldg(&P.step_r[P.steps - 1]) + 1);
+        max_cells *= max_cells;
+        list = reinterpret_cast<int *>(win_s + max_cells);
+        for (int i = tid; i < max_cells; i += NT) win_s[i] = 0u;
+    }
+    __syncthreads();
+
+    // ---- particles: hypothesis draw + start state ----
+    const float sx0 = __ldg(&P.start_xy[2 * h]), sy0 = __ldg(&P.start_xy[2 * h + 1]);
+    int cx, cy;
+    cell_ref(sx0, sy0, P, cx, cy);
+    const unsigned long long seed = __ldg(&P.seed[h]);
+    const int plen = __ldg(&P.prefix_len[h]);
+    SSPool pool_pre = ss_pool_init(seed);
+    for (int i = 0; i < plen; ++i) ss_absorb(pool_pre, __ldg(&P.prefix[4 * h + i]));
+
+    float px[K], py[K];
+    int ph[K];
+    U4 rnd[K];
+    const int pbase = blk * P.ppc;
+    {
+        uint64_t hk0 = 0, hk1 = 0;
+        if (MODE == MODE_REF && !P.hyp_in && !P.hyp_u) {
+            SSPool s = pool_pre;
+            ss_absorb(s, 0u);  // HYPOTHESIS_DRAWS namespace (rng.py:19)
+            ss_key(s, hk0, hk1);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int p = pbase + k * NT + tid;
+            px[k] = sx0; py[k] = sy0; ph[k] = 0;
+            rnd[k] = U4{0, 0, 0, 0};
+            if (p >= P.n) continue;
+            int hi;
+            if (P.hyp_in) {
+                hi = __ldg(&P.hyp_in[(long long)h * P.n + p]);
+            } else {
+                double u;
+                if (P.hyp_u) u = __ldg(&P.hyp_u[(long long)h * P.n + p]);
+                else if (MODE == MODE_REF) u = philox64_f64(hk0, hk1, (uint64_t)p);
+                else {
+                    const U4 o = philox4x32(U4{(unsigned)p, 0xFFFFFFFFu, (unsigned)h, 0x5EEDu},
+                                            (unsigned)seed, (unsigned)(seed >> 32));
+                    u = ((double)(o.x >> 5) * 67108864.0 + (double)(o.y >> 6)) * (1.0 / 9007199254740992.0);
+                }
+                hi = 0;
+                for (int i = 0; i < nh; ++i) hi += (S.cdf[i] <= u) ? 1 : 0;  // searchsorted right
+                hi = hi < nh - 1 ? hi : nh - 1;
+            }
+            ph[k] = hi;
+            if (P.hyp_out) P.hyp_out[(long long)h * P.n + p] = hi;
+        }
+    }
+    SSPool pool_step = pool_pre;
+    if (MODE == MODE_REF) ss_absorb(pool_step, 1u);  // STEP_DRAWS namespace
+
+    const long long hbase = (long long)h * P.human_stride;
+    for (int t = 1; t <= P.steps; ++t) {
+        const int R = __ldg(&P.step_r[t - 1]);
+        const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
+        const int y0 = max(0, cy - R), y1 = min(P.grid_h - 1, cy + R);
+        const int ww = x1 - x0 + 1, wh = y1 - y0 + 1;
+        unsigned *gcount = P.counts + hbase + __ldg(&P.step_off[t - 1]);
+        uint64_t sk0 = 0, sk1 = 0;
+        int key_chunk = -1;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int p = pbase + k * NT + tid;
+            const bool valid = p < P.n;
+            int local = -1;
+            if (valid) {
+                float x = px[k], y = py[k];
+                if (MODE == MODE_REF) {
+                    float u;
+                    if (P.uniforms) {
+                        u = __ldg(&P.uniforms[((long long)h * P.steps + (t - 1)) * P.n + p]);
+                    } else {
+                        const int c = p >> 10;
+                        if (c != key_chunk) {
+                            SSPool s = pool_step;
+                            ss_absorb(s, (unsigned)t);
+                            ss_absorb(s, (unsigned)c);
+                            ss_key(s, sk0, sk1);
+                            key_chunk = c;
+                        }
+                        u = philox64_f32(sk0, sk1, (uint64_t)(p & 1023));
+                    }
+                    const int a = ref_pick(S, x, y, ph[k], u);
+                    x = __fadd_rn(x, S.adx[a]);
+                    y = __fadd_rn(y, S.ady[a]);
+                } else {
+                    if (((t - 1) & 1) == 0)
+                        rnd[k] = philox4x32(U4{(unsigned)p, (unsigned)((t - 1) >> 1), (unsigned)h, 0xA11CEu},
+                                            (unsigned)seed, (unsigned)(seed >> 32));
+                    const uint32_t ua = ((t - 1) & 1) ? rnd[k].z : rnd[k].x;
+                    const uint32_t ub = ((t - 1) & 1) ? rnd[k].w : rnd[k].y;
+                    if (MODE == MODE_FACT) {
+                        if (S.wth != 0.f) fact_step<true>(S, P, x, y, ph[k], u24(ua), u24(ub));
+                        else fact_step<false>(S, P, x, y, ph[k], u24(ua), u24(ub));
+                    } else {
+                        const int a = gen_pick(S, x, y, ph[k], u24(ua));
+                        x += S.adx[a];
+                        y += S.ady[a];
+                    }
+                }
+                px[k] = x; py[k] = y;
+                int ix, iy;
+                if (MODE == MODE_REF) cell_ref(x, y, P, ix, iy);
+                else cell_fast(x, y, P, ix, iy);
+                const int lx = ix - x0, ly = iy - y0;
+                if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) {
+                    if (P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
+                } else {
+                    local = ly * ww + lx;
+                }
+            }
+            // warp-aggregated increment (all 32 lanes execute the match)
+            const unsigned peers = __match_any_sync(0xffffffffu, local);
+            if (local >= 0 && lane == __ffs(peers) - 1) {
+                const unsigned cnt = __popc(peers);
+                if (P.smem_window) {
+                    const unsigned old = atomicAdd(&win_s[local], cnt);
+                    if (old == 0u) list[atomicAdd(&S.list_n[t & 1], 1)] = local;
+                } else {
+                    atomicAdd(&gcount[local], cnt);
+                }
+            }
+        }
+        if (P.smem_window) {
+            __syncthreads();
+            const int nl = S.list_n[t & 1];
+            if (tid == 0) S.list_n[(t + 1) & 1] = 0;
+            for (int i = tid; i < nl; i += NT) {
+                const int c = list[i];
+                const unsigned v = win_s[c];
+                win_s[c] = 0u;
+                atomicAdd(&gcount[c], v);
+            }
+            __syncthreads();
+        }
+    }
+    if (P.xy_out) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int p = pbase + k * NT + tid;
+            if (p < P.n) {
+                P.xy_out[((long long)h * P.n + p) * 2] = px[k];
+                P.xy_out[((long long)h * P.n + p) * 2 + 1] = py[k];
+            }
+        }
+    }
+}
+
+// ---- one explicit propagate_step (prediction.py:165-211) ------------------------------
+__global__ void __launch_bounds__(NT) k_propagate_step(float *xy, const int *hyp, int n,
+                                                       const float *beta32, const float *goal32,
+                                                       int n_hyp, KTable T, const float *u01,
+                                                       unsigned long long seed, unsigned p0,
+                                                       unsigned p1, unsigned p2, unsigned p3,
+                                                       int plen, int step) {
+    __shared__ SmemTabs S;
+    const int tid = threadIdx.x;
+    if (tid == 0) { S.m_keep = T.m_keep; S.q_kind = T.q_kind; }
+    for (int k = tid; k < T.m_keep; k += NT) {
+        const int j = T.keep[k];
+        S.ax[k] = T.sx[j]; S.ay[k] = T.sy[j];
+        S.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? T.pen[j] : T.at[j];
+        S.adx[k] = T.dispx[j]; S.ady[k] = T.dispy[j];
+    }
+    for (int i = tid; i < n_hyp; i += NT) {
+        S.hb[i] = beta32[i]; S.hgx[i] = goal32[2 * i]; S.hgy[i] = goal32[2 * i + 1];
+    }
+    __syncthreads();
+    const int p = blockIdx.x * NT + tid;
+    if (p >= n) return;
+    float u;
+    if (u01) {
+        u = u01[p];
+    } else {
+        SSPool s = ss_pool_init(seed);
+        const unsigned pre[4] = {p0, p1, p2, p3};
+        for (int i = 0; i < plen; ++i) ss_absorb(s, pre[i]);
+        ss_absorb(s, 1u);
+        ss_absorb(s, (unsigned)step);
+        ss_absorb(s, (unsigned)(p >> 10));
+        uint64_t k0, k1;
+        ss_key(s, k0, k1);
+        u = philox64_f32(k0, k1, (uint64_t)(p & 1023));
+    }
+    const float x = xy[2 * p], y = xy[2 * p + 1];
+    const int a = ref_pick(S, x, y, hyp[p], u);
+    xy[2 * p] = __fadd_rn(x, S.adx[a]);
+    xy[2 * p + 1] = __fadd_rn(y, S.ady[a]);
+}
+
+// ---- sample_hypotheses (prediction.py:124-131) ----------------------------------------
+__global__ void k_sample_hyp(const double *cdf, int n_hyp, int n, uint64_t k0, uint64_t k1, int *out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const double u = philox64_f64(k0, k1, (uint64_t)p);
+    int hi = 0;
+    for (int i = 0; i < n_hyp; ++i) hi += (cdf[i] <= u) ? 1 : 0;
+    out[p] = hi < n_hyp - 1 ? hi : n_hyp - 1;
+}
+
+static KTable to_ktable(const gc_action_table &a) {
+    KTable t;
+    t.m = a.m; t.m_keep = a.m_keep; t.q_kind = a.q_kind; t.n_speeds = a.n_speeds;
+    t.n_headings = a.n_headings; t.dv = a.dv; t.tau = a.tau; t.w_v = a.w_v; t.w_th = a.w_th;
+    t.sx = a.d_sx; t.sy = a.d_sy; t.at = a.d_at; t.pen = a.d_pen; t.dispx = a.d_dispx;
+    t.dispy = a.d_dispy; t.keep = a.d_keep; t.a_index = a.d_a_index;
+    return t;
+}
+
+template <int MODE, int K>
+static gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t st) {
+    auto fn = k_predict<MODE, K>;
+    if (smem > 48 * 1024)
+        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<grid, NT, smem, st>>>(P);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_predict launch");
+}
+
+template <int MODE>
+static gc_status dispatch_k(const KParams &P, int K, int grid, size_t smem, cudaStream_t st) {
+    switch (K) {
+        case 1: return launch_predict<MODE, 1>(P, grid, smem, st);
+        case 2: return launch_predict<MODE, 2>(P, grid, smem, st);
+        case 4: return launch_predict<MODE, 4>(P, grid, smem, st);
+        default: return launch_predict<MODE, 8>(P, grid, smem, st);
+    }
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
+    GC_CHECK_ARG(a != nullptr, "gc_predict: null args");
+    GC_CHECK_ARG(a->n_humans >= 1 && a->n >= 1 && a->steps >= 1, "gc_predict: need n_humans, n, steps >= 1");
+    GC_CHECK_ARG(a->n_tables >= 1 && a->n_tables <= 4 && a->h_tables, "gc_predict: 1..4 action tables");
+    GC_CHECK_ARG(a->d_counts && a->d_step_r && a->d_step_off && a->d_start_xy && a->d_hyp_off,
+                 "gc_predict: missing device buffers");
+    GC_CHECK_ARG(a->d_seed && a->d_prefix && a->d_prefix_len && a->d_table_id, "gc_predict: missing rng/table ids");
+    GC_CHECK_ARG(a->d_cdf || a->d_log_w || a->d_hyp_in, "gc_predict: need a cdf, log weights or hypotheses");
+    GC_CHECK_ARG(a->grid_w >= 1 && a->grid_h >= 1 && a->res32 > 0.f, "gc_predict: bad grid");
+    KParams P;
+    memset(&P, 0, sizeof(P));
+    P.n_humans = a->n_humans; P.n = a->n; P.steps = a->steps; P.rng_mode = a->rng_mode;
+    P.grid_w = a->grid_w; P.grid_h = a->grid_h;
+    P.ox = a->origin_x32; P.oy = a->origin_y32; P.res = a->res32; P.inv_res = 1.0f / a->res32;
+    P.start_xy = a->d_start_xy; P.hyp_off = a->d_hyp_off; P.beta32 = a->d_beta32; P.goal32 = a->d_goal32;
+    P.cdf = a->d_cdf; P.log_w = a->d_log_w;
+    P.seed = (const unsigned long long *)a->d_seed; P.prefix = a->d_prefix; P.prefix_len = a->d_prefix_len;
+    P.uniforms = a->rng_mode == GC_RNG_UNIFORMS ? a->d_uniforms : nullptr;
+    P.hyp_u = a->rng_mode == GC_RNG_UNIFORMS ? a->d_hyp_u : nullptr;
+    P.hyp_in = a->d_hyp_in;
+    GC_CHECK_ARG(a->rng_mode != GC_RNG_UNIFORMS || a->d_uniforms, "gc_predict: GC_RNG_UNIFORMS needs d_uniforms");
+    P.n_tables = a->n_tables; P.table_id = a->d_table_id;
+    bool fact = a->rng_mode == GC_RNG_PRODUCTION;
+    for (int i = 0; i < a->n_tables; ++i) {
+        const gc_action_table &t = a->h_tables[i];
+        if (t.m < 1 || t.m_keep < 1) { set_error("all actions are masked"); return GC_EMPTY_CONTROL_SET; }
+        GC_CHECK_ARG(t.m <= MAXM && t.m_keep <= t.m, "gc_predict: at most %d actions", MAXM);
+        P.tab[i] = to_ktable(t);
+        const bool ok = t.n_speeds >= 2 && t.n_speeds <= NAF && t.n_headings == NBF && t.d_a_index &&
+                        t.d_cos_h && (t.q_kind == GC_Q_GOAL_PROGRESS || t.q_kind == GC_Q_GOAL_PROGRESS_FULL);
+        fact = fact && ok;
+    }
+    if (fact) {
+        // every table of the launch shares the heading set (checked by the host mirror);
+        // copy it into the parameter bank so the heading loop reads constant operands
+        std::vector<float> c(NBF), s(NBF), th(NBF);
+        GC_CUDA(cudaMemcpyAsync(c.data(), a->h_tables[0].d_cos_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+        GC_CUDA(cudaMemcpyAsync(s.data(), a->h_tables[0].d_sin_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+        GC_CUDA(cudaMemcpyAsync(th.data(), a->h_tables[0].d_theta_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+        GC_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+        for (int b = 0; b < NBF; ++b) { P.hcos[b] = c[b]; P.hsin[b] = s[b]; P.hth2[b] = th[b] * th[b]; }
+    }
+    P.step_r = a->d_step_r; P.step_off = (const long long *)a->d_step_off;
+    P.human_stride = a->human_stride; P.counts = a->d_counts;
+    P.hyp_out = a->d_hyp_out; P.xy_out = a->d_xy_out; P.error = a->d_error;
+
+    // particles per thread: enough CTAs to fill 148 SMs at 2 CTAs/SM, then grow K
+    const long long total = (long long)a->n_humans * a->n;
+    int K = 1;
+    while (K < 8 && total / ((long long)NT * K * 2) >= 2 * 148 * 2) K *= 2;
+    const int ppc = NT * K;
+    P.ppc = ppc;
+    P.ctas_per_human = (a->n + ppc - 1) / ppc;
+    const long long grid = (long long)P.ctas_per_human * a->n_humans;
+    GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
+    const size_t win_bytes = (size_t)a->max_win_cells * 4 + (size_t)ppc * 4;
+    P.smem_window = win_bytes <= 200 * 1024 ? 1 : 0;
+    const size_t smem = P.smem_window ? win_bytes : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? MODE_FACT : MODE_GEN) : MODE_REF;
+    if (mode == MODE_REF) return dispatch_k<MODE_REF>(P, K, (int)grid, smem, st);
+    if (mode == MODE_FACT) return dispatch_k<MODE_FACT>(P, K, (int)grid, smem, st);
+    return dispatch_k<MODE_GEN>(P, K, (int)grid, smem, st);
+}
+
+extern "C" gc_status gc_propagate_step(float *d_xy, const int32_t *d_hyp, int32_t n, const float *d_beta32,
+                                       const float *d_goal32, int32_t n_hyp, const gc_action_table *h_table,
+                                       const float *d_u01, uint64_t seed, const uint32_t *h_prefix,
+                                       int32_t prefix_len, int32_t step, void *stream) {
+    GC_CHECK_ARG(d_xy && d_hyp && h_table && d_beta32 && d_goal32 && n >= 1, "gc_propagate_step: bad args");
+    GC_CHECK_ARG(prefix_len >= 0 && prefix_len <= 4, "gc_propagate_step: prefix of at most 4 words");
+    if (h_table->m_keep < 1) { set_error("all actions are masked"); return GC_EMPTY_CONTROL_SET; }
+    GC_CHECK_ARG(h_table->m <= MAXM, "gc_propagate_step: at most %d actions", MAXM);
+    GC_CHECK_ARG(n_hyp >= 1 && n_hyp <= MAXH, "gc_propagate_step: 1..%d hypotheses", MAXH);
+    unsigned pre[4] = {0, 0, 0, 0};
+    for (int i = 0; i < prefix_len; ++i) pre[i] = h_prefix[i];
+    k_propagate_step<<<(n + NT - 1) / NT, NT, 0, (cudaStream_t)stream>>>(
+        d_xy, d_hyp, n, d_beta32, d_goal32, n_hyp, to_ktable(*h_table), d_u01,
+        (unsigned long long)seed, pre[0], pre[1], pre[2], pre[3], prefix_len, step);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_propagate_step launch");
+}
+
+extern "C" gc_status gc_sample_hypotheses(const double *d_cdf, int32_t n_hyp, int32_t n, uint64_t seed,
+                                          const uint32_t *h_prefix, int32_t prefix_len, int32_t *d_out,
+                                          void *stream) {
+    GC_CHECK_ARG(d_cdf && d_out && n >= 1 && n_hyp >= 1, "gc_sample_hypotheses: bad args");
+    SSPool s = ss_pool_init(seed);
+    for (int i = 0; i < prefix_len; ++i) ss_absorb(s, h_prefix[i]);
+    ss_absorb(s, 0u);
+    uint64_t k0, k1;
+    ss_key(s, k0, k1);
+    k_sample_hyp<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(d_cdf, n_hyp, n, k0, k1, d_out);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_sample_hyp launch");
+}

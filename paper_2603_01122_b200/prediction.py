@@ -1,0 +1,370 @@
+"""Particle occupancy prediction on the GPU (reference prediction.py:1-414).
+
+Public names and semantics follow the reference; the work runs in three kernels:
+K2 ``gc_predict`` (hypothesis draw + whole-horizon propagation in registers fused with
+the per-step histogram), K3 ``gc_grid_epilogue`` (counts/n, smoothing, union) and, for
+the standalone helpers, ``gc_propagate_step`` / ``gc_sample_hypotheses``.
+
+``PredictionConfig.mode``:
+  "reference"  (default) regenerates the reference's own Philox streams in-register and
+               runs its float32 arithmetic op for op: for the same inputs and seed the
+               per-step counts -- hence every unsmoothed layer -- are bit-identical to
+               gridcast.predict; smoothed layers agree to <= 1e-15.
+  "production" Philox4x32 + the factorised exact-in-distribution sampler (fast path);
+               layers agree with the reference in distribution (TV bound).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections import OrderedDict
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .agents import ControlSet, HumanState, QFunction
+from .belief import HypothesisSpace, JointBelief
+from .device import device, stream_handle
+from .occupancy import GridSpec, OccupancyGrid
+from .tables import ActionTables, Geometry, hypothesis_arrays
+
+CHUNK = 1024  # particles per reference random stream (prediction.py:33)
+MODES = {"reference": _lib.GC_RNG_REFERENCE, "production": _lib.GC_RNG_PRODUCTION}
+_MASK64 = (1 << 64) - 1
+
+
+class EnumerationCapExceeded(ValueError):
+    """Instance too large for exact enumeration."""
+
+
+@dataclass(frozen=True)
+class ParticleBatch:
+    xy: np.ndarray
+    hypothesis_idx: np.ndarray
+
+    def __post_init__(self):
+        xy = np.asarray(self.xy, dtype=np.float32)
+        hyp = np.asarray(self.hypothesis_idx, dtype=np.int32)
+        if xy.ndim != 2 or xy.shape[1] != 2 or xy.shape[0] == 0:
+            raise ValueError("particle positions must form a nonempty (n, 2) array")
+        if hyp.shape != (xy.shape[0],):
+            raise ValueError("one hypothesis index per particle required")
+        if (hyp < 0).any():
+            raise ValueError("hypothesis indices must be nonnegative")
+        object.__setattr__(self, "xy", xy)
+        object.__setattr__(self, "hypothesis_idx", hyp)
+
+    @property
+    def n(self) -> int:
+        return self.xy.shape[0]
+
+    @classmethod
+    def duplicated(cls, z: HumanState, hypothesis_idx) -> "ParticleBatch":
+        n = len(hypothesis_idx)
+        return cls(np.tile(np.array([z.x, z.y], dtype=np.float32), (n, 1)), hypothesis_idx)
+
+
+@dataclass(frozen=True)
+class PredictionConfig:
+    n: int = 8192
+    steps: int = 6
+    dt: float = 0.5
+    smoothing_sigma: float = 0.1
+    seed: int = 0
+    mode: str = "reference"
+
+    def __post_init__(self):
+        if self.n < 1 or self.steps < 1:
+            raise ValueError("need n >= 1 and steps >= 1")
+        if self.dt <= 0:
+            raise ValueError("dt must be > 0")
+        if self.smoothing_sigma < 0:
+            raise ValueError("smoothing sigma must be >= 0")
+        if self.mode not in MODES:
+            raise ValueError(f"mode must be one of {sorted(MODES)}")
+
+
+class PredictionStack:
+    """T occupancy layers; layer k is p(z at base_time + (k+1) dt).
+
+    Device-resident: ``layers_device`` is the (T, H, W) float64 CUDA tensor written by
+    the epilogue; ``layers`` materialises a read-only host copy on first access (the
+    reference returns host arrays, prediction.py:98-106)."""
+
+    def __init__(self, spec: GridSpec, layers, base_time: float, dt: float):
+        if dt <= 0:
+            raise ValueError("dt must be > 0")
+        self.spec, self.base_time, self.dt = spec, float(base_time), float(dt)
+        if isinstance(layers, torch.Tensor):
+            if layers.dim() != 3 or tuple(layers.shape[1:]) != spec.shape:
+                raise ValueError("layers must be (T, height, width) matching the spec")
+            self._dev, self._host = layers, None
+        else:
+            arr = np.asarray(layers, dtype=float)
+            if arr.ndim != 3 or arr.shape[1:] != spec.shape:
+                raise ValueError("layers must be (T, height, width) matching the spec")
+            arr = arr.copy()
+            arr.setflags(write=False)
+            self._dev, self._host = None, arr
+
+    @property
+    def layers(self) -> np.ndarray:
+        if self._host is None:
+            arr = self._dev.cpu().numpy()
+            arr.setflags(write=False)
+            self._host = arr
+        return self._host
+
+    @property
+    def layers_device(self) -> torch.Tensor:
+        if self._dev is None:
+            self._dev = torch.as_tensor(self._host, device=device())
+        return self._dev
+
+    @property
+    def steps(self) -> int:
+        return (self._dev if self._dev is not None else self._host).shape[0]
+
+    def grid(self, layer: int) -> OccupancyGrid:
+        return OccupancyGrid(self.spec, self.layers[layer])
+
+    def grids(self) -> list:
+        return [self.grid(k) for k in range(self.steps)]
+
+    def layer_index_for(self, time: float) -> int:
+        k = int(round((time - self.base_time) / self.dt)) - 1
+        return min(max(k, 0), self.steps - 1)
+
+
+# ---- caches of device tables ----------------------------------------------------------
+_ACTION_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_GEOM_CACHE: "OrderedDict[tuple, Geometry]" = OrderedDict()
+
+
+def action_tables(control_set, q, dt, dev) -> ActionTables:
+    key = (id(control_set), id(q), float(dt), str(dev))
+    hit = _ACTION_CACHE.get(key)
+    if hit is not None and hit[0] is control_set and hit[1] is q:
+        return hit[2]
+    t = ActionTables(control_set, q, dt, dev)
+    _ACTION_CACHE[key] = (control_set, q, t)
+    while len(_ACTION_CACHE) > 64:
+        _ACTION_CACHE.popitem(last=False)
+    return t
+
+
+def geometry(spec: GridSpec, steps: int, max_step: float, sigma: float, dev) -> Geometry:
+    key = (spec.width, spec.height, spec.resolution, spec.origin, steps, max_step, sigma, str(dev))
+    g = _GEOM_CACHE.get(key)
+    if g is None:
+        g = Geometry(spec, steps, max_step, sigma, dev)
+        _GEOM_CACHE[key] = g
+        while len(_GEOM_CACHE) > 32:
+            _GEOM_CACHE.popitem(last=False)
+    return g
+
+
+def host_cdf(log_weights) -> np.ndarray:
+    """cdf exactly as sample_hypotheses builds it (prediction.py:128-129)."""
+    cdf = np.cumsum(np.exp(np.asarray(log_weights, dtype=float)))
+    cdf[-1] = 1.0
+    return cdf
+
+
+def _prefix_words(prefix) -> list:
+    words = [int(p) & 0xFFFFFFFF for p in prefix]
+    if len(words) > 4:
+        raise NotImplementedError("random-stream prefixes of at most 4 elements are supported")
+    return words
+
+
+@dataclass
+class HumanJob:
+    """One human of a batched predict: start state, belief, hypotheses, stream key."""
+
+    z0: HumanState
+    log_weights: np.ndarray
+    beta_of: np.ndarray
+    goal_xy_of: np.ndarray
+    seed: int
+    prefix: tuple = ()
+    table: int = 0
+
+
+def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int, steps: int, dt: float,
+                sigma: float, spec: GridSpec, mode: str, per_human_layers: bool = True,
+                union64: bool = False, union32: bool = False, time_union: bool = False,
+                uniforms: Optional[torch.Tensor] = None, hyp_in: Optional[torch.Tensor] = None,
+                want_hyp: bool = False, want_xy: bool = False, stream=None):
+    """Batched K2 + K3 launch; returns a dict of device tensors."""
+    dev = device()
+    H = len(jobs)
+    max_step = max(t.max_step for t in tables)
+    geo = geometry(spec, steps, max_step, float(sigma), dev)
+    hyp_off = np.zeros(H + 1, dtype=np.int32)
+    for i, j in enumerate(jobs):
+        if len(j.beta_of) > 128:
+            raise NotImplementedError("at most 128 hypotheses per human")
+        hyp_off[i + 1] = hyp_off[i] + len(j.beta_of)
+    up = lambda a, dt_: torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=dt_)), device=dev)
+    d_start = up([[np.float32(j.z0.x), np.float32(j.z0.y)] for j in jobs], np.float32)
+    d_hyp_off = up(hyp_off, np.int32)
+    d_beta = up(np.concatenate([j.beta_of for j in jobs]).astype(np.float32), np.float32)
+    d_goal = up(np.concatenate([j.goal_xy_of for j in jobs]).astype(np.float32), np.float32)
+    d_cdf = up(np.concatenate([host_cdf(j.log_weights) for j in jobs]), np.float64)
+    d_seed = up([int(j.seed) & _MASK64 for j in jobs], np.uint64)
+    pre = np.zeros((H, 4), dtype=np.uint32)
+    plen = np.zeros(H, dtype=np.int32)
+    for i, j in enumerate(jobs):
+        w = _prefix_words(j.prefix)
+        pre[i, :len(w)] = w
+        plen[i] = len(w)
+    d_pre, d_plen = up(pre, np.uint32), up(plen, np.int32)
+    d_tid = up([j.table for j in jobs], np.int32)
+    counts = torch.zeros(H * geo.human_stride, dtype=torch.int32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = {}
+    if want_hyp:
+        out["hyp"] = torch.empty((H, n), dtype=torch.int32, device=dev)
+    if want_xy:
+        out["xy"] = torch.empty((H, n, 2), dtype=torch.float32, device=dev)
+
+    a = _lib.PredictArgs()
+    a.n_humans, a.n, a.steps = H, n, steps
+    a.rng_mode = _lib.GC_RNG_UNIFORMS if uniforms is not None else MODES[mode]
+    a.grid_w, a.grid_h = spec.width, spec.height
+    a.origin_x32 = float(np.float32(spec.origin[0]))
+    a.origin_y32 = float(np.float32(spec.origin[1]))
+    a.res32 = float(np.float32(spec.resolution))
+    a.d_start_xy, a.d_hyp_off = d_start.data_ptr(), d_hyp_off.data_ptr()
+    a.d_beta32, a.d_goal32, a.d_cdf, a.d_log_w = d_beta.data_ptr(), d_goal.data_ptr(), d_cdf.data_ptr(), None
+    a.d_seed, a.d_prefix, a.d_prefix_len = d_seed.data_ptr(), d_pre.data_ptr(), d_plen.data_ptr()
+    a.d_uniforms = uniforms.data_ptr() if uniforms is not None else None
+    a.d_hyp_u = None
+    a.d_hyp_in = hyp_in.data_ptr() if hyp_in is not None else None
+    tarr = (_lib.ActionTable * len(tables))(*[t.struct for t in tables])
+    a.h_tables, a.n_tables, a.d_table_id = tarr, len(tables), d_tid.data_ptr()
+    a.d_step_r, a.d_step_off = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr()
+    a.human_stride, a.max_win_cells = geo.human_stride, geo.max_win_cells
+    a.d_counts = counts.data_ptr()
+    a.d_hyp_out = out["hyp"].data_ptr() if want_hyp else None
+    a.d_xy_out = out["xy"].data_ptr() if want_xy else None
+    a.d_error = err.data_ptr()
+    sh = stream_handle(stream)
+    _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")
+
+    e = _lib.EpilogueArgs()
+    e.n_humans, e.n, e.steps = H, n, steps
+    e.grid_w, e.grid_h, e.radius = spec.width, spec.height, geo.radius
+    e.d_kernel, e.d_zx, e.d_zy = geo.d_kernel.data_ptr(), geo.d_zx.data_ptr(), geo.d_zy.data_ptr()
+    e.origin_x32, e.origin_y32, e.res32 = a.origin_x32, a.origin_y32, a.res32
+    e.n_tiles, e.d_start_xy = geo.n_tiles, d_start.data_ptr()
+    e.d_step_r, e.d_step_off, e.human_stride = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr(), geo.human_stride
+    e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), counts.data_ptr()
+    if per_human_layers:
+        out["layers"] = torch.zeros((H, steps, spec.height, spec.width), dtype=torch.float64, device=dev)
+        e.d_layers64 = out["layers"].data_ptr()
+    if union64:
+        out["union64"] = torch.zeros((steps, spec.height, spec.width), dtype=torch.float64, device=dev)
+        e.d_union64 = out["union64"].data_ptr()
+    if union32:
+        out["union32"] = torch.zeros((steps, spec.height, spec.width), dtype=torch.float32, device=dev)
+        e.d_union32 = out["union32"].data_ptr()
+    e.time_union = int(time_union)
+    _lib.check(_lib.lib().gc_grid_epilogue(ctypes.byref(e), sh), "gc_grid_epilogue")
+    if int(err.item()) != 0:
+        raise RuntimeError("gc_predict: a particle left its reachable-cell window (internal error)")
+    out["counts"] = counts
+    out["geometry"] = geo
+    return out
+
+
+def _as_state(z_history) -> HumanState:
+    if isinstance(z_history, HumanState) or (hasattr(z_history, "x") and hasattr(z_history, "y")):
+        return z_history
+    seq = list(z_history)
+    if not seq:
+        raise ValueError("empty state history")
+    return seq[-1]
+
+
+def sample_hypotheses(belief: JointBelief, n: int, seed: int, prefix: tuple = ()) -> np.ndarray:
+    """n i.i.d. hypothesis indices drawn with the reference stream (prediction.py:124-131)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    dev = device()
+    cdf = torch.as_tensor(host_cdf(belief.log_weights), device=dev)
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    words = _prefix_words(prefix)
+    arr = (ctypes.c_uint32 * max(1, len(words)))(*words)
+    _lib.check(_lib.lib().gc_sample_hypotheses(ctypes.c_void_p(cdf.data_ptr()), len(cdf), n,
+                                               int(seed) & _MASK64, arr, len(words),
+                                               ctypes.c_void_p(out.data_ptr()), stream_handle()),
+               "sample_hypotheses")
+    return out.cpu().numpy()
+
+
+def propagate_step(batch: ParticleBatch, control_set: ControlSet, q: QFunction, space: HypothesisSpace,
+                   dt: float, seed: int, step: int = 0, workers: Optional[int] = None,
+                   prefix: tuple = ()) -> ParticleBatch:
+    """One reference-arithmetic step of an explicit batch (prediction.py:165-211)."""
+    dev = device()
+    tab = action_tables(control_set, q, dt, dev)
+    beta_of, goal_of = hypothesis_arrays(space)
+    if batch.hypothesis_idx.max() >= len(beta_of):
+        raise ValueError("hypothesis index out of range for the space")
+    xy = torch.as_tensor(batch.xy.copy(), device=dev)
+    hyp = torch.as_tensor(batch.hypothesis_idx, device=dev)
+    db = torch.as_tensor(beta_of.astype(np.float32), device=dev)
+    dg = torch.as_tensor(np.ascontiguousarray(goal_of.astype(np.float32)), device=dev)
+    words = _prefix_words(prefix)
+    arr = (ctypes.c_uint32 * max(1, len(words)))(*words)
+    _lib.check(_lib.lib().gc_propagate_step(
+        ctypes.c_void_p(xy.data_ptr()), ctypes.c_void_p(hyp.data_ptr()), batch.n,
+        ctypes.c_void_p(db.data_ptr()), ctypes.c_void_p(dg.data_ptr()), len(beta_of),
+        ctypes.byref(tab.struct), None, int(seed) & _MASK64, arr, len(words), int(step),
+        stream_handle()), "propagate_step")
+    return ParticleBatch(xy.cpu().numpy(), batch.hypothesis_idx)
+
+
+def predict(z_history, belief: JointBelief, cfg: PredictionConfig, control_set: ControlSet, q: QFunction,
+            space: HypothesisSpace, grid_spec: GridSpec, workers: Optional[int] = None,
+            base_time: float = 0.0, prefix: tuple = ()) -> PredictionStack:
+    """Monte-Carlo occupancy prediction over cfg.steps steps (Alg. 1; prediction.py:223-255)."""
+    z0 = _as_state(z_history)
+    if len(belief) != space.size:
+        raise ValueError("belief size does not match hypothesis space")
+    dev = device()
+    tab = action_tables(control_set, q, cfg.dt, dev)
+    beta_of, goal_of = hypothesis_arrays(space)
+    job = HumanJob(z0, belief.log_weights, beta_of, goal_of, cfg.seed, tuple(prefix), 0)
+    out = run_predict([job], [tab], cfg.n, cfg.steps, cfg.dt, cfg.smoothing_sigma, grid_spec,
+                      getattr(cfg, "mode", "reference"))
+    return PredictionStack(grid_spec, out["layers"][0], base_time, cfg.dt)
+
+
+def predict_multi(humans: Sequence[tuple], cfg: PredictionConfig, control_set: ControlSet, q: QFunction,
+                  space: HypothesisSpace, grid_spec: GridSpec, workers: Optional[int] = None,
+                  base_time: float = 0.0) -> PredictionStack:
+    """Per-human prediction merged layer-wise by pointwise max (prediction.py:380-409):
+    one batched launch, union by the epilogue's atomicMax."""
+    if not humans:
+        raise ValueError("need at least one human")
+    dev = device()
+    tab = action_tables(control_set, q, cfg.dt, dev)
+    beta_of, goal_of = hypothesis_arrays(space)
+    jobs = []
+    for hist, b in humans:
+        if len(b) != space.size:
+            raise ValueError("belief size does not match hypothesis space")
+        jobs.append(HumanJob(_as_state(hist), b.log_weights, beta_of, goal_of, cfg.seed, (), 0))
+    out = run_predict(jobs, [tab], cfg.n, cfg.steps, cfg.dt, cfg.smoothing_sigma, grid_spec,
+                      getattr(cfg, "mode", "reference"), per_human_layers=False, union64=True)
+    return PredictionStack(grid_spec, out["union64"], base_time, cfg.dt)
+
+
+def total_variation(a, b) -> float:
+    return 0.5 * float(np.abs(np.asarray(a, dtype=float) - np.asarray(b, dtype=float)).sum())

@@ -1,0 +1,172 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference's golden vectors and
+the oracle restatement.  Reference RNG mode must reproduce counts bit-for-bit."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_01122_b200 as G  # noqa: E402
+from paper_2603_01122_b200 import prediction as PR  # noqa: E402
+
+
+def _objects(case):
+    m = case.meta
+    cs = G.ControlSet([G.ControlAction(float(v), float(t)) for v, t in zip(m["v"], m["theta"])])
+    space = G.HypothesisSpace(G.RationalitySet(tuple(m["betas"])), G.GoalSet(np.array(m["goals"])))
+    qd = m["q"]
+    if qd["family"] == "goal_progress":
+        q = G.q_goal_progress(qd["tau"], (qd["w_v"], qd["w_th"]))
+    else:
+        q = G.q_default((qd["w_v"], qd["w_th"]))
+    if qd["v_threshold"] is not None:
+        q = G.mask_stationary(q, cs, qd["v_threshold"])
+    W, H, res, org = case.grid
+    spec = G.GridSpec(W, H, res, org)
+    return cs, space, q, spec
+
+
+def full_counts(out, jobs, spec, steps):
+    """Expand the windowed count buffer into (humans, T, H, W)."""
+    geo = out["geometry"]
+    c = out["counts"].cpu().numpy().view(np.uint32)
+    res = np.zeros((len(jobs), steps, spec.height, spec.width), dtype=np.int64)
+    for h, j in enumerate(jobs):
+        for t in range(steps):
+            x0, y0, w, hh = geo.window((np.float32(j.z0.x), np.float32(j.z0.y)), t)
+            base = h * geo.human_stride + geo.step_off[t]
+            res[h, t, y0:y0 + hh, x0:x0 + w] = c[base:base + w * hh].reshape(hh, w)
+    return res
+
+
+@pytest.mark.parametrize("name", golden_io.predict_case_names())
+def test_predict_reference_mode_bit_exact(name):
+    case = golden_io.PredictCase(name)
+    cs, space, q, spec = _objects(case)
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, case.dt, dev)
+    # tables computed on this host equal the reference's (else the box's numpy differs)
+    np.testing.assert_array_equal(tab.disp_np, case.ref_disp)
+    bo, go = space.beta_of, space.goal_xy_of
+    job = PR.HumanJob(G.HumanState(*case.z0), case.log_w, bo, go, case.seed, case.prefix, 0)
+    out = PR.run_predict([job], [tab], case.n, case.steps, case.dt, case.sigma, spec, "reference",
+                         want_hyp=True, want_xy=True)
+    np.testing.assert_array_equal(out["hyp"][0].cpu().numpy(), case.hyp)
+    np.testing.assert_array_equal(out["xy"][0].cpu().numpy(), case.xy_last)
+    counts = full_counts(out, [job], spec, case.steps)[0]
+    np.testing.assert_array_equal(counts, case.counts())
+    layers = out["layers"][0].cpu().numpy()
+    got = layers[case.layer_steps]
+    if case.sigma == 0:
+        np.testing.assert_array_equal(got, case.layers)
+    else:
+        np.testing.assert_allclose(got, case.layers, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(layers.sum(axis=(1, 2)), case.layer_sums, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["cfg1_s0", "ragged_w", "masked", "qdefault", "lattice"])
+def test_public_predict_and_helpers(name):
+    case = golden_io.PredictCase(name)
+    cs, space, q, spec = _objects(case)
+    b = G.JointBelief(case.log_w)
+    cfg = G.PredictionConfig(n=case.n, steps=case.steps, dt=case.dt, smoothing_sigma=case.sigma,
+                             seed=case.seed)
+    st = G.predict(G.HumanState(*case.z0), b, cfg, cs, q, space, spec, prefix=case.prefix)
+    if case.sigma == 0:
+        np.testing.assert_array_equal(st.layers[case.layer_steps], case.layers)
+    else:
+        np.testing.assert_allclose(st.layers[case.layer_steps], case.layers, rtol=0, atol=1e-15)
+    hyp = G.sample_hypotheses(b, case.n, case.seed, prefix=case.prefix)
+    np.testing.assert_array_equal(hyp, case.hyp)
+    batch = G.ParticleBatch.duplicated(G.HumanState(*case.z0), hyp)
+    batch = G.propagate_step(batch, cs, q, space, case.dt, case.seed, step=1, prefix=case.prefix)
+    np.testing.assert_array_equal(batch.xy, case.xy_first)
+
+
+def test_belief_update_chains():
+    z = golden_io.load("belief.npz")
+    meta = json.loads(str(z["meta"]))
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    space = G.HypothesisSpace(G.RationalitySet(tuple(meta["betas"])), G.GoalSet(np.array(meta["goals"])))
+    worst = 0.0
+    for chain in meta["chains"]:
+        qd = chain["q"]
+        if qd["family"] == "goal_progress":
+            q = G.q_goal_progress(qd["tau"], (qd["w_v"], qd["w_th"]))
+        else:
+            q = G.q_default((qd["w_v"], qd["w_th"]))
+        if qd["v_threshold"] is not None:
+            q = G.mask_stationary(q, cs, qd["v_threshold"])
+        for row in chain["rows"]:
+            prior = G.JointBelief(np.array(row["prior"]))
+            zt, zn = G.HumanState(*row["z"]), G.HumanState(*row["zn"])
+            tol = None
+            if row["status"] == 1:
+                with pytest.raises(G.ControlSnapMismatch):
+                    G.update_belief(prior, zt, zn, meta["dt"], cs, q, space, fallback_theta=row["heading"])
+                tol = math.inf
+            post = G.update_belief(prior, zt, zn, meta["dt"], cs, q, space, fallback_theta=row["heading"],
+                                   snap_tol=tol)
+            ref = np.array(row["post"])
+            fin = np.isfinite(ref)
+            np.testing.assert_array_equal(np.isfinite(post.log_weights), fin)
+            pr, pg = np.exp(ref[fin]), np.exp(post.log_weights[fin])
+            rel = np.max(np.abs(pg - pr) / np.maximum(pr, 1e-300))
+            worst = max(worst, rel)
+    assert worst < 1e-5, worst  # north-star bound; observed ~1e-13
+
+
+def test_multi_union_time_union():
+    z = golden_io.load("multi.npz")
+    meta = json.loads(str(z["meta"]))
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    spec = G.GridSpec(100, 100, 0.1)
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, meta["dt"], dev)
+    jobs = []
+    for i, hm in enumerate(meta["humans"]):
+        space = G.HypothesisSpace(G.RationalitySet.log_spaced(5), G.GoalSet(np.array(hm["goals"])))
+        jobs.append(PR.HumanJob(G.HumanState(*hm["start"]), np.array(hm["log_w"]), space.beta_of,
+                                space.goal_xy_of, int(meta["seed"]), (2, i), 0))
+    out = PR.run_predict(jobs, [tab], meta["n"], meta["steps"], meta["dt"], meta["sigma"], spec,
+                         "reference", per_human_layers=False, union64=True)
+    np.testing.assert_allclose(out["union64"].cpu().numpy(), z["union"], rtol=0, atol=1e-15)
+    out = PR.run_predict(jobs, [tab], meta["n"], meta["steps"], meta["dt"], meta["sigma"], spec,
+                         "reference", per_human_layers=False, union64=True, union32=True, time_union=True)
+    np.testing.assert_allclose(out["union64"].cpu().numpy(), z["time_union"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(out["union32"].cpu().numpy(), z["time_union"].astype(np.float32), rtol=0,
+                               atol=1e-7)
+
+
+def test_predict_multi_semantics():
+    case = golden_io.PredictCase("lattice")
+    cs, space, q, spec = _objects(case)
+    b = G.init_belief(space)
+    cfg = G.PredictionConfig(n=2048, steps=3, dt=1.0, smoothing_sigma=0.0, seed=21)
+    z0 = G.HumanState(4.5, 4.5)
+    merged = G.predict_multi([(z0, b)], cfg, cs, q, space, spec)
+    single = G.predict(z0, b, cfg, cs, q, space, spec)
+    np.testing.assert_array_equal(merged.layers, single.layers)
+    merged2 = G.predict_multi([(z0, b), (z0, b)], cfg, cs, q, space, spec)
+    np.testing.assert_array_equal(merged2.layers, single.layers)
+
+
+def test_smoothing_and_emplace_helpers():
+    z = golden_io.load("smooth.npz")
+    items = json.loads(str(z["meta"]))
+    off = 0
+    for w, h, res, sig in items:
+        x = z["x"][off:off + w * h].reshape(h, w)
+        y = z["y"][off:off + w * h].reshape(h, w)
+        off += w * h
+        np.testing.assert_allclose(G.smooth_values(x, G.GridSpec(w, h, res), sig), y, rtol=0, atol=1e-15)
+    spec = G.GridSpec(4, 4, 1.0)
+    g = G.emplace(G.ParticleBatch(np.array([[-3.0, 9.0], [2.5, 2.5]], np.float32), np.zeros(2, np.int32)), spec)
+    assert g.at(0, 3) == 0.5 and g.at(2, 2) == 0.5
