@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark: the full predict+update cycle of BASELINE.json configs[2] (cfg3) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one prediction cycle: belief update of every human (K1) + prediction of
+every human (K2: 262,144 particles x 250 steps, dt 0.02) + smoothing and max-union into
+the shared 400x400 grid (K3).  N GPUs: weak scaling, 8 humans per rank; with N > 1 the
+per-rank unions are merged into one fused grid by an NCCL max-reduce each cycle.
+
+``value``  -- particle-steps/s of the whole job, inputs resident in HBM (CUDA graph
+              replay, CUDA events, max over ranks);  ``hz`` = cycles/s, ``p99_ms``.
+``e2e``    -- the same metric with the cycle's observations copied from pinned host
+              memory and the fused float32 (T, H, W) union read back to pinned host
+              memory every cycle (double-buffered on a copy stream).
+``--impl reference`` times the reference CPU implementation (oracle/port.py, a
+restatement pinned bit-exact to the reference) on the host cores on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # fair CPU timing
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "particle-steps/s"
+# reference-algorithm work per particle-step: 9m+10 FP32 ops, m = 96
+REF_OPS_PER_PSTEP = 9 * 96 + 10
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback"}
+    f = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(f):
+        d = json.load(open(f))
+        p.update({k: d[k] for k in ("hbm_gbs", "sm_max_mhz") if k in d})
+        p["source"] = "measured"
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU baseline: the reference CPU cycle (oracle/port.py) on a bounded sample of cfg3
+# ---------------------------------------------------------------------------------------
+def cpu_sample(scene, t_steps=10, reps=3, workers=None):
+    """Time 1 human x n particles x t_steps (+ one belief update) with the reference CPU
+    path; extrapolate linearly in T and in humans (predict is linear in both,
+    cli.py:135-146) to one full cycle."""
+    from oracle import model, port
+    from oracle.predict import Grid, belief_update
+    workers = workers or (os.cpu_count() or 1)
+    cs = scene.control_set
+    tb = model.make_tables(cs.v, cs.theta, scene.dt, model.QSpec("goal_progress", 0.5))
+    sp = scene.spaces[0]
+    beta_of, goal_of = sp.beta_of, sp.goal_xy_of
+    lw = np.full(len(beta_of), -np.log(len(beta_of)))
+    grid = Grid(scene.spec.width, scene.spec.height, scene.spec.resolution)
+    prev, obs = scene.prev_xy[0], scene.track[0][0]
+    t_upd, t_pred = [], []
+    for r in range(reps + 1):
+        t0 = time.perf_counter()
+        post, _ = belief_update(lw, prev, obs, 0.1, cs.v, cs.theta, model.QSpec("goal_progress", 0.5),
+                                beta_of, goal_of, 0.0, snap_tol=float("inf"))
+        t1 = time.perf_counter()
+        port.predict(obs, post, scene.n, t_steps, scene.dt, 0.1, 0, tb, beta_of, goal_of, grid,
+                     prefix=(2, 0), workers=workers)
+        t2 = time.perf_counter()
+        if r > 0:
+            t_upd.append(t1 - t0)
+            t_pred.append(t2 - t1)
+    H = len(scene.spaces)
+    cycle_s = H * (float(np.median(t_upd)) + float(np.median(t_pred)) * scene.steps / t_steps)
+    psteps = H * scene.n * scene.steps
+    return {
+        "value": psteps / cycle_s, "unit": UNIT, "cores": workers, "kind": "port",
+        "hz": 1.0 / cycle_s, "cycle_s": cycle_s,
+        "sample": (f"1 human x {scene.n} particles x {t_steps} steps + 1 belief update, median of {reps}; "
+                   f"extrapolated x{H} humans x{scene.steps // t_steps} in T (reference CPU path restated "
+                   f"in oracle/port.py, ThreadPool {workers} workers, OPENBLAS_NUM_THREADS=1)"),
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2603_01122_b200.scenario import make_scene
+    scene = make_scene(args.config, cycles=2)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(scene, t_steps=args.cpu_t, reps=1)
+        if i >= args.warmup:
+            vals.append(r)
+    v = float(np.median([r["value"] for r in vals]))
+    cycle_s = float(np.median([r["cycle_s"] for r in vals]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cycle_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "hz": 1.0 / cycle_s,
+        "config": {"workload": f"{args.config}: 8 humans x 262144 particles x 250 steps dt 0.02, 400x400 union",
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2603_01122_b200 import _lib
+    from paper_2603_01122_b200.engine import CycleEngine, EngineConfig, fused_reduce
+    from paper_2603_01122_b200.scenario import make_scene
+
+    K, W = args.steps, args.warmup
+    scene = make_scene(args.config, cycles=W + K + 4, humans=8, human_offset=8 * rank)
+    cfg = EngineConfig(n=scene.n, steps=scene.steps, dt=scene.dt, smoothing_sigma=0.1, seed=0,
+                       mode=args.mode, time_union=False)
+    eng = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec, cfg)
+    # posterior after 10 observations (also warms every kernel)
+    eng.prime(scene.warmup_track[0])
+    for k in range(1, 11):
+        eng.stage(scene.warmup_track[k], buf=k % 2)
+        eng.run_cycle(buf=k % 2)
+    torch.cuda.synchronize()
+    eng.check_errors()
+    fused = world > 1 and not args.no_fused
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.Stream()
+    # ---- kernel timing (eager cycles, events on the launching stream) ----
+    n_k = max(3, min(K, 10))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_k)]
+    for i in range(n_k):
+        eng.run_cycle(buf=0, with_h2d=False, stream=stream, events=ev[i])
+    stream.synchronize()
+    k2_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    k3_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+
+    # ---- value: device-resident cycle (CUDA graph replay) ----
+    g = eng.capture(buf=0, with_h2d=False)
+    cyc_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            g.replay()
+            if fused:
+                fused_reduce(eng.unions[0], dst=0)
+    launches0 = _lib.lib().gc_launch_count()
+    barrier()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            t_start.record(stream)
+            for i in range(K):
+                cyc_ev[i][0].record(stream)
+                g.replay()
+                if fused:
+                    fused_reduce(eng.unions[0], dst=0)
+                cyc_ev[i][1].record(stream)
+            t_end.record(stream)
+        barrier()
+    ms = t_start.elapsed_time(t_end) / K
+    ms = max_over_ranks(ms)
+    per_cycle = [a.elapsed_time(b) for a, b in cyc_ev]
+    p99 = max_over_ranks(float(np.percentile(per_cycle, 99)))
+    p50 = max_over_ranks(float(np.percentile(per_cycle, 50)))
+    # graph replays do not pass through the C ABI launch counter: 3 kernels per cycle
+    # (K1 belief, K2 predict, K3 epilogue) are captured in the graph
+    gpu_launches = 3 * K
+    assert _lib.lib().gc_launch_count() == launches0  # nothing eager snuck in
+
+    # ---- e2e: pinned H2D of observations + D2H of the fused union every cycle ----
+    ga = [eng.capture(buf=b, with_h2d=True) for b in (0, 1)]
+    copy = torch.cuda.Stream()
+    u0 = eng.unions[0]
+    h_out = [torch.empty(u0.shape, dtype=u0.dtype).pin_memory() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    copied = [torch.cuda.Event() for _ in range(2)]
+    staged_ok = [torch.cuda.Event() for _ in range(2)]
+    tr = scene.track
+    h2d = eng._nb
+    d2h = u0.numel() * u0.element_size()
+    lat = []
+
+    def e2e_loop(n_cycles, base, timed):
+        e2e_ev = []
+        for i in range(n_cycles):
+            b = i % 2
+            staged_ok[b].synchronize()          # pinned input b free again
+            eng.stage(tr[(base + i) % len(tr)], buf=b)
+            with torch.cuda.stream(stream):
+                stream.wait_event(copied[b])    # union b drained to host
+                s_ev = torch.cuda.Event(enable_timing=True)
+                s_ev.record(stream)
+                ga[b].replay()
+                staged_ok[b].record(stream)
+                if fused:
+                    fused_reduce(eng.unions[b], dst=0)
+                done[b].record(stream)
+            with torch.cuda.stream(copy):
+                copy.wait_event(done[b])
+                if rank == 0 or not fused:
+                    h_out[b].copy_(eng.unions[b], non_blocking=True)
+                e_ev = torch.cuda.Event(enable_timing=True)
+                e_ev.record(copy)
+                copied[b].record(copy)
+            e2e_ev.append((s_ev, e_ev))
+        return e2e_ev
+
+    e2e_loop(W, 0, False)
+    barrier()
+    copy.synchronize()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    evs = e2e_loop(K, W, True)
+    stream.wait_stream(copy)
+    e_end.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e_start.elapsed_time(e_end) / K)
+    lat = [a.elapsed_time(b) for a, b in evs]
+    e2e_p99 = max_over_ranks(float(np.percentile(lat, 99)))
+    eng.check_errors()
+
+    psteps_rank = len(scene.spaces) * scene.n * scene.steps
+    psteps = psteps_rank * world
+    value = psteps / (ms * 1e-3)
+    pk = peaks()
+    clk = clocks.summary()
+    sm_mhz = pk["sm_max_mhz"]
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s at the max SM clock
+    k2_achieved = psteps_rank * REF_OPS_PER_PSTEP / (k2_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    ncu = None
+    if os.path.exists(prof):
+        try:
+            ncu = json.load(open(prof)).get(args.mode, {}).get("k_predict")
+            traffic = ncu.get("dram_bytes_per_launch") if ncu else None
+        except (ValueError, AttributeError):
+            ncu = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "hz": 1000.0 / ms, "p50_ms": p50, "p99_ms": p99,
+        "config": {
+            "workload": (f"{args.config}: {len(scene.spaces)} humans/GPU x {scene.n} particles x {scene.steps} "
+                         f"steps dt {scene.dt}, |H|=20, |U|=96, 400x400 @0.1 m union, sigma 0.1 m, "
+                         f"update+predict per cycle"),
+            "mode": args.mode, "humans": len(scene.spaces) * world, "particles": scene.n,
+            "horizon": scene.steps, "grid": [scene.spec.width, scene.spec.height],
+            "fused_grid_nccl": fused, "parallelism": f"humans sharded over {world} GPU(s)",
+            "l2": "per-cycle working set > L2: 160 MB union + counts rewritten each cycle (no explicit flush)",
+        },
+        "e2e": {"value": psteps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h if (rank == 0 or not fused) else 0,
+                "hz": 1000.0 / e2e_ms, "p99_latency_ms": e2e_p99,
+                "note": "pinned obs H2D + fused f32 union D2H each cycle, D2H overlapped with next cycle"},
+        "gpu_launches": gpu_launches,
+        "kernels_ms": {"k_predict": k2_ms, "k_epilogue": k3_ms},
+        "roofline": {
+            "bound": "fp32", "kernel": "k_predict",
+            "achieved": k2_achieved, "peak": fp32_peak, "unit": "Tops/s", "frac": k2_achieved / fp32_peak,
+            "traffic": traffic,
+            "work": (f"reference-algorithm-equivalent: {REF_OPS_PER_PSTEP} FP32 ops per particle-step "
+                     f"(9m+10, m=96, SURVEY 8d) x {psteps_rank} particle-steps per launch; the factorised "
+                     f"production sampler executes fewer ops, so frac > 1 is possible"),
+            "peak_source": f"148 SM x 128 FP32 lanes x {sm_mhz:.0f} MHz ({pk['source']} sm_max_mhz)",
+            "ncu": ncu,
+        },
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline and rank == 0:
+        line["cpu_baseline"] = cpu_sample(scene, t_steps=args.cpu_t, reps=3)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--mode", default="production", choices=["production", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--cpu-t", type=int, default=10)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -70,6 +70,9 @@ typedef struct {
     float dv, tau, w_v, w_th;
     const float *d_cos_h, *d_sin_h, *d_theta_h; /* (n_headings,) */
     const int32_t *d_a_index;                   /* (n_speeds*n_headings,) or NULL */
+    /* optional HOST copies of the heading tables: when set, gc_predict never reads the
+     * device copies back, so the call is CUDA-graph capturable */
+    const float *h_cos_h, *h_sin_h, *h_theta_h;
 } gc_action_table;
 
 /* Batched Alg. 1 (prediction.py:223-255, sim.py:489-499): every human h of the batch

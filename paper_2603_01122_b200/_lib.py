@@ -47,6 +47,7 @@ class ActionTable(ctypes.Structure):
         ("n_speeds", I32), ("n_headings", I32),
         ("dv", F32), ("tau", F32), ("w_v", F32), ("w_th", F32),
         ("d_cos_h", P), ("d_sin_h", P), ("d_theta_h", P), ("d_a_index", P),
+        ("h_cos_h", P), ("h_sin_h", P), ("h_theta_h", P),
     ]
 
 

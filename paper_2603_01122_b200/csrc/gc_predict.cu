@@ -30,7 +30,7 @@ constexpr int MAXH = 128;      // max hypotheses per human
 constexpr int NBF = 24;        // headings of the factorised sampler (ControlSet.grid default)
 constexpr int NAF = 4;         // max speeds of the factorised sampler
 
-enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2 };
+enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2, MODE_FACTS = 3 };  // FACTS: standard headings
 
 struct KTable {
     int m, m_keep, q_kind, n_speeds, n_headings;
@@ -167,14 +167,33 @@ __device__ __forceinline__ int gen_pick(const SmemTabs &S, float x, float y, int
 //   G_a = exp(a k r - c a^2 - S),     S = max_a (a k r - c a^2),  H_b = exp(-beta w_th th_b^2)
 // -> per step: NB ex2 (e_b), 4 ex2 (G_a), Horner in e_b, inverse CDF over headings then
 //    over speeds.  Zero-speed actions share displacement 0 and merge into one "stay".
-template <bool WTH>
+// the standard ControlSet.grid heading set theta_b = -pi + b*pi/12 (agents.py:79-87),
+// float32 cos/sin as the host computes them; compiled in so the heading loop uses
+// immediate operands instead of constant-bank loads
+#define GC_STD_COS                                                                                  \
+    {-1.f, -0.965925813f, -0.866025388f, -0.707106769f, -0.5f, -0.258819044f, 6.12323426e-17f,     \
+     0.258819044f, 0.5f, 0.707106769f, 0.866025388f, 0.965925813f, 1.f, 0.965925813f, 0.866025388f, \
+     0.707106769f, 0.5f, 0.258819044f, 6.12323426e-17f, -0.258819044f, -0.5f, -0.707106769f,       \
+     -0.866025388f, -0.965925813f}
+#define GC_STD_SIN                                                                                  \
+    {-1.22464685e-16f, -0.258819044f, -0.5f, -0.707106769f, -0.866025388f, -0.965925813f, -1.f,    \
+     -0.965925813f, -0.866025388f, -0.707106769f, -0.5f, -0.258819044f, 0.f, 0.258819044f, 0.5f,   \
+     0.707106769f, 0.866025388f, 0.965925813f, 1.f, 0.965925813f, 0.866025388f, 0.707106769f, 0.5f, \
+     0.258819044f}
+__device__ constexpr float kStdCos[NBF] = GC_STD_COS;
+__device__ constexpr float kStdSin[NBF] = GC_STD_SIN;
+static const float hStdCos[NBF] = GC_STD_COS;
+static const float hStdSin[NBF] = GC_STD_SIN;
+
+template <bool STDH, bool WTH>
 __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, float &x, float &y,
                                           int h, float u1, float u2) {
     const float rx = x - S.hgx[h], ry = y - S.hgy[h];
     const float r2 = fmaf(rx, rx, ry * ry);
-    const float r = r2 > 0.f ? r2 * rsqrtf(r2) : 0.f;
+    const float r = r2 * rsqrtf(fmaxf(r2, 1e-30f));
     const float kk = S.hk[h], c2 = S.hc2[h];
     const float kr = kk * r;
+    const float A = -kk * rx, B = -kk * ry, nkr = -kr;
     const int na = S.n_speeds;
     const float s1 = kr - c2, s2 = fmaf(2.f, kr, -4.f * c2), s3 = fmaf(3.f, kr, -9.f * c2);
     float Smax = fmaxf(0.f, s1);
@@ -186,36 +205,60 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     const float G3 = na > 3 ? ex2_approx(s3 - Smax) : 0.f;
     float cum[NBF];
     float C = 0.f;
-    const float nkr = -kr;
 #pragma unroll
     for (int b = 0; b < NBF; ++b) {
-        const float d = fmaf(rx, P.hcos[b], ry * P.hsin[b]);
-        const float e = ex2_approx(fmaf(-kk, d, nkr));
-        float m = e * fmaf(e, fmaf(e, G3, G2), G1);
-        if (WTH) m *= ex2_approx(-S.wth * S.hb[h] * P.hth2[b]);
-        C += m;
+        const float cb = STDH ? kStdCos[b] : P.hcos[b];
+        const float sb = STDH ? kStdSin[b] : P.hsin[b];
+        // e_b = exp(-k (d_b + r)), d_b = rel . (cos th_b, sin th_b): 2 FFMA + 1 MUFU
+        const float e = ex2_approx(fmaf(A, cb, fmaf(B, sb, nkr)));
+        // cumulative moving weight: C += H_b e (G1 + e (G2 + e G3)), 3 FFMA
+        const float poly = fmaf(e, fmaf(e, G3, G2), G1);
+        if (WTH) C = fmaf(e * ex2_approx(-S.wth * S.hb[h] * P.hth2[b]), poly, C);
+        else C = fmaf(e, poly, C);
         cum[b] = C;
     }
     const float Z0 = G0 * S.hsumH[h];
     const float rr = u1 * (Z0 + C);
-    if (rr < Z0) return;  // stay: every zero-speed action has displacement 0
     const float t = rr - Z0;
+    // heading = #{b : cum_b <= t}: cum is monotone, so halve the candidate set with one
+    // compare + selects per level (24 -> 12 -> 6 -> 3), then count the last three
     int b = 0;
+    {
+        bool p = cum[11] <= t;
+        b += p ? 12 : 0;
 #pragma unroll
-    for (int bb = 0; bb < NBF; ++bb) b += (cum[bb] <= t) ? 1 : 0;
+        for (int i = 0; i < 12; ++i) cum[i] = p ? cum[i + 12] : cum[i];
+        p = cum[5] <= t;
+        b += p ? 6 : 0;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) cum[i] = p ? cum[i + 6] : cum[i];
+        p = cum[2] <= t;
+        b += p ? 3 : 0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) cum[i] = p ? cum[i + 3] : cum[i];
+        b += (cum[0] <= t ? 1 : 0) + (cum[1] <= t ? 1 : 0) + (cum[2] <= t ? 1 : 0);
+    }
     b = b < NBF - 1 ? b : NBF - 1;
-    const float d = fmaf(rx, P.hcos[b], ry * P.hsin[b]);
-    const float e = ex2_approx(fmaf(-kk, d, nkr));
+    const float e = ex2_approx(fmaf(A, P.hcos[b], fmaf(B, P.hsin[b], nkr)));
     const float w1 = G1 * e, w2 = G2 * e * e, w3 = G3 * e * e * e;
     const float r2u = u2 * (w1 + w2 + w3);
     int a = 1 + ((w1 <= r2u) ? 1 : 0) + ((w1 + w2 <= r2u) ? 1 : 0);
     a = a < na - 1 ? a : na - 1;
-    x += S.fdx[a * NBF + b];
-    y += S.fdy[a * NBF + b];
+    // stay (rr < Z0): every zero-speed action has displacement 0 -- branch-free select
+    const bool stay = rr < Z0;
+    const float dx = S.fdx[a * NBF + b], dy = S.fdy[a * NBF + b];
+    x += stay ? 0.f : dx;
+    y += stay ? 0.f : dy;
+}
+
+// shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
+// particles, so a per-CTA cell count cannot overflow its half-word)
+__device__ __forceinline__ void win_add(unsigned *win, int local, unsigned cnt) {
+    atomicAdd(&win[local >> 1], cnt << ((local & 1) << 4));
 }
 
 template <int MODE, int K>
-__global__ void __launch_bounds__(NT) k_predict(const KParams P) {
+__global__ void __launch_bounds__(NT, 3) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ SmemTabs S;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -229,18 +272,18 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
     // ---- stage tables in shared memory ----
     if (tid == 0) {
         S.n_hyp = nh; S.m_keep = T.m_keep; S.q_kind = T.q_kind; S.n_speeds = T.n_speeds;
-        S.wth = T.w_th;
-        S.list_n[0] = 0; S.list_n[1] = 0;
+        S.wth = T.w_th * 1.4426950408889634f;
     }
-    for (int k = tid; k < T.m_keep; k += NT) {
-        const int j = __ldg(&T.keep[k]);
-        S.ax[k] = __ldg(&T.sx[j]);
-        S.ay[k] = __ldg(&T.sy[j]);
-        S.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? __ldg(&T.pen[j]) : __ldg(&T.at[j]);
-        S.adx[k] = __ldg(&T.dispx[j]);
-        S.ady[k] = __ldg(&T.dispy[j]);
-    }
-    if (MODE == MODE_FACT) {
+    if (MODE != MODE_FACT && MODE != MODE_FACTS) {
+        for (int k = tid; k < T.m_keep; k += NT) {
+            const int j = __ldg(&T.keep[k]);
+            S.ax[k] = __ldg(&T.sx[j]);
+            S.ay[k] = __ldg(&T.sy[j]);
+            S.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? __ldg(&T.pen[j]) : __ldg(&T.at[j]);
+            S.adx[k] = __ldg(&T.dispx[j]);
+            S.ady[k] = __ldg(&T.dispy[j]);
+        }
+    } else {
         for (int i = tid; i < NAF * NBF; i += NT) {
             const int a = i / NBF;
             const int j = a < T.n_speeds ? __ldg(&T.a_index[i]) : -1;
@@ -253,7 +296,7 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
         S.hb[i] = b;
         S.hgx[i] = __ldg(&P.goal32[2 * (h0 + i)]);
         S.hgy[i] = __ldg(&P.goal32[2 * (h0 + i) + 1]);
-        if (MODE == MODE_FACT) {
+        if (MODE == MODE_FACT || MODE == MODE_FACTS) {
             const float L2E = 1.4426950408889634f;
             S.hk[i] = 2.f * b * T.tau * T.dv * L2E;
             S.hc2[i] = b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E;
@@ -272,18 +315,11 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
             S.cdf[nh - 1] = 1.0;
         }
     }
-    if (MODE == MODE_FACT && T.w_th != 0.f) {
-        // pre-scale theta^2 by log2(e) once: hth2 already holds theta^2; fold beta*w_th*L2E
-        if (tid == 0) S.wth = T.w_th * 1.4426950408889634f;
-    }
-    unsigned *win_s = reinterpret_cast<unsigned *>(smem_dyn);
-    int *list = reinterpret_cast<int *>(smem_dyn) + (P.smem_window ? 0 : 0);
-    int max_cells = 0;
+    unsigned *win = reinterpret_cast<unsigned *>(smem_dyn);
     if (P.smem_window) {
-        max_cells = (2 * __ldg(&P.step_r[P.steps - 1]) + 1);
-        max_cells *= max_cells;
-        list = reinterpret_cast<int *>(win_s + max_cells);
-        for (int i = tid; i < max_cells; i += NT) win_s[i] = 0u;
+        const int R = __ldg(&P.step_r[P.steps - 1]);
+        const int words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
+        for (int i = tid; i < words; i += NT) win[i] = 0u;
     }
     __syncthreads();
 
@@ -292,13 +328,17 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
     int cx, cy;
     cell_ref(sx0, sy0, P, cx, cy);
     const unsigned long long seed = __ldg(&P.seed[h]);
-    const int plen = __ldg(&P.prefix_len[h]);
-    SSPool pool_pre = ss_pool_init(seed);
-    for (int i = 0; i < plen; ++i) ss_absorb(pool_pre, __ldg(&P.prefix[4 * h + i]));
+    const unsigned sk_lo = (unsigned)seed, sk_hi = (unsigned)(seed >> 32);
+    SSPool pool_pre;
+    if (MODE == MODE_REF) {
+        pool_pre = ss_pool_init(seed);
+        const int plen = __ldg(&P.prefix_len[h]);
+        for (int i = 0; i < plen; ++i) ss_absorb(pool_pre, __ldg(&P.prefix[4 * h + i]));
+    }
 
     float px[K], py[K];
     int ph[K];
-    U4 rnd[K];
+    unsigned rz[K], rw[K];  // the unused half of the last Philox4x32 block (odd steps)
     const int pbase = blk * P.ppc;
     {
         uint64_t hk0 = 0, hk1 = 0;
@@ -310,9 +350,8 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
-            px[k] = sx0; py[k] = sy0; ph[k] = 0;
-            rnd[k] = U4{0, 0, 0, 0};
-            if (p >= P.n) continue;
+            px[k] = sx0; py[k] = sy0; ph[k] = 0; rz[k] = 0u; rw[k] = 0u;
+            if (p >= P.n || k * NT + tid >= P.ppc) continue;
             int hi;
             if (P.hyp_in) {
                 hi = __ldg(&P.hyp_in[(long long)h * P.n + p]);
@@ -321,8 +360,7 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
                 if (P.hyp_u) u = __ldg(&P.hyp_u[(long long)h * P.n + p]);
                 else if (MODE == MODE_REF) u = philox64_f64(hk0, hk1, (uint64_t)p);
                 else {
-                    const U4 o = philox4x32(U4{(unsigned)p, 0xFFFFFFFFu, (unsigned)h, 0x5EEDu},
-                                            (unsigned)seed, (unsigned)(seed >> 32));
+                    const U4 o = philox4x32(U4{(unsigned)p, 0xFFFFFFFFu, (unsigned)h, 0x5EEDu}, sk_lo, sk_hi);
                     u = ((double)(o.x >> 5) * 67108864.0 + (double)(o.y >> 6)) * (1.0 / 9007199254740992.0);
                 }
                 hi = 0;
@@ -333,8 +371,8 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
             if (P.hyp_out) P.hyp_out[(long long)h * P.n + p] = hi;
         }
     }
-    SSPool pool_step = pool_pre;
-    if (MODE == MODE_REF) ss_absorb(pool_step, 1u);  // STEP_DRAWS namespace
+    SSPool pool_step;
+    if (MODE == MODE_REF) { pool_step = pool_pre; ss_absorb(pool_step, 1u); }  // STEP_DRAWS
 
     const long long hbase = (long long)h * P.human_stride;
     for (int t = 1; t <= P.steps; ++t) {
@@ -348,47 +386,56 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
-            const bool valid = p < P.n;
+            const bool valid = p < P.n && k * NT + tid < P.ppc;
             int local = -1;
-            if (valid) {
+            if (MODE != MODE_REF) {
+                // production: padded lanes compute too (no divergence), they just do not count
                 float x = px[k], y = py[k];
-                if (MODE == MODE_REF) {
-                    float u;
-                    if (P.uniforms) {
-                        u = __ldg(&P.uniforms[((long long)h * P.steps + (t - 1)) * P.n + p]);
-                    } else {
-                        const int c = p >> 10;
-                        if (c != key_chunk) {
-                            SSPool s = pool_step;
-                            ss_absorb(s, (unsigned)t);
-                            ss_absorb(s, (unsigned)c);
-                            ss_key(s, sk0, sk1);
-                            key_chunk = c;
-                        }
-                        u = philox64_f32(sk0, sk1, (uint64_t)(p & 1023));
-                    }
-                    const int a = ref_pick(S, x, y, ph[k], u);
-                    x = __fadd_rn(x, S.adx[a]);
-                    y = __fadd_rn(y, S.ady[a]);
+                unsigned ua, ub;
+                if ((t & 1) == 1) {
+                    const U4 o = philox4x32(U4{(unsigned)p, (unsigned)(t >> 1), (unsigned)h, 0xA11CEu}, sk_lo, sk_hi);
+                    ua = o.x; ub = o.y; rz[k] = o.z; rw[k] = o.w;
                 } else {
-                    if (((t - 1) & 1) == 0)
-                        rnd[k] = philox4x32(U4{(unsigned)p, (unsigned)((t - 1) >> 1), (unsigned)h, 0xA11CEu},
-                                            (unsigned)seed, (unsigned)(seed >> 32));
-                    const uint32_t ua = ((t - 1) & 1) ? rnd[k].z : rnd[k].x;
-                    const uint32_t ub = ((t - 1) & 1) ? rnd[k].w : rnd[k].y;
-                    if (MODE == MODE_FACT) {
-                        if (S.wth != 0.f) fact_step<true>(S, P, x, y, ph[k], u24(ua), u24(ub));
-                        else fact_step<false>(S, P, x, y, ph[k], u24(ua), u24(ub));
-                    } else {
-                        const int a = gen_pick(S, x, y, ph[k], u24(ua));
-                        x += S.adx[a];
-                        y += S.ady[a];
-                    }
+                    ua = rz[k]; ub = rw[k];
+                }
+                if (MODE == MODE_FACT || MODE == MODE_FACTS) {
+                    constexpr bool STDH = MODE == MODE_FACTS;
+                    if (S.wth != 0.f) fact_step<STDH, true>(S, P, x, y, ph[k], u24(ua), u24(ub));
+                    else fact_step<STDH, false>(S, P, x, y, ph[k], u24(ua), u24(ub));
+                } else {
+                    const int a = gen_pick(S, x, y, ph[k], u24(ua));
+                    x += S.adx[a];
+                    y += S.ady[a];
                 }
                 px[k] = x; py[k] = y;
                 int ix, iy;
-                if (MODE == MODE_REF) cell_ref(x, y, P, ix, iy);
-                else cell_fast(x, y, P, ix, iy);
+                cell_fast(x, y, P, ix, iy);
+                const unsigned lx = (unsigned)(ix - x0), ly = (unsigned)(iy - y0);
+                const bool inside = lx < (unsigned)ww && ly < (unsigned)wh;
+                if (valid && !inside && P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
+                local = (valid && inside) ? (int)(ly * ww + lx) : -1;
+            } else if (valid) {
+                float x = px[k], y = py[k];
+                float u;
+                if (P.uniforms) {
+                    u = __ldg(&P.uniforms[((long long)h * P.steps + (t - 1)) * P.n + p]);
+                } else {
+                    const int c = p >> 10;
+                    if (c != key_chunk) {
+                        SSPool s = pool_step;
+                        ss_absorb(s, (unsigned)t);
+                        ss_absorb(s, (unsigned)c);
+                        ss_key(s, sk0, sk1);
+                        key_chunk = c;
+                    }
+                    u = philox64_f32(sk0, sk1, (uint64_t)(p & 1023));
+                }
+                const int a = ref_pick(S, x, y, ph[k], u);
+                x = __fadd_rn(x, S.adx[a]);
+                y = __fadd_rn(y, S.ady[a]);
+                px[k] = x; py[k] = y;
+                int ix, iy;
+                cell_ref(x, y, P, ix, iy);
                 const int lx = ix - x0, ly = iy - y0;
                 if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) {
                     if (P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
@@ -396,27 +443,31 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
                     local = ly * ww + lx;
                 }
             }
-            // warp-aggregated increment (all 32 lanes execute the match)
-            const unsigned peers = __match_any_sync(0xffffffffu, local);
-            if (local >= 0 && lane == __ffs(peers) - 1) {
-                const unsigned cnt = __popc(peers);
-                if (P.smem_window) {
-                    const unsigned old = atomicAdd(&win_s[local], cnt);
-                    if (old == 0u) list[atomicAdd(&S.list_n[t & 1], 1)] = local;
-                } else {
-                    atomicAdd(&gcount[local], cnt);
+            // whole warp on one cell (early steps): one aggregated add; else per lane
+            const int l0 = __shfl_sync(0xffffffffu, local, 0);
+            if (__all_sync(0xffffffffu, local == l0)) {
+                if (lane == 0 && l0 >= 0) {
+                    if (P.smem_window) win_add(win, l0, 32u);
+                    else atomicAdd(&gcount[l0], 32u);
                 }
+            } else if (local >= 0) {
+                if (P.smem_window) win_add(win, local, 1u);
+                else atomicAdd(&gcount[local], 1u);
             }
         }
         if (P.smem_window) {
             __syncthreads();
-            const int nl = S.list_n[t & 1];
-            if (tid == 0) S.list_n[(t + 1) & 1] = 0;
-            for (int i = tid; i < nl; i += NT) {
-                const int c = list[i];
-                const unsigned v = win_s[c];
-                win_s[c] = 0u;
-                atomicAdd(&gcount[c], v);
+            // flush: scan the window's packed words, one global reduction per nonzero cell
+            const int cells = ww * wh;
+            const int words = (cells + 1) >> 1;
+            for (int i = tid; i < words; i += NT) {
+                const unsigned w = win[i];
+                if (w) {
+                    win[i] = 0u;
+                    const unsigned lo = w & 0xFFFFu, hi = w >> 16;
+                    if (lo) atomicAdd(&gcount[2 * i], lo);
+                    if (hi) atomicAdd(&gcount[2 * i + 1], hi);
+                }
             }
             __syncthreads();
         }
@@ -425,7 +476,7 @@ __global__ void __launch_bounds__(NT) k_predict(const KParams P) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
-            if (p < P.n) {
+            if (p < P.n && k * NT + tid < P.ppc) {
                 P.xy_out[((long long)h * P.n + p) * 2] = px[k];
                 P.xy_out[((long long)h * P.n + p) * 2 + 1] = py[k];
             }
@@ -497,8 +548,11 @@ static KTable to_ktable(const gc_action_table &a) {
 template <int MODE, int K>
 static gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t st) {
     auto fn = k_predict<MODE, K>;
-    if (smem > 48 * 1024)
-        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static bool configured = false;  // per instantiation: raise the dynamic limit once
+    if (!configured) {
+        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        configured = true;
+    }
     fn<<<grid, NT, smem, st>>>(P);
     count_launch();
     return cuda_check(cudaGetLastError(), "k_predict launch");
@@ -509,8 +563,7 @@ static gc_status dispatch_k(const KParams &P, int K, int grid, size_t smem, cuda
     switch (K) {
         case 1: return launch_predict<MODE, 1>(P, grid, smem, st);
         case 2: return launch_predict<MODE, 2>(P, grid, smem, st);
-        case 4: return launch_predict<MODE, 4>(P, grid, smem, st);
-        default: return launch_predict<MODE, 8>(P, grid, smem, st);
+        default: return launch_predict<MODE, 4>(P, grid, smem, st);
     }
 }
 
@@ -554,31 +607,44 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
         // every table of the launch shares the heading set (checked by the host mirror);
         // copy it into the parameter bank so the heading loop reads constant operands
         std::vector<float> c(NBF), s(NBF), th(NBF);
-        GC_CUDA(cudaMemcpyAsync(c.data(), a->h_tables[0].d_cos_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-        GC_CUDA(cudaMemcpyAsync(s.data(), a->h_tables[0].d_sin_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-        GC_CUDA(cudaMemcpyAsync(th.data(), a->h_tables[0].d_theta_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-        GC_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+        const gc_action_table &t0 = a->h_tables[0];
+        if (t0.h_cos_h && t0.h_sin_h && t0.h_theta_h) {
+            memcpy(c.data(), t0.h_cos_h, NBF * 4);
+            memcpy(s.data(), t0.h_sin_h, NBF * 4);
+            memcpy(th.data(), t0.h_theta_h, NBF * 4);
+        } else {
+            GC_CUDA(cudaMemcpyAsync(c.data(), t0.d_cos_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+            GC_CUDA(cudaMemcpyAsync(s.data(), t0.d_sin_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+            GC_CUDA(cudaMemcpyAsync(th.data(), t0.d_theta_h, NBF * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+            GC_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+        }
         for (int b = 0; b < NBF; ++b) { P.hcos[b] = c[b]; P.hsin[b] = s[b]; P.hth2[b] = th[b] * th[b]; }
     }
     P.step_r = a->d_step_r; P.step_off = (const long long *)a->d_step_off;
     P.human_stride = a->human_stride; P.counts = a->d_counts;
     P.hyp_out = a->d_hyp_out; P.xy_out = a->d_xy_out; P.error = a->d_error;
 
-    // particles per thread: enough CTAs to fill 148 SMs at 2 CTAs/SM, then grow K
+    // particles per thread K and particles per CTA: enough CTAs to fill 148 SMs x 3
+    // resident CTAs, then grow K to amortise the per-step window flush
     const long long total = (long long)a->n_humans * a->n;
     int K = 1;
-    while (K < 8 && total / ((long long)NT * K * 2) >= 2 * 148 * 2) K *= 2;
-    const int ppc = NT * K;
-    P.ppc = ppc;
+    while (K < 4 && total / ((long long)NT * K * 2) >= 3 * 148) K *= 2;
+    int ppc = NT * K;
     P.ctas_per_human = (a->n + ppc - 1) / ppc;
+    ppc = (a->n + P.ctas_per_human - 1) / P.ctas_per_human;  // balance the last CTA
+    P.ppc = ppc;
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
-    const size_t win_bytes = (size_t)a->max_win_cells * 4 + (size_t)ppc * 4;
-    P.smem_window = win_bytes <= 200 * 1024 ? 1 : 0;
+    const size_t win_bytes = (size_t)((a->max_win_cells + 1) / 2) * 4;
+    P.smem_window = win_bytes <= 64 * 1024 ? 1 : 0;
     const size_t smem = P.smem_window ? win_bytes : 0;
     cudaStream_t st = (cudaStream_t)stream;
-    const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? MODE_FACT : MODE_GEN) : MODE_REF;
+    bool stdh = fact;
+    for (int b = 0; stdh && b < NBF; ++b) stdh = P.hcos[b] == hStdCos[b] && P.hsin[b] == hStdSin[b];
+    const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? (stdh ? MODE_FACTS : MODE_FACT) : MODE_GEN)
+                                                      : MODE_REF;
     if (mode == MODE_REF) return dispatch_k<MODE_REF>(P, K, (int)grid, smem, st);
+    if (mode == MODE_FACTS) return dispatch_k<MODE_FACTS>(P, K, (int)grid, smem, st);
     if (mode == MODE_FACT) return dispatch_k<MODE_FACT>(P, K, (int)grid, smem, st);
     return dispatch_k<MODE_GEN>(P, K, (int)grid, smem, st);
 }

@@ -1,0 +1,263 @@
+"""CycleEngine: the batched, device-resident update + predict cycle of many humans.
+
+This is the reference's closed-loop caller pattern (sim.py:455-514) -- per observation
+every human's belief is updated (belief.py:159-198), then every human is predicted with
+its own hypothesis space, the stationary-masked Q when it stands still (sim.py:480,
+:495), prefix (HUMAN_PREFIX, i) and cycle seed derive_seed(seed, 7, k), and the layers
+are merged by the max union (+ optional conservative time union, sim.py:500-504) --
+restructured for the B200:
+
+  * all state (posteriors, count windows, the fused (T, H, W) union) stays in HBM;
+  * one packed pinned H2D copy of the cycle's observations, then K1 (gc_belief_update,
+    warp per human) -> memsets -> K2 (gc_predict, all humans in one launch) -> K3
+    (gc_grid_epilogue: smoothing + atomicMax union [+ time union]);
+  * the whole cycle is captured once in a CUDA graph and replayed;
+  * optionally the union is read back to pinned host memory on a copy stream,
+    double-buffered so the D2H of cycle k overlaps the compute of cycle k+1.
+
+Multi-GPU: one engine per rank over that rank's humans; ``fused_reduce`` merges the
+per-rank unions with NCCL (max) only when a single fused grid is requested.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .belief import belief_tables, launch_belief_update, mask_stationary
+from .device import device
+from .prediction import MODES, action_tables, geometry
+from .rng import HUMAN_PREFIX, SIM_PREDICT, derive_seed
+from .tables import hypothesis_arrays
+
+
+@dataclass
+class EngineConfig:
+    n: int = 262_144
+    steps: int = 250
+    dt: float = 0.02
+    smoothing_sigma: float = 0.1
+    seed: int = 0
+    mode: str = "production"
+    obs_dt: float = 0.1
+    stationary_speed: float = 0.05     # sim.py:480 (observed speed below -> masked Q)
+    stationary_mask_v: float = 0.5     # mask_stationary threshold (sim.py:111)
+    union_dtype: str = "float32"       # fused union precision: float32 | float64
+    time_union: bool = False
+    per_human_layers: bool = False
+
+
+class CycleEngine:
+    def __init__(self, control_set, q_model, spaces: Sequence, grid_spec, cfg: EngineConfig,
+                 initial_log_weights: Optional[Sequence[np.ndarray]] = None):
+        self.dev = device()
+        self.cfg = cfg
+        self.spec = grid_spec
+        self.n_humans = len(spaces)
+        self.control_set = control_set
+        self.q_model = q_model
+        self.q_masked = mask_stationary(q_model, control_set, cfg.stationary_mask_v)
+        dev = self.dev
+        self.tables = [action_tables(control_set, q_model, cfg.dt, dev),
+                       action_tables(control_set, self.q_masked, cfg.dt, dev)]
+        self.btab = belief_tables(control_set, q_model, dev)
+        max_step = max(t.max_step for t in self.tables)
+        self.geo = geometry(grid_spec, cfg.steps, max_step, float(cfg.smoothing_sigma), dev)
+        H = self.n_humans
+        betas, goals, off = [], [], [0]
+        for sp in spaces:
+            b, g = hypothesis_arrays(sp)
+            if len(b) > 128:
+                raise NotImplementedError("at most 128 hypotheses per human")
+            betas.append(b)
+            goals.append(g)
+            off.append(off[-1] + len(b))
+        self.hyp_off = np.array(off, dtype=np.int32)
+        up = lambda a, t: torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=t)), device=dev)
+        self.d_hyp_off = up(self.hyp_off, np.int32)
+        self.d_beta64 = up(np.concatenate(betas), np.float64)
+        self.d_goal64 = up(np.concatenate(goals), np.float64)
+        self.d_beta32 = up(np.concatenate(betas).astype(np.float32), np.float32)
+        self.d_goal32 = up(np.concatenate(goals).astype(np.float32), np.float32)
+        if initial_log_weights is None:
+            lw = np.concatenate([np.full(len(b), -np.log(len(b))) for b in betas])
+        else:
+            lw = np.concatenate([np.asarray(x, dtype=float) for x in initial_log_weights])
+        self.d_logw = up(lw, np.float64)
+        self.d_status = torch.zeros(H, dtype=torch.int32, device=dev)
+        pre = np.zeros((H, 4), dtype=np.uint32)
+        pre[:, 0] = HUMAN_PREFIX
+        pre[:, 1] = np.arange(H)
+        self.d_prefix = up(pre, np.uint32)
+        self.d_plen = up(np.full(H, 2), np.int32)
+        # packed per-cycle inputs: f64 [obs (H,4) | fallback (H,)], u64 seeds (H,),
+        # f32 start (H,2), i32 table ids (H,)
+        self._nb = H * 5 * 8 + H * 8 + H * 2 * 4 + H * 4
+        self._nb = (self._nb + 15) // 16 * 16
+        # two pinned staging buffers so the host can pack cycle k+1 while cycle k runs
+        self.h_ins = [torch.empty(self._nb, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        self.h_in = self.h_ins[0]
+        self.d_in = torch.empty(self._nb, dtype=torch.uint8, device=dev)
+        o = 0
+        self.d_obs = self.d_in[o:o + H * 32].view(torch.float64); o += H * 32
+        self.d_fallback = self.d_in[o:o + H * 8].view(torch.float64); o += H * 8
+        self.d_seed = self.d_in[o:o + H * 8].view(torch.int64); o += H * 8
+        self.d_start = self.d_in[o:o + H * 8].view(torch.float32); o += H * 8
+        self.d_tid = self.d_in[o:o + H * 4].view(torch.int32); o += H * 4
+        self._views = [self._host_views(b.numpy(), H) for b in self.h_ins]
+        self._select(0)
+        self.counts = torch.zeros(H * self.geo.human_stride, dtype=torch.int32, device=dev)
+        udt = torch.float32 if cfg.union_dtype == "float32" else torch.float64
+        T, Hh, W = cfg.steps, grid_spec.height, grid_spec.width
+        self.unions = [torch.zeros((T, Hh, W), dtype=udt, device=dev) for _ in range(2)]
+        self.layers = (torch.zeros((H, T, Hh, W), dtype=torch.float64, device=dev)
+                       if cfg.per_human_layers else None)
+        self.d_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._tarr = (_lib.ActionTable * 2)(*[t.struct for t in self.tables])
+        self.last_xy = None
+        self.heading = np.zeros(H)
+        self.cycle = 0
+        self.graphs = {}
+        self.h_out = None
+
+    @staticmethod
+    def _host_views(hnp, H):
+        o = 0
+        obs = hnp[o:o + H * 32].view(np.float64).reshape(H, 4); o += H * 32
+        fb = hnp[o:o + H * 8].view(np.float64); o += H * 8
+        seed = hnp[o:o + H * 8].view(np.uint64); o += H * 8
+        start = hnp[o:o + H * 8].view(np.float32).reshape(H, 2); o += H * 8
+        tid = hnp[o:o + H * 4].view(np.int32); o += H * 4
+        return obs, fb, seed, start, tid
+
+    def _select(self, buf):
+        self.h_obs, self.h_fallback, self.h_seed, self.h_start, self.h_tid = self._views[buf]
+
+    def prime(self, xy):
+        """Record the observation preceding the first cycle (sim.py:462, :485)."""
+        self.last_xy = np.asarray(xy, dtype=float).copy()
+
+    # ---- host-side packing of one observation cycle ----------------------------------
+    def stage(self, obs_xy: np.ndarray, buf: int = 0):
+        """Pack the cycle's observations (H, 2) float64 into the pinned input buffer."""
+        obs_xy = np.asarray(obs_xy, dtype=float)
+        self._select(buf)
+        prev = self.last_xy if self.last_xy is not None else obs_xy
+        self.h_obs[:, 0:2] = prev
+        self.h_obs[:, 2:4] = obs_xy
+        self.h_fallback[:] = self.heading
+        d = obs_xy - prev
+        moved = np.hypot(d[:, 0], d[:, 1])
+        stationary = moved / self.cfg.obs_dt < self.cfg.stationary_speed
+        self.h_tid[:] = stationary.astype(np.int32)
+        mv = moved > 1e-9
+        self.heading = np.where(mv, np.arctan2(d[:, 1], d[:, 0]), self.heading)
+        self.h_start[:] = obs_xy.astype(np.float32)
+        self.h_seed[:] = np.uint64(derive_seed(self.cfg.seed, SIM_PREDICT, self.cycle))
+        self.last_xy = obs_xy.copy()
+        self.cycle += 1
+
+    # ---- the device cycle ---------------------------------------------------------------
+    def _launch(self, buf: int, with_update: bool, stream, events=None):
+        cfg, geo, H = self.cfg, self.geo, self.n_humans
+        sh = ctypes.c_void_p(stream.cuda_stream)
+        if with_update:
+            launch_belief_update(self.btab, self.d_hyp_off, self.d_beta64, self.d_goal64, self.d_obs,
+                                 self.d_fallback, self.d_logw, self.d_logw, self.d_status, cfg.obs_dt,
+                                 math.inf, 1, H, stream=stream)
+        self.counts.zero_()
+        u = self.unions[buf]
+        u.zero_()
+        a = _lib.PredictArgs()
+        a.n_humans, a.n, a.steps, a.rng_mode = H, cfg.n, cfg.steps, MODES[cfg.mode]
+        a.grid_w, a.grid_h = self.spec.width, self.spec.height
+        a.origin_x32 = float(np.float32(self.spec.origin[0]))
+        a.origin_y32 = float(np.float32(self.spec.origin[1]))
+        a.res32 = float(np.float32(self.spec.resolution))
+        a.d_start_xy, a.d_hyp_off = self.d_start.data_ptr(), self.d_hyp_off.data_ptr()
+        a.d_beta32, a.d_goal32 = self.d_beta32.data_ptr(), self.d_goal32.data_ptr()
+        a.d_cdf, a.d_log_w = None, self.d_logw.data_ptr()
+        a.d_seed, a.d_prefix, a.d_prefix_len = self.d_seed.data_ptr(), self.d_prefix.data_ptr(), self.d_plen.data_ptr()
+        a.h_tables, a.n_tables, a.d_table_id = self._tarr, 2, self.d_tid.data_ptr()
+        a.d_step_r, a.d_step_off = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr()
+        a.human_stride, a.max_win_cells = geo.human_stride, geo.max_win_cells
+        a.d_counts, a.d_error = self.counts.data_ptr(), self.d_err.data_ptr()
+        if events is not None:
+            events[0].record(stream)
+        _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")
+        if events is not None:
+            events[1].record(stream)
+        e = _lib.EpilogueArgs()
+        e.n_humans, e.n, e.steps = H, cfg.n, cfg.steps
+        e.grid_w, e.grid_h, e.radius = self.spec.width, self.spec.height, geo.radius
+        e.d_kernel, e.d_zx, e.d_zy = geo.d_kernel.data_ptr(), geo.d_zx.data_ptr(), geo.d_zy.data_ptr()
+        e.origin_x32, e.origin_y32, e.res32 = a.origin_x32, a.origin_y32, a.res32
+        e.n_tiles, e.d_start_xy = geo.n_tiles, self.d_start.data_ptr()
+        e.d_step_r, e.d_step_off, e.human_stride = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr(), geo.human_stride
+        e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), self.counts.data_ptr()
+        if self.layers is not None:
+            self.layers.zero_()
+            e.d_layers64 = self.layers.data_ptr()
+        if u.dtype == torch.float32:
+            e.d_union32 = u.data_ptr()
+        else:
+            e.d_union64 = u.data_ptr()
+        e.time_union = int(cfg.time_union)
+        _lib.check(_lib.lib().gc_grid_epilogue(ctypes.byref(e), sh), "gc_grid_epilogue")
+        if events is not None:
+            events[2].record(stream)
+
+    def run_cycle(self, buf: int = 0, with_h2d: bool = True, with_update: bool = True, stream=None,
+                  events=None):
+        """Eager (uncaptured) cycle on ``stream``; ``events`` = 3 CUDA events recorded
+        before K2, after K2 and after K3 (kernel timing on the launching stream)."""
+        s = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            if with_h2d:
+                self.d_in.copy_(self.h_ins[buf], non_blocking=True)
+            self._launch(buf, with_update, s, events)
+        return self.unions[buf]
+
+    def capture(self, buf: int = 0, with_h2d: bool = True, with_update: bool = True):
+        """Capture one cycle into a CUDA graph (replay with ``replay``)."""
+        key = (buf, with_h2d, with_update)
+        if key in self.graphs:
+            return self.graphs[key]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        # warm the library once outside capture (function attributes, lazy loading)
+        self.run_cycle(buf, with_h2d, with_update, stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            if with_h2d:
+                self.d_in.copy_(self.h_ins[buf], non_blocking=True)
+            self._launch(buf, with_update, s)
+        self.graphs[key] = g
+        return g
+
+    def posterior(self, i: int) -> np.ndarray:
+        a, b = self.hyp_off[i], self.hyp_off[i + 1]
+        return self.d_logw[a:b].cpu().numpy()
+
+    def check_errors(self):
+        if int(self.d_err.item()) != 0:
+            raise RuntimeError("gc_predict: a particle left its reachable-cell window")
+
+
+def fused_reduce(union: torch.Tensor, group=None, dst: Optional[int] = None):
+    """Merge per-rank unions into one fused grid with a max reduction over NCCL
+    (torch.distributed); all_reduce when dst is None."""
+    import torch.distributed as dist
+    if dst is None:
+        dist.all_reduce(union, op=dist.ReduceOp.MAX, group=group)
+    else:
+        dist.reduce(union, dst=dst, op=dist.ReduceOp.MAX, group=group)
+    return union

@@ -52,14 +52,14 @@ def recognise_q(q) -> Optional[LoweredQ]:
     for fn in (bp, base):
         qn = getattr(fn, "__qualname__", "")
         cv = _closure_vars(fn)
-        if qn.startswith("q_goal_progress.<locals>.shift_free"):
+        if qn.endswith("q_goal_progress.<locals>.shift_free"):
             return LoweredQ("goal_progress", float(cv["tau"]), float(cv["w_v"]), float(cv["w_th"]), full)
-        if qn.startswith("q_goal_progress.<locals>.base"):
+        if qn.endswith("q_goal_progress.<locals>.base"):
             inner = _closure_vars(cv.get("shift_free"))
             if "tau" in inner:
                 return LoweredQ("goal_progress", float(inner["tau"]), float(inner["w_v"]),
                                 float(inner["w_th"]), full)
-        if qn.startswith("q_default.<locals>.base"):
+        if qn.endswith("q_default.<locals>.base"):
             return LoweredQ("default", 0.5, float(cv["w_v"]), float(cv["w_th"]), True)
     return None
 
@@ -182,6 +182,12 @@ class ActionTables:
             t.dv, t.tau, t.w_v, t.w_th = dv, lq.tau, lq.w_v, lq.w_th
             t.d_cos_h, t.d_sin_h = self.d_cos.data_ptr(), self.d_sin.data_ptr()
             t.d_theta_h, t.d_a_index = self.d_theta.data_ptr(), self.d_aidx.data_ptr()
+            self.h_cos = np.ascontiguousarray(np.cos(heads).astype(np.float32))
+            self.h_sin = np.ascontiguousarray(np.sin(heads).astype(np.float32))
+            self.h_theta = np.ascontiguousarray(heads.astype(np.float32))
+            t.h_cos_h = self.h_cos.ctypes.data
+            t.h_sin_h = self.h_sin.ctypes.data
+            t.h_theta_h = self.h_theta.ctypes.data
             self.headings = heads
         self.struct = t
 

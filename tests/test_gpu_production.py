@@ -1,0 +1,136 @@
+"""GPU: production RNG mode is exact in distribution.
+
+* one-step action distributions (every action on its own cell) vs the exact float64
+  Boltzmann mixture -- factorised sampler (plain, stationary-masked, weighted) and the
+  generic per-action sampler;
+* multi-step layers vs the reference mode, TV bounded by the reference's own
+  seed-to-seed spread (self-calibrated);
+* the lattice instance vs exact enumeration (test_prediction.py:100-106 pattern);
+* hypothesis frequencies vs the belief.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_01122_b200 as G  # noqa: E402
+from paper_2603_01122_b200 import prediction as PR  # noqa: E402
+
+
+def exact_action_probs(z, belief, cs, q, space):
+    """float64 mixture over hypotheses of the Boltzmann policy at state z."""
+    p = np.zeros(len(cs))
+    w = belief.probs()
+    for h, (b, g) in enumerate(zip(space.beta_of, space.goal_xy_of)):
+        if w[h] > 0:
+            p += w[h] * G.boltzmann_policy(z, b, g, cs, q)
+    return p
+
+
+def one_step_tv(q_factory, n=1 << 22, weights=None, mask_v=None, goals=((0.5, 0.3), (0.1, 0.15))):
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = q_factory()
+    if mask_v is not None:
+        q = G.mask_stationary(q, cs, mask_v)
+    space = G.HypothesisSpace(G.RationalitySet((0.3, 2.0, 9.0)), G.GoalSet(np.array(goals)))
+    b = G.JointBelief.from_probs(weights if weights is not None else np.full(space.size, 1.0 / space.size))
+    spec = G.GridSpec(400, 400, 0.001)
+    z = G.HumanState(0.2005, 0.2005)
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, 0.1, dev)
+    job = PR.HumanJob(z, b.log_weights, space.beta_of, space.goal_xy_of, 12345, (), 0)
+    out = PR.run_predict([job], [tab], n, 1, 0.1, 0.0, spec, "production")
+    layer = out["layers"][0, 0].cpu().numpy()
+    # exact: action -> cell with the production kernel's float32 cell arithmetic
+    p = exact_action_probs(z, b, cs, q, space)
+    disp = cs.displacements(0.1).astype(np.float32)
+    x = np.float32(z.x) + disp[:, 0]
+    y = np.float32(z.y) + disp[:, 1]
+    inv = np.float32(1.0) / np.float32(0.001)
+    ix = np.clip(np.floor((x - np.float32(0)) * inv).astype(int), 0, 399)
+    iy = np.clip(np.floor((y - np.float32(0)) * inv).astype(int), 0, 399)
+    exact = np.zeros((400, 400))
+    np.add.at(exact, (iy, ix), p)
+    return 0.5 * np.abs(layer - exact).sum(), tab.factorised
+
+
+def test_factorised_one_step_exact_in_distribution():
+    tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5))
+    assert fact
+    assert tv < 0.006, tv
+
+
+def test_factorised_masked_and_weighted():
+    tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5), mask_v=0.5)
+    assert fact and tv < 0.006, tv
+    tv, fact = one_step_tv(lambda: G.q_goal_progress(0.4, (0.3, 0.2)), weights=[0.1, 0.2, 0.05, 0.3, 0.05, 0.3])
+    assert fact and tv < 0.006, tv
+
+
+def test_generic_sampler_one_step():
+    tv, fact = one_step_tv(lambda: G.q_default((0.3, 2.0)))
+    assert not fact
+    assert tv < 0.006, tv
+
+
+def test_far_goal_high_beta_no_overflow():
+    # |rel| ~ 57 m, beta = 9: logits reach hundreds; weights must stay finite
+    tv, _ = one_step_tv(lambda: G.q_goal_progress(0.5), goals=((40.2, 40.2), (-39.8, 0.2)))
+    assert tv < 0.006, tv
+
+
+def test_multistep_tv_within_reference_seed_spread():
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    goals = np.array([[17.0, 10.0], [10.0, 17.0], [3.0, 10.0], [10.0, 3.0]])
+    space = G.HypothesisSpace(G.RationalitySet.log_spaced(5), G.GoalSet(goals))
+    case = golden_io.PredictCase("cfg2_t30")
+    b = G.JointBelief(case.log_w)
+    spec = G.GridSpec(200, 200, 0.1)
+    z = G.HumanState(10.0, 10.0)
+    worst = {}
+    for sigma in (0.0, 0.1):
+        layers = {}
+        for tag, seed, mode in (("a", 1, "reference"), ("b", 2, "reference"), ("p", 3, "production")):
+            cfg = G.PredictionConfig(n=65536, steps=100, dt=0.02, smoothing_sigma=sigma, seed=seed, mode=mode)
+            layers[tag] = G.predict(z, b, cfg, cs, q, space, spec).layers
+        tv = lambda u, v: max(0.5 * np.abs(u[k] - v[k]).sum() for k in range(100))
+        spread = tv(layers["a"], layers["b"])
+        got = max(tv(layers["p"], layers["a"]), tv(layers["p"], layers["b"]))
+        worst[sigma] = (got, spread)
+        assert got <= 1.5 * spread + 0.005, (sigma, got, spread)
+
+
+def test_lattice_production_matches_enumeration():
+    z = golden_io.load("exact.npz")
+    case = golden_io.PredictCase("lattice")
+    m = case.meta
+    cs = G.ControlSet([G.ControlAction(float(v), float(t)) for v, t in zip(m["v"], m["theta"])])
+    space = G.HypothesisSpace(G.RationalitySet(tuple(m["betas"])), G.GoalSet(np.array(m["goals"])))
+    q = G.q_goal_progress(1.0)
+    spec = G.GridSpec(10, 10, 1.0)
+    b = G.JointBelief(z["log_w"])
+    cfg = G.PredictionConfig(n=65536, steps=3, dt=1.0, smoothing_sigma=0.0, seed=14, mode="production")
+    mc = G.predict(G.HumanState(4.5, 4.5), b, cfg, cs, q, space, spec)
+    for k in range(3):
+        assert G.total_variation(mc.layers[k], z["layers"][k]) < 0.05
+
+
+def test_production_hypothesis_frequencies():
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    space = G.HypothesisSpace(G.RationalitySet((1.0, 3.0)), G.GoalSet(np.array([[1.0, 1.0], [2.0, 2.0]])))
+    probs = np.array([0.1, 0.2, 0.3, 0.4])
+    b = G.JointBelief.from_probs(probs)
+    tab = PR.action_tables(cs, q, 0.1, torch.device("cuda"))
+    job = PR.HumanJob(G.HumanState(1.5, 1.5), b.log_weights, space.beta_of, space.goal_xy_of, 99, (), 0)
+    out = PR.run_predict([job], [tab], 200_000, 1, 0.1, 0.0, G.GridSpec(40, 40, 0.1), "production",
+                         want_hyp=True)
+    freq = np.bincount(out["hyp"][0].cpu().numpy(), minlength=4) / 200_000
+    np.testing.assert_allclose(freq, probs, atol=0.01)

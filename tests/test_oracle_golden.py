@@ -124,3 +124,14 @@ def test_multi_union_and_time_union():
     u = OP.union_max(stacks)
     np.testing.assert_array_equal(u, z["union"])
     np.testing.assert_array_equal(OP.time_union(u), z["time_union"])
+
+
+@pytest.mark.parametrize("name", ["cfg1_s0", "cfg1_s01", "ragged_w", "masked", "qdefault"])
+def test_cpu_baseline_port_matches_reference(name):
+    """The timed CPU baseline (oracle/port.py) is the reference computation."""
+    from oracle import port
+    c = golden_io.PredictCase(name)
+    W, H, res, org = c.grid
+    layers = port.predict(c.z0, c.log_w, c.n, c.steps, c.dt, c.sigma, c.seed, c.tables(),
+                          c.beta_of, c.goal_xy_of, OP.Grid(W, H, res, org), prefix=c.prefix, workers=4)
+    np.testing.assert_array_equal(layers[c.layer_steps], c.layers)

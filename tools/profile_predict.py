@@ -1,0 +1,39 @@
+"""Run one k_predict launch of a cfg3-shaped workload (for ncu captures).
+
+    python tools/profile_predict.py [--mode production|reference] [--steps T] [--humans H] [--n N]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2603_01122_b200.engine import CycleEngine, EngineConfig  # noqa: E402
+from paper_2603_01122_b200.scenario import make_scene  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", default="production")
+    ap.add_argument("--steps", type=int, default=250)
+    ap.add_argument("--humans", type=int, default=8)
+    ap.add_argument("--n", type=int, default=262144)
+    ap.add_argument("--cycles", type=int, default=2)
+    a = ap.parse_args()
+    sc = make_scene("cfg3", cycles=4, humans=a.humans)
+    eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec,
+                      EngineConfig(n=a.n, steps=a.steps, dt=sc.dt, mode=a.mode))
+    eng.prime(sc.warmup_track[0])
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for k in range(a.cycles):
+        eng.stage(sc.warmup_track[1 + k], buf=0)
+        eng.run_cycle(buf=0, events=ev)
+        torch.cuda.synchronize()
+        print(f"cycle {k}: k_predict {ev[0].elapsed_time(ev[1]):.3f} ms, epilogue {ev[1].elapsed_time(ev[2]):.3f} ms")
+    eng.check_errors()
+
+
+if __name__ == "__main__":
+    main()
