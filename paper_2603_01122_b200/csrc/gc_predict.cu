@@ -17,6 +17,7 @@
 //   MODE_FACT : production, exact in distribution for grid control sets with
 //               goal-progress utility: weight(a,b) = H_b G_a e_b^a, one ex2 per heading.
 //   MODE_GEN  : production generic per-action softmax (fast ex2) for any control set.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "gc_common.cuh"
@@ -76,11 +77,22 @@ __device__ __forceinline__ void cell_ref(float x, float y, const KParams &P, int
     iy = fy < 0.f ? 0 : (fy > (float)(P.grid_h - 1) ? P.grid_h - 1 : (int)fy);
 }
 
+// production cell index: floor((x - ox) / res) without the XU pipe (FRND/F2I would
+// compete with the exponentials): clamp to [-1, W], round with the 1.5*2^23 magic
+// constant, correct round-up to floor, clamp to the grid.  Differs from the IEEE
+// division form only for positions within an ulp of a cell edge.
+__device__ __forceinline__ int floor_clamp(float f, int n) {
+    f = fminf(fmaxf(f, -1.f), (float)n);
+    const float r = f + 12582912.f;
+    const float fr = r - 12582912.f;
+    int i = __float_as_int(r) - 0x4B400000;
+    i -= (fr > f) ? 1 : 0;
+    return min(max(i, 0), n - 1);
+}
+
 __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, int &ix, int &iy) {
-    const float fx = floorf((x - P.ox) * P.inv_res);
-    const float fy = floorf((y - P.oy) * P.inv_res);
-    ix = fx < 0.f ? 0 : (fx > (float)(P.grid_w - 1) ? P.grid_w - 1 : (int)fx);
-    iy = fy < 0.f ? 0 : (fy > (float)(P.grid_h - 1) ? P.grid_h - 1 : (int)fy);
+    ix = floor_clamp((x - P.ox) * P.inv_res, P.grid_w);
+    iy = floor_clamp((y - P.oy) * P.inv_res, P.grid_h);
 }
 
 struct SmemTabs {
@@ -258,7 +270,7 @@ __device__ __forceinline__ void win_add(unsigned *win, int local, unsigned cnt) 
 }
 
 template <int MODE, int K>
-__global__ void __launch_bounds__(NT, 3) k_predict(const KParams P) {
+__global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ SmemTabs S;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -316,10 +328,13 @@ __global__ void __launch_bounds__(NT, 3) k_predict(const KParams P) {
         }
     }
     unsigned *win = reinterpret_cast<unsigned *>(smem_dyn);
+    int *list = nullptr;  // packed-word indices touched this step (<= one per particle)
     if (P.smem_window) {
         const int R = __ldg(&P.step_r[P.steps - 1]);
         const int words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
         for (int i = tid; i < words; i += NT) win[i] = 0u;
+        list = reinterpret_cast<int *>(win + ((words + 3) & ~3));
+        if (tid == 0) { S.list_n[0] = 0; S.list_n[1] = 0; }
     }
     __syncthreads();
 
@@ -443,31 +458,47 @@ __global__ void __launch_bounds__(NT, 3) k_predict(const KParams P) {
                     local = ly * ww + lx;
                 }
             }
-            // whole warp on one cell (early steps): one aggregated add; else per lane
+            // whole warp on one cell (early steps): one aggregated add; else per lane.
+            // A word seen zero by its first add is appended to the touched list
+            // (warp-aggregated: one shared atomic per warp).
             const int l0 = __shfl_sync(0xffffffffu, local, 0);
-            if (__all_sync(0xffffffffu, local == l0)) {
-                if (lane == 0 && l0 >= 0) {
-                    if (P.smem_window) win_add(win, l0, 32u);
-                    else atomicAdd(&gcount[l0], 32u);
+            const bool uni = __all_sync(0xffffffffu, local == l0);
+            if (P.smem_window) {
+                bool first = false;
+                if (uni) {
+                    if (lane == 0 && l0 >= 0)
+                        first = atomicAdd(&win[l0 >> 1], 32u << ((l0 & 1) << 4)) == 0u;
+                } else if (local >= 0) {
+                    first = atomicAdd(&win[local >> 1], 1u << ((local & 1) << 4)) == 0u;
                 }
-            } else if (local >= 0) {
-                if (P.smem_window) win_add(win, local, 1u);
-                else atomicAdd(&gcount[local], 1u);
+                const unsigned m = __ballot_sync(0xffffffffu, first);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    int base = 0;
+                    if (lane == leader) base = atomicAdd(&S.list_n[t & 1], __popc(m));
+                    base = __shfl_sync(0xffffffffu, base, leader);
+                    if (first) list[base + __popc(m & ((1u << lane) - 1u))] = (uni ? l0 : local) >> 1;
+                }
+            } else {
+                if (uni) {
+                    if (lane == 0 && l0 >= 0) atomicAdd(&gcount[l0], 32u);
+                } else if (local >= 0) {
+                    atomicAdd(&gcount[local], 1u);
+                }
             }
         }
         if (P.smem_window) {
             __syncthreads();
-            // flush: scan the window's packed words, one global reduction per nonzero cell
-            const int cells = ww * wh;
-            const int words = (cells + 1) >> 1;
-            for (int i = tid; i < words; i += NT) {
-                const unsigned w = win[i];
-                if (w) {
-                    win[i] = 0u;
-                    const unsigned lo = w & 0xFFFFu, hi = w >> 16;
-                    if (lo) atomicAdd(&gcount[2 * i], lo);
-                    if (hi) atomicAdd(&gcount[2 * i + 1], hi);
-                }
+            // flush only the touched words: one global reduction per nonzero cell
+            const int nl = S.list_n[t & 1];
+            if (tid == 0) S.list_n[(t + 1) & 1] = 0;
+            for (int i = tid; i < nl; i += NT) {
+                const int wi = list[i];
+                const unsigned w = win[wi];
+                win[wi] = 0u;
+                const unsigned lo = w & 0xFFFFu, hi = w >> 16;
+                if (lo) atomicAdd(&gcount[2 * wi], lo);
+                if (hi) atomicAdd(&gcount[2 * wi + 1], hi);
             }
             __syncthreads();
         }
@@ -627,15 +658,20 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     // particles per thread K and particles per CTA: enough CTAs to fill 148 SMs x 3
     // resident CTAs, then grow K to amortise the per-step window flush
     const long long total = (long long)a->n_humans * a->n;
+    static const int kmax = [] {
+        const char *e = getenv("GC_PREDICT_MAXK");  // tuning knob (1, 2 or 4)
+        const int v = e ? atoi(e) : 4;
+        return v >= 4 ? 4 : (v >= 2 ? 2 : 1);
+    }();
     int K = 1;
-    while (K < 4 && total / ((long long)NT * K * 2) >= 3 * 148) K *= 2;
+    while (K < kmax && total / ((long long)NT * K * 2) >= 4 * 148) K *= 2;
     int ppc = NT * K;
     P.ctas_per_human = (a->n + ppc - 1) / ppc;
     ppc = (a->n + P.ctas_per_human - 1) / P.ctas_per_human;  // balance the last CTA
     P.ppc = ppc;
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
-    const size_t win_bytes = (size_t)((a->max_win_cells + 1) / 2) * 4;
+    const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4 + (size_t)ppc * 4;
     P.smem_window = win_bytes <= 64 * 1024 ? 1 : 0;
     const size_t smem = P.smem_window ? win_bytes : 0;
     cudaStream_t st = (cudaStream_t)stream;
