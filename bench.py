@@ -155,7 +155,7 @@ def run_reference(args):
     scene = make_scene(args.config, cycles=2)
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(scene, t_steps=args.cpu_t, reps=1)
+        r = cpu_sample(scene, t_steps=args.ref_t, reps=1)
         if i >= args.warmup:
             vals.append(r)
     v = float(np.median([r["value"] for r in vals]))
@@ -196,7 +196,8 @@ def run_ours(args):
     scene = make_scene(args.config, cycles=W + K + 4, humans=8, human_offset=8 * rank)
     cfg = EngineConfig(n=scene.n, steps=scene.steps, dt=scene.dt, smoothing_sigma=0.1, seed=0,
                        mode=args.mode, time_union=False)
-    eng = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec, cfg)
+    eng = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec, cfg,
+                      human_ids=list(range(8 * rank, 8 * rank + len(scene.spaces))))
     # posterior after 10 observations (also warms every kernel)
     eng.prime(scene.warmup_track[0])
     for k in range(1, 11):
@@ -239,7 +240,8 @@ def run_ours(args):
     launches0 = _lib.lib().gc_launch_count()
     barrier()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    clocks = ClockSampler(local).__enter__()
+    if True:
         with torch.cuda.stream(stream):
             t_start.record(stream)
             for i in range(K):
@@ -307,6 +309,7 @@ def run_ours(args):
     stream.wait_stream(copy)
     e_end.record(stream)
     barrier()
+    clocks.__exit__(None, None, None)
     e2e_ms = max_over_ranks(e_start.elapsed_time(e_end) / K)
     lat = [a.elapsed_time(b) for a, b in evs]
     e2e_p99 = max_over_ranks(float(np.percentile(lat, 99)))
@@ -320,6 +323,7 @@ def run_ours(args):
     sm_mhz = pk["sm_max_mhz"]
     fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s at the max SM clock
     k2_achieved = psteps_rank * REF_OPS_PER_PSTEP / (k2_ms * 1e-3) / 1e12
+    issue = None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     ncu = None
@@ -327,6 +331,13 @@ def run_ours(args):
         try:
             ncu = json.load(open(prof)).get(args.mode, {}).get("k_predict")
             traffic = ncu.get("dram_bytes_per_launch") if ncu else None
+            ipp = ncu.get("lane_instr_per_particle_step") if ncu else None
+            if ipp:
+                # executed-instruction issue rate: 148 SM x 4 schedulers x 32 lanes per clock
+                ach = psteps_rank * ipp / (k2_ms * 1e-3) / 1e12
+                issue = {"achieved": ach, "peak": fp32_peak, "unit": "T lane-instr/s",
+                         "frac": ach / fp32_peak, "lane_instr_per_particle_step": ipp,
+                         "source": "profiles/ncu_summary.json (ncu --set full of k_predict)"}
         except (ValueError, AttributeError):
             ncu = None
     line = {
@@ -357,6 +368,7 @@ def run_ours(args):
                      f"(9m+10, m=96, SURVEY 8d) x {psteps_rank} particle-steps per launch; the factorised "
                      f"production sampler executes fewer ops, so frac > 1 is possible"),
             "peak_source": f"148 SM x 128 FP32 lanes x {sm_mhz:.0f} MHz ({pk['source']} sm_max_mhz)",
+            "issue": issue,
             "ncu": ncu,
         },
         "clocks": clk,
@@ -373,14 +385,15 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--mode", default="production", choices=["production", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
-    ap.add_argument("--cpu-t", type=int, default=10)
+    ap.add_argument("--cpu-t", type=int, default=25)
+    ap.add_argument("--ref-t", type=int, default=10)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -96,6 +96,9 @@ typedef struct {
     const uint64_t *d_seed;    /* (n_humans,) */
     const uint32_t *d_prefix;  /* (n_humans, 4) */
     const int32_t *d_prefix_len; /* (n_humans,) 0..4 */
+    /* production RNG: per-human stream id (the human's GLOBAL index, so a scene sharded
+     * over GPUs draws the same numbers for any partition); NULL = batch index */
+    const uint32_t *d_stream_id;
     /* GC_RNG_UNIFORMS inputs */
     const float *d_uniforms;   /* (n_humans, steps, n) float32 or NULL */
     const double *d_hyp_u;     /* (n_humans, n) float64 or NULL */

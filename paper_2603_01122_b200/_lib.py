@@ -58,7 +58,7 @@ class PredictArgs(ctypes.Structure):
         ("origin_x32", F32), ("origin_y32", F32), ("res32", F32),
         ("d_start_xy", P), ("d_hyp_off", P), ("d_beta32", P), ("d_goal32", P),
         ("d_cdf", P), ("d_log_w", P),
-        ("d_seed", P), ("d_prefix", P), ("d_prefix_len", P),
+        ("d_seed", P), ("d_prefix", P), ("d_prefix_len", P), ("d_stream_id", P),
         ("d_uniforms", P), ("d_hyp_u", P), ("d_hyp_in", P),
         ("h_tables", ctypes.POINTER(ActionTable)), ("n_tables", I32), ("d_table_id", P),
         ("d_step_r", P), ("d_step_off", P), ("human_stride", I64),

@@ -51,6 +51,7 @@ struct KParams {
     const unsigned long long *seed;
     const unsigned *prefix;
     const int *prefix_len;
+    const unsigned *stream_id;
     const float *uniforms;
     const double *hyp_u;
     const int *hyp_in;
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     cell_ref(sx0, sy0, P, cx, cy);
     const unsigned long long seed = __ldg(&P.seed[h]);
     const unsigned sk_lo = (unsigned)seed, sk_hi = (unsigned)(seed >> 32);
+    const unsigned sid = P.stream_id ? __ldg(&P.stream_id[h]) : (unsigned)h;
     SSPool pool_pre;
     if (MODE == MODE_REF) {
         pool_pre = ss_pool_init(seed);
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 if (P.hyp_u) u = __ldg(&P.hyp_u[(long long)h * P.n + p]);
                 else if (MODE == MODE_REF) u = philox64_f64(hk0, hk1, (uint64_t)p);
                 else {
-                    const U4 o = philox4x32(U4{(unsigned)p, 0xFFFFFFFFu, (unsigned)h, 0x5EEDu}, sk_lo, sk_hi);
+                    const U4 o = philox4x32(U4{(unsigned)p, 0xFFFFFFFFu, sid, 0x5EEDu}, sk_lo, sk_hi);
                     u = ((double)(o.x >> 5) * 67108864.0 + (double)(o.y >> 6)) * (1.0 / 9007199254740992.0);
                 }
                 hi = 0;
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 float x = px[k], y = py[k];
                 unsigned ua, ub;
                 if ((t & 1) == 1) {
-                    const U4 o = philox4x32(U4{(unsigned)p, (unsigned)(t >> 1), (unsigned)h, 0xA11CEu}, sk_lo, sk_hi);
+                    const U4 o = philox4x32(U4{(unsigned)p, (unsigned)(t >> 1), sid, 0xA11CEu}, sk_lo, sk_hi);
                     ua = o.x; ub = o.y; rz[k] = o.z; rw[k] = o.w;
                 } else {
                     ua = rz[k]; ub = rw[k];
@@ -619,6 +621,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.start_xy = a->d_start_xy; P.hyp_off = a->d_hyp_off; P.beta32 = a->d_beta32; P.goal32 = a->d_goal32;
     P.cdf = a->d_cdf; P.log_w = a->d_log_w;
     P.seed = (const unsigned long long *)a->d_seed; P.prefix = a->d_prefix; P.prefix_len = a->d_prefix_len;
+    P.stream_id = a->d_stream_id;
     P.uniforms = a->rng_mode == GC_RNG_UNIFORMS ? a->d_uniforms : nullptr;
     P.hyp_u = a->rng_mode == GC_RNG_UNIFORMS ? a->d_hyp_u : nullptr;
     P.hyp_in = a->d_hyp_in;

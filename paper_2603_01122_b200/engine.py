@@ -55,7 +55,8 @@ class EngineConfig:
 
 class CycleEngine:
     def __init__(self, control_set, q_model, spaces: Sequence, grid_spec, cfg: EngineConfig,
-                 initial_log_weights: Optional[Sequence[np.ndarray]] = None):
+                 initial_log_weights: Optional[Sequence[np.ndarray]] = None,
+                 human_ids: Optional[Sequence[int]] = None):
         self.dev = device()
         self.cfg = cfg
         self.spec = grid_spec
@@ -91,10 +92,14 @@ class CycleEngine:
             lw = np.concatenate([np.asarray(x, dtype=float) for x in initial_log_weights])
         self.d_logw = up(lw, np.float64)
         self.d_status = torch.zeros(H, dtype=torch.int32, device=dev)
+        # global human ids: prefix (HUMAN_PREFIX, i) and production stream id are the
+        # same for a human whatever GPU / batch slot it lands on
+        self.human_ids = np.arange(H) if human_ids is None else np.asarray(human_ids, dtype=np.int64)
         pre = np.zeros((H, 4), dtype=np.uint32)
         pre[:, 0] = HUMAN_PREFIX
-        pre[:, 1] = np.arange(H)
+        pre[:, 1] = self.human_ids.astype(np.uint32)
         self.d_prefix = up(pre, np.uint32)
+        self.d_sid = up(self.human_ids.astype(np.uint32), np.uint32)
         self.d_plen = up(np.full(H, 2), np.int32)
         # packed per-cycle inputs: f64 [obs (H,4) | fallback (H,)], u64 seeds (H,),
         # f32 start (H,2), i32 table ids (H,)
@@ -184,6 +189,7 @@ class CycleEngine:
         a.d_beta32, a.d_goal32 = self.d_beta32.data_ptr(), self.d_goal32.data_ptr()
         a.d_cdf, a.d_log_w = None, self.d_logw.data_ptr()
         a.d_seed, a.d_prefix, a.d_prefix_len = self.d_seed.data_ptr(), self.d_prefix.data_ptr(), self.d_plen.data_ptr()
+        a.d_stream_id = self.d_sid.data_ptr()
         a.h_tables, a.n_tables, a.d_table_id = self._tarr, 2, self.d_tid.data_ptr()
         a.d_step_r, a.d_step_off = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr()
         a.human_stride, a.max_win_cells = geo.human_stride, geo.max_win_cells

@@ -1,0 +1,90 @@
+"""CPU, world_size 2 over gloo: the multi-GPU decomposition of a scene.
+
+Humans are sharded across ranks with their GLOBAL index in the random-stream prefix
+(HUMAN_PREFIX, i) (sim.py:493-499), each rank merges its own humans by max, and the
+per-rank unions are merged into one fused grid by a max reduction
+(engine.fused_reduce -- NCCL on the GPU box, gloo here).  The fused grid must equal the
+single-process union over all humans for any partition (checked with the oracle, which
+stands in for the per-rank CUDA predict on this GPU-less host).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import model
+from oracle import predict as OP
+
+N, T, DT, SIG, SEED = 600, 6, 0.1, 0.1, 12345
+GRID = OP.Grid(60, 60, 0.1)
+
+
+def humans():
+    r = np.random.default_rng(3)
+    out = []
+    for i in range(5):
+        s = r.uniform(1.5, 4.5, 2)
+        goals = s + 2.0 * np.stack([np.cos(np.arange(4) * 1.57), np.sin(np.arange(4) * 1.57)], 1)
+        beta_of, goal_of = model.hypothesis_tables(np.geomspace(0.1, 10, 5), goals)
+        lw = np.log(r.dirichlet(np.ones(20)))
+        out.append((s, lw - np.log(np.exp(lw).sum()), beta_of, goal_of))
+    return out
+
+
+def layers_of(i, hm, tb):
+    s, lw, b, g = hm
+    return OP.predict(s, lw, N, T, DT, SIG, SEED, tb, b, g, GRID, prefix=(2, i))["layers"]
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _worker(rank, world, port, shards, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_01122_b200.engine import fused_reduce
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, DT, model.QSpec())
+    hs = humans()
+    local = np.zeros((T, GRID.height, GRID.width))
+    for i in shards[rank]:
+        np.maximum(local, layers_of(i, hs[i], tb), out=local)
+    u = torch.from_numpy(local)
+    fused_reduce(u, dst=0)
+    # timing rule of bench.py: the step time is the max over ranks
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        np.save(result_path, u.numpy())
+        assert float(t.item()) == world
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shards", [([0, 1, 2], [3, 4]), ([4, 0], [2, 1, 3])])
+def test_fused_grid_equals_single_process_union(tmp_path, shards):
+    path = str(tmp_path / "fused.npy")
+    mp.spawn(_worker, args=(2, _free_port(), shards, path), nprocs=2, join=True)
+    fused = np.load(path)
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, DT, model.QSpec())
+    hs = humans()
+    ref = OP.union_max([layers_of(i, h, tb) for i, h in enumerate(hs)])
+    np.testing.assert_array_equal(fused, ref)
+
+
+def test_scene_shards_are_disjoint_and_sized():
+    from paper_2603_01122_b200.scenario import make_scene
+    a = make_scene("cfg3", cycles=1, humans=8, human_offset=0)
+    b = make_scene("cfg3", cycles=1, humans=8, human_offset=8)
+    assert len(a.spaces) == len(b.spaces) == 8
+    assert not np.allclose(a.starts, b.starts)
+    assert a.n == 262144 and a.steps == 250

@@ -1,0 +1,13 @@
+#!/bin/bash
+# ncu evidence for profiles/: launch list of one bench run + full captures of K2/K3/K1.
+set -x
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_bench.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+python tools/profile_predict.py --steps 250 --cycles 3 > gpurun_out/plain_prof.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_predict|k_epilogue|k_belief" -s 3 -c 3 \
+    -o gpurun_out/cycle_cfg3 python tools/profile_predict.py --steps 250 --cycles 3 > gpurun_out/ncu_full.log 2>&1
+python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/plain_ref.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
+    -o gpurun_out/k2_refmode python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/ncu_ref.log 2>&1
+tail -2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_ref.log
