@@ -63,6 +63,8 @@ struct KParams {
     long long human_stride;
     unsigned *counts;
     int smem_window;
+    int act_off;  // byte offset of SmemAct in dynamic shared memory (REF/GEN modes)
+    int debug;  // ablation bits (tuning only, env GC_PREDICT_DEBUG): 1 no global flush, 2 no histogram, 4 hash RNG
     int *hyp_out;
     float *xy_out;
     unsigned *error;
@@ -96,9 +98,13 @@ __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, in
     iy = floor_clamp((y - P.oy) * P.inv_res, P.grid_h);
 }
 
-struct SmemTabs {
-    // MODE_REF / MODE_GEN: per-action rows compacted over keep
+// MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
+// after the window and the touched list; absent from the production kernel)
+struct SmemAct {
     float ax[MAXM], ay[MAXM], aat[MAXM], adx[MAXM], ady[MAXM];
+};
+
+struct SmemTabs {
     // hypotheses of this CTA's human
     double cdf[MAXH];
     float hb[MAXH], hgx[MAXH], hgy[MAXH];
@@ -111,7 +117,7 @@ struct SmemTabs {
 };
 
 // ---- reference float32 step (prediction.py:147-162), 3 passes, no stored row --------
-__device__ __forceinline__ float ref_logit(const SmemTabs &S, int k, float rx, float ry, float d2,
+__device__ __forceinline__ float ref_logit(const SmemAct &S, int k, float rx, float ry, float d2,
                                            float beta, int qk) {
     float L;
     if (qk == GC_Q_DEFAULT) {
@@ -124,11 +130,11 @@ __device__ __forceinline__ float ref_logit(const SmemTabs &S, int k, float rx, f
     return __fmul_rn(L, beta);
 }
 
-__device__ __forceinline__ int ref_pick(const SmemTabs &S, float x, float y, int h, float u) {
-    const float rx = __fsub_rn(x, S.hgx[h]), ry = __fsub_rn(y, S.hgy[h]);
+__device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
+    const float rx = __fsub_rn(x, H.hgx[h]), ry = __fsub_rn(y, H.hgy[h]);
     const float d2 = __fadd_rn(__fmul_rn(rx, rx), __fmul_rn(ry, ry));
-    const float beta = S.hb[h];
-    const int mk = S.m_keep, qk = S.q_kind;
+    const float beta = H.hb[h];
+    const int mk = H.m_keep, qk = H.q_kind;
     float M = -__int_as_float(0x7f800000);
     for (int k = 0; k < mk; ++k) M = fmaxf(M, ref_logit(S, k, rx, ry, d2, beta, qk));
     float c = 0.f;
@@ -148,11 +154,11 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &S, float x, float y, int
 }
 
 // ---- production generic per-action softmax ------------------------------------------
-__device__ __forceinline__ int gen_pick(const SmemTabs &S, float x, float y, int h, float u) {
-    const float rx = x - S.hgx[h], ry = y - S.hgy[h];
+__device__ __forceinline__ int gen_pick(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
+    const float rx = x - H.hgx[h], ry = y - H.hgy[h];
     const float d2 = fmaf(rx, rx, ry * ry);
-    const float bl = S.hb[h] * 1.4426950408889634f;
-    const int mk = S.m_keep, qk = S.q_kind;
+    const float bl = H.hb[h] * 1.4426950408889634f;
+    const int mk = H.m_keep, qk = H.q_kind;
     auto L = [&](int k) {
         float q;
         if (qk == GC_Q_DEFAULT) q = -d2 - S.aat[k];
@@ -200,7 +206,7 @@ static const float hStdSin[NBF] = GC_STD_SIN;
 
 template <bool STDH, bool WTH>
 __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, float &x, float &y,
-                                          int h, float u1, float u2) {
+                                          int h, float u1) {
     const float rx = x - S.hgx[h], ry = y - S.hgy[h];
     const float r2 = fmaf(rx, rx, ry * ry);
     const float r = r2 * rsqrtf(fmaxf(r2, 1e-30f));
@@ -234,28 +240,42 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     const float rr = u1 * (Z0 + C);
     const float t = rr - Z0;
     // heading = #{b : cum_b <= t}: cum is monotone, so halve the candidate set with one
-    // compare + selects per level (24 -> 12 -> 6 -> 3), then count the last three
+    // compare + selects per level (24 -> 12 -> 6 -> 3), then count the last three; lo
+    // tracks the largest cum_b <= t (the start of the chosen heading's interval)
     int b = 0;
+    float lo = 0.f;
     {
         bool p = cum[11] <= t;
         b += p ? 12 : 0;
+        lo = p ? cum[11] : lo;
 #pragma unroll
         for (int i = 0; i < 12; ++i) cum[i] = p ? cum[i + 12] : cum[i];
         p = cum[5] <= t;
         b += p ? 6 : 0;
+        lo = p ? cum[5] : lo;
 #pragma unroll
         for (int i = 0; i < 6; ++i) cum[i] = p ? cum[i + 6] : cum[i];
         p = cum[2] <= t;
         b += p ? 3 : 0;
+        lo = p ? cum[2] : lo;
 #pragma unroll
         for (int i = 0; i < 3; ++i) cum[i] = p ? cum[i + 3] : cum[i];
-        b += (cum[0] <= t ? 1 : 0) + (cum[1] <= t ? 1 : 0) + (cum[2] <= t ? 1 : 0);
+        const bool p0 = cum[0] <= t, p1 = cum[1] <= t, p2 = cum[2] <= t;
+        b += (p0 ? 1 : 0) + (p1 ? 1 : 0) + (p2 ? 1 : 0);
+        lo = p2 ? cum[2] : (p1 ? cum[1] : (p0 ? cum[0] : lo));
     }
     b = b < NBF - 1 ? b : NBF - 1;
+    // speed within the heading from the residual of the same uniform: given b,
+    // (t - lo) is uniform on [0, H_b sum_a G_a e_b^a) (up to the 2^-24 resolution of u1)
     const float e = ex2_approx(fmaf(A, P.hcos[b], fmaf(B, P.hsin[b], nkr)));
-    const float w1 = G1 * e, w2 = G2 * e * e, w3 = G3 * e * e * e;
-    const float r2u = u2 * (w1 + w2 + w3);
-    int a = 1 + ((w1 <= r2u) ? 1 : 0) + ((w1 + w2 <= r2u) ? 1 : 0);
+    float w1 = G1 * e, w2 = G2 * e * e;
+    if (WTH) {
+        const float hb = ex2_approx(-S.wth * S.hb[h] * P.hth2[b]);
+        w1 *= hb;
+        w2 *= hb;
+    }
+    const float res = t - lo;
+    int a = 1 + ((w1 <= res) ? 1 : 0) + ((w1 + w2 <= res) ? 1 : 0);
     a = a < na - 1 ? a : na - 1;
     // stay (rr < Z0): every zero-speed action has displacement 0 -- branch-free select
     const bool stay = rr < Z0;
@@ -270,7 +290,7 @@ __device__ __forceinline__ void win_add(unsigned *win, int local, unsigned cnt) 
     atomicAdd(&win[local >> 1], cnt << ((local & 1) << 4));
 }
 
-template <int MODE, int K>
+template <int MODE, int K, bool WTH>
 __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ SmemTabs S;
@@ -287,14 +307,15 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         S.n_hyp = nh; S.m_keep = T.m_keep; S.q_kind = T.q_kind; S.n_speeds = T.n_speeds;
         S.wth = T.w_th * 1.4426950408889634f;
     }
+    SmemAct &A = *reinterpret_cast<SmemAct *>(smem_dyn + P.act_off);
     if (MODE != MODE_FACT && MODE != MODE_FACTS) {
         for (int k = tid; k < T.m_keep; k += NT) {
             const int j = __ldg(&T.keep[k]);
-            S.ax[k] = __ldg(&T.sx[j]);
-            S.ay[k] = __ldg(&T.sy[j]);
-            S.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? __ldg(&T.pen[j]) : __ldg(&T.at[j]);
-            S.adx[k] = __ldg(&T.dispx[j]);
-            S.ady[k] = __ldg(&T.dispy[j]);
+            A.ax[k] = __ldg(&T.sx[j]);
+            A.ay[k] = __ldg(&T.sy[j]);
+            A.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? __ldg(&T.pen[j]) : __ldg(&T.at[j]);
+            A.adx[k] = __ldg(&T.dispx[j]);
+            A.ady[k] = __ldg(&T.dispy[j]);
         }
     } else {
         for (int i = tid; i < NAF * NBF; i += NT) {
@@ -355,7 +376,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
 
     float px[K], py[K];
     int ph[K];
-    unsigned rz[K], rw[K];  // the unused half of the last Philox4x32 block (odd steps)
+    unsigned r1[K], r2[K], r3[K];  // unused words of the particle's current Philox4x32 block
     const int pbase = blk * P.ppc;
     {
         uint64_t hk0 = 0, hk1 = 0;
@@ -367,7 +388,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
-            px[k] = sx0; py[k] = sy0; ph[k] = 0; rz[k] = 0u; rw[k] = 0u;
+            px[k] = sx0; py[k] = sy0; ph[k] = 0; r1[k] = r2[k] = r3[k] = 0u;
             if (p >= P.n || k * NT + tid >= P.ppc) continue;
             int hi;
             if (P.hyp_in) {
@@ -408,21 +429,23 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             if (MODE != MODE_REF) {
                 // production: padded lanes compute too (no divergence), they just do not count
                 float x = px[k], y = py[k];
-                unsigned ua, ub;
-                if ((t & 1) == 1) {
-                    const U4 o = philox4x32(U4{(unsigned)p, (unsigned)(t >> 1), sid, 0xA11CEu}, sk_lo, sk_hi);
-                    ua = o.x; ub = o.y; rz[k] = o.z; rw[k] = o.w;
+                // one Philox4x32-10 block per particle per four steps (one 24-bit uniform
+                // per step); the block counter is (particle, step/4, human stream, tag)
+                unsigned ua;
+                if (P.debug & 4) {
+                    ua = (unsigned)p * 0x9E3779B9u ^ (unsigned)t * 0x85EBCA6Bu;
+                } else if (((t - 1) & 3) == 0) {
+                    const U4 o = philox4x32(U4{(unsigned)p, (unsigned)((t - 1) >> 2), sid, 0xA11CEu}, sk_lo, sk_hi);
+                    ua = o.x; r1[k] = o.y; r2[k] = o.z; r3[k] = o.w;
                 } else {
-                    ua = rz[k]; ub = rw[k];
+                    ua = r1[k]; r1[k] = r2[k]; r2[k] = r3[k];
                 }
                 if (MODE == MODE_FACT || MODE == MODE_FACTS) {
-                    constexpr bool STDH = MODE == MODE_FACTS;
-                    if (S.wth != 0.f) fact_step<STDH, true>(S, P, x, y, ph[k], u24(ua), u24(ub));
-                    else fact_step<STDH, false>(S, P, x, y, ph[k], u24(ua), u24(ub));
+                    fact_step<MODE == MODE_FACTS, WTH>(S, P, x, y, ph[k], u24(ua));
                 } else {
-                    const int a = gen_pick(S, x, y, ph[k], u24(ua));
-                    x += S.adx[a];
-                    y += S.ady[a];
+                    const int a = gen_pick(S, A, x, y, ph[k], u24(ua));
+                    x += A.adx[a];
+                    y += A.ady[a];
                 }
                 px[k] = x; py[k] = y;
                 int ix, iy;
@@ -431,6 +454,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 const bool inside = lx < (unsigned)ww && ly < (unsigned)wh;
                 if (valid && !inside && P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
                 local = (valid && inside) ? (int)(ly * ww + lx) : -1;
+                if (P.debug & 2) local = -1;
             } else if (valid) {
                 float x = px[k], y = py[k];
                 float u;
@@ -447,9 +471,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                     }
                     u = philox64_f32(sk0, sk1, (uint64_t)(p & 1023));
                 }
-                const int a = ref_pick(S, x, y, ph[k], u);
-                x = __fadd_rn(x, S.adx[a]);
-                y = __fadd_rn(y, S.ady[a]);
+                const int a = ref_pick(S, A, x, y, ph[k], u);
+                x = __fadd_rn(x, A.adx[a]);
+                y = __fadd_rn(y, A.ady[a]);
                 px[k] = x; py[k] = y;
                 int ix, iy;
                 cell_ref(x, y, P, ix, iy);
@@ -499,6 +523,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 const unsigned w = win[wi];
                 win[wi] = 0u;
                 const unsigned lo = w & 0xFFFFu, hi = w >> 16;
+                if (P.debug & 1) continue;
                 if (lo) atomicAdd(&gcount[2 * wi], lo);
                 if (hi) atomicAdd(&gcount[2 * wi + 1], hi);
             }
@@ -525,13 +550,14 @@ __global__ void __launch_bounds__(NT) k_propagate_step(float *xy, const int *hyp
                                                        unsigned p1, unsigned p2, unsigned p3,
                                                        int plen, int step) {
     __shared__ SmemTabs S;
+    __shared__ SmemAct A;
     const int tid = threadIdx.x;
     if (tid == 0) { S.m_keep = T.m_keep; S.q_kind = T.q_kind; }
     for (int k = tid; k < T.m_keep; k += NT) {
         const int j = T.keep[k];
-        S.ax[k] = T.sx[j]; S.ay[k] = T.sy[j];
-        S.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? T.pen[j] : T.at[j];
-        S.adx[k] = T.dispx[j]; S.ady[k] = T.dispy[j];
+        A.ax[k] = T.sx[j]; A.ay[k] = T.sy[j];
+        A.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? T.pen[j] : T.at[j];
+        A.adx[k] = T.dispx[j]; A.ady[k] = T.dispy[j];
     }
     for (int i = tid; i < n_hyp; i += NT) {
         S.hb[i] = beta32[i]; S.hgx[i] = goal32[2 * i]; S.hgy[i] = goal32[2 * i + 1];
@@ -554,9 +580,9 @@ __global__ void __launch_bounds__(NT) k_propagate_step(float *xy, const int *hyp
         u = philox64_f32(k0, k1, (uint64_t)(p & 1023));
     }
     const float x = xy[2 * p], y = xy[2 * p + 1];
-    const int a = ref_pick(S, x, y, hyp[p], u);
-    xy[2 * p] = __fadd_rn(x, S.adx[a]);
-    xy[2 * p + 1] = __fadd_rn(y, S.ady[a]);
+    const int a = ref_pick(S, A, x, y, hyp[p], u);
+    xy[2 * p] = __fadd_rn(x, A.adx[a]);
+    xy[2 * p + 1] = __fadd_rn(y, A.ady[a]);
 }
 
 // ---- sample_hypotheses (prediction.py:124-131) ----------------------------------------
@@ -578,12 +604,12 @@ static KTable to_ktable(const gc_action_table &a) {
     return t;
 }
 
-template <int MODE, int K>
+template <int MODE, int K, bool WTH>
 static gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t st) {
-    auto fn = k_predict<MODE, K>;
+    auto fn = k_predict<MODE, K, WTH>;
     static bool configured = false;  // per instantiation: raise the dynamic limit once
     if (!configured) {
-        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 + (int)sizeof(SmemAct)));
         configured = true;
     }
     fn<<<grid, NT, smem, st>>>(P);
@@ -591,12 +617,12 @@ static gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStr
     return cuda_check(cudaGetLastError(), "k_predict launch");
 }
 
-template <int MODE>
+template <int MODE, bool WTH>
 static gc_status dispatch_k(const KParams &P, int K, int grid, size_t smem, cudaStream_t st) {
     switch (K) {
-        case 1: return launch_predict<MODE, 1>(P, grid, smem, st);
-        case 2: return launch_predict<MODE, 2>(P, grid, smem, st);
-        default: return launch_predict<MODE, 4>(P, grid, smem, st);
+        case 1: return launch_predict<MODE, 1, WTH>(P, grid, smem, st);
+        case 2: return launch_predict<MODE, 2, WTH>(P, grid, smem, st);
+        default: return launch_predict<MODE, 4, WTH>(P, grid, smem, st);
     }
 }
 
@@ -622,6 +648,8 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.cdf = a->d_cdf; P.log_w = a->d_log_w;
     P.seed = (const unsigned long long *)a->d_seed; P.prefix = a->d_prefix; P.prefix_len = a->d_prefix_len;
     P.stream_id = a->d_stream_id;
+    static const int dbg = [] { const char *e = getenv("GC_PREDICT_DEBUG"); return e ? atoi(e) : 0; }();
+    P.debug = dbg;
     P.uniforms = a->rng_mode == GC_RNG_UNIFORMS ? a->d_uniforms : nullptr;
     P.hyp_u = a->rng_mode == GC_RNG_UNIFORMS ? a->d_hyp_u : nullptr;
     P.hyp_in = a->d_hyp_in;
@@ -676,16 +704,24 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
     const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4 + (size_t)ppc * 4;
     P.smem_window = win_bytes <= 64 * 1024 ? 1 : 0;
-    const size_t smem = P.smem_window ? win_bytes : 0;
+    P.act_off = P.smem_window ? (int)win_bytes : 0;
+    const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;
+    const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : 0);
     cudaStream_t st = (cudaStream_t)stream;
     bool stdh = fact;
     for (int b = 0; stdh && b < NBF; ++b) stdh = P.hcos[b] == hStdCos[b] && P.hsin[b] == hStdSin[b];
     const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? (stdh ? MODE_FACTS : MODE_FACT) : MODE_GEN)
                                                       : MODE_REF;
-    if (mode == MODE_REF) return dispatch_k<MODE_REF>(P, K, (int)grid, smem, st);
-    if (mode == MODE_FACTS) return dispatch_k<MODE_FACTS>(P, K, (int)grid, smem, st);
-    if (mode == MODE_FACT) return dispatch_k<MODE_FACT>(P, K, (int)grid, smem, st);
-    return dispatch_k<MODE_GEN>(P, K, (int)grid, smem, st);
+    bool wth = false;
+    for (int i = 0; i < a->n_tables; ++i) wth = wth || a->h_tables[i].w_th != 0.f;
+    if (mode == MODE_REF) return dispatch_k<MODE_REF, false>(P, K, (int)grid, smem, st);
+    if (mode == MODE_FACTS)
+        return wth ? dispatch_k<MODE_FACTS, true>(P, K, (int)grid, smem, st)
+                   : dispatch_k<MODE_FACTS, false>(P, K, (int)grid, smem, st);
+    if (mode == MODE_FACT)
+        return wth ? dispatch_k<MODE_FACT, true>(P, K, (int)grid, smem, st)
+                   : dispatch_k<MODE_FACT, false>(P, K, (int)grid, smem, st);
+    return dispatch_k<MODE_GEN, false>(P, K, (int)grid, smem, st);
 }
 
 extern "C" gc_status gc_propagate_step(float *d_xy, const int32_t *d_hyp, int32_t n, const float *d_beta32,
