@@ -114,6 +114,7 @@ struct SmemTabs {
     int list_n[2];
     int n_hyp, m_keep, q_kind, n_speeds;
     float wth;
+    unsigned char phyp[4 * 256];  // hypothesis index of particle slot k*NT+tid (frees registers)
 };
 
 // ---- reference float32 step (prediction.py:147-162), 3 passes, no stored row --------
@@ -406,6 +407,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 hi = hi < nh - 1 ? hi : nh - 1;
             }
             ph[k] = hi;
+            S.phyp[k * NT + tid] = (unsigned char)hi;
             if (P.hyp_out) P.hyp_out[(long long)h * P.n + p] = hi;
         }
     }
@@ -441,9 +443,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                     ua = r1[k]; r1[k] = r2[k]; r2[k] = r3[k];
                 }
                 if (MODE == MODE_FACT || MODE == MODE_FACTS) {
-                    fact_step<MODE == MODE_FACTS, WTH>(S, P, x, y, ph[k], u24(ua));
+                    fact_step<MODE == MODE_FACTS, WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
-                    const int a = gen_pick(S, A, x, y, ph[k], u24(ua));
+                    const int a = gen_pick(S, A, x, y, S.phyp[k * NT + tid], u24(ua));
                     x += A.adx[a];
                     y += A.ady[a];
                 }
