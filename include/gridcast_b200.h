@@ -202,6 +202,16 @@ gc_status gc_smooth_layers(const double *d_in, double *d_out, int32_t n_layers, 
                            int32_t grid_h, int32_t radius, const double *d_kernel,
                            const double *d_zx, const double *d_zy, void *stream);
 
+/* collision_field (occupancy.py:222-239) of n_layers (H, W) occupancy layers (float32 when
+ * dtype_bytes == 4, float64 when 8): the clamped-to-1 mass within the robot disc of each
+ * cell centre, h_offsets = (n_offsets, 2) int32 (dx, dy) disc offsets in the reference's
+ * order (occupancy.py:208-215, at most 33x33); outputs: d_field float64 and/or d_blocked
+ * uint8 = field >= threshold (planners/anastar.py:107-119). Bit-identical float64 sums. */
+gc_status gc_collision_field(const void *d_layers, int32_t dtype_bytes, int32_t n_layers,
+                             int32_t grid_w, int32_t grid_h, const int32_t *h_offsets,
+                             int32_t n_offsets, double threshold, double *d_field,
+                             uint8_t *d_blocked, void *stream);
+
 /* rng.derive_seed (rng.py:34-39): SeedSequence(seed, path).generate_state(2,u64) xor-folded. */
 uint64_t gc_derive_seed(uint64_t seed, const uint32_t *h_path, int32_t path_len);
 

@@ -317,6 +317,34 @@ def gen_exact(G):
     np.savez_compressed(os.path.join(OUT, "exact.npz"), log_w=b.log_weights, layers=st.layers)
 
 
+def gen_collision(G):
+    """collision_field (occupancy.py:222-239) on random layers, several radii/resolutions."""
+    from gridcast.occupancy import GridSpec, OccupancyGrid, collision_field, collision_probability
+    r = np.random.default_rng(21)
+    items, xs, ys = [], [], []
+    for (w, h, res, rad) in [(37, 23, 0.1, 0.25), (40, 40, 0.1, 0.5), (16, 30, 0.25, 0.6), (9, 9, 1.0, 0.0),
+                             (50, 20, 0.05, 0.3)]:
+        v = r.random((h, w)) * 0.05
+        v[r.random((h, w)) < 0.5] = 0
+        g = OccupancyGrid(GridSpec(w, h, res), v)
+        items.append([w, h, res, rad, collision_probability(g, (w * res * 0.4, h * res * 0.6), rad)])
+        xs.append(v.ravel())
+        ys.append(collision_field(g, rad).ravel())
+    np.savez_compressed(os.path.join(OUT, "collision.npz"), meta=json.dumps(items),
+                        x=np.concatenate(xs), y=np.concatenate(ys))
+
+
+def gen_gcst(G):
+    """A stack file written by the reference (gridio.py:36-51) for format round trips."""
+    from gridcast.gridio import save_stack
+    from gridcast.occupancy import GridSpec
+    from gridcast.prediction import PredictionStack
+    r = np.random.default_rng(5)
+    spec = GridSpec(12, 7, 0.25, (-1.5, 2.0))
+    st = PredictionStack(spec, r.random((3, 7, 12)), 4.5, 0.2)
+    save_stack(st, os.path.join(OUT, "stack_ref.grd"))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     G = _ref()
@@ -327,6 +355,8 @@ def main():
     gen_smooth(G)
     gen_multi(G)
     gen_exact(G)
+    gen_collision(G)
+    gen_gcst(G)
     import platform
     with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
         f.write(f"generated by oracle/gen_golden.py from {REF}\n")

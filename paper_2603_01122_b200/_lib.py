@@ -94,6 +94,7 @@ EXPORTS = (
     "gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
     "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
     "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
+    "gc_collision_field",
 )
 
 _lib = None
@@ -120,8 +121,9 @@ def lib():
     L.gc_sample_hypotheses.argtypes = [P, I32, I32, U64, P, I32, P, P]
     L.gc_emplace_counts.argtypes = [P, I64, I32, I32, F32, F32, F32, P, P]
     L.gc_smooth_layers.argtypes = [P, P, I32, I32, I32, I32, P, P, P, P]
+    L.gc_collision_field.argtypes = [P, I32, I32, I32, I32, P, I32, F64, P, P, P]
     for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
-               "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers"):
+               "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field"):
         getattr(L, fn).restype = ctypes.c_int
     L.gc_derive_seed.argtypes = [U64, P, I32]
     L.gc_derive_seed.restype = U64

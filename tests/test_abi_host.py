@@ -131,3 +131,27 @@ def test_window_geometry_bounds():
         c = out["counts"][t]
         assert c.sum() == case.n
         assert c[y0:y0 + h, x0:x0 + w].sum() == case.n
+
+
+def test_gcst_reads_reference_file_and_writes_identical_bytes(tmp_path):
+    """gridio format row (f1): a file written by the reference loads, and a host-backed
+    stack is written back byte-for-byte (header <4sIIII5d + row-major float64 layers)."""
+    from paper_2603_01122_b200 import gridio
+    src = os.path.join(golden_io.GOLDEN, "stack_ref.grd")
+    st = gridio.load_stack(src)
+    assert st.layers.shape == (3, 7, 12) and st.spec.origin == (-1.5, 2.0)
+    assert st.dt == 0.2 and st.base_time == 4.5 and st.spec.resolution == 0.25
+    out = tmp_path / "w.grd"
+    gridio.save_stack(st, out)
+    assert open(src, "rb").read() == open(out, "rb").read()
+    with pytest.raises(ValueError):
+        open(tmp_path / "bad.grd", "wb").write(b"XXXX" + b"\0" * 60)
+        gridio.load_stack(tmp_path / "bad.grd")
+
+
+def test_disc_offsets_order():
+    import paper_2603_01122_b200 as G
+    from paper_2603_01122_b200.occupancy import disc_offsets
+    offs = disc_offsets(G.GridSpec(10, 10, 0.1), 0.25)
+    assert offs[0].tolist() == [-1, -2] and len(offs) == 21
+    assert (np.diff(offs[:, 1]) >= 0).all()

@@ -170,3 +170,36 @@ def test_smoothing_and_emplace_helpers():
     spec = G.GridSpec(4, 4, 1.0)
     g = G.emplace(G.ParticleBatch(np.array([[-3.0, 9.0], [2.5, 2.5]], np.float32), np.zeros(2, np.int32)), spec)
     assert g.at(0, 3) == 0.5 and g.at(2, 2) == 0.5
+
+
+def test_collision_field_bit_exact():
+    """f2 row: collision_field (occupancy.py:222-239) on the GPU == the reference bit-for-bit,
+    from float64 and from float32 layers; thresholded blocked mask."""
+    from paper_2603_01122_b200.occupancy import collision_layers_device
+    z = golden_io.load("collision.npz")
+    items = json.loads(str(z["meta"]))
+    off = 0
+    for w, h, res, rad, _ in items:
+        x = z["x"][off:off + w * h].reshape(h, w)
+        y = z["y"][off:off + w * h].reshape(h, w)
+        off += w * h
+        spec = G.GridSpec(w, h, res)
+        got = G.occupancy.collision_field(G.OccupancyGrid(spec, x), rad)
+        np.testing.assert_array_equal(got, y)
+        d32 = torch.as_tensor(x.astype(np.float32)[None], device="cuda")
+        f, blk = collision_layers_device(d32, spec, rad, threshold=0.02)
+        ref32 = G.occupancy.collision_field(G.OccupancyGrid(spec, x.astype(np.float32).astype(float)), rad)
+        np.testing.assert_array_equal(f[0].cpu().numpy(), ref32)
+        np.testing.assert_array_equal(blk[0].cpu().numpy(), (ref32 >= 0.02).astype(np.uint8))
+
+
+def test_gcst_save_from_device_stack(tmp_path):
+    from paper_2603_01122_b200 import gridio
+    spec = G.GridSpec(33, 17, 0.1)
+    r = np.random.default_rng(1)
+    host = r.random((40, 17, 33))
+    dev32 = torch.as_tensor(host.astype(np.float32), device="cuda")
+    st = PR.PredictionStack(spec, dev32, 1.0, 0.02)
+    gridio.save_stack(st, tmp_path / "a.grd", chunk_layers=7)
+    back = gridio.load_stack(tmp_path / "a.grd")
+    np.testing.assert_array_equal(back.layers, host.astype(np.float32).astype(np.float64))
