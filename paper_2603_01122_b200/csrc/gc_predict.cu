@@ -64,7 +64,6 @@ struct KParams {
     unsigned *counts;
     int smem_window;
     int act_off;  // byte offset of SmemAct in dynamic shared memory (REF/GEN modes)
-    int debug;  // ablation bits (tuning only, env GC_PREDICT_DEBUG): 1 no global flush, 2 no histogram, 4 hash RNG
     int *hyp_out;
     float *xy_out;
     unsigned *error;
@@ -109,8 +108,9 @@ struct SmemTabs {
     double cdf[MAXH];
     float hb[MAXH], hgx[MAXH], hgy[MAXH];
     float hk[MAXH], hc2[MAXH], hsumH[MAXH];
-    // MODE_FACT displacement of (a, b)
+    // MODE_FACT displacement of (a, b); heading cos/sin for per-lane (divergent) lookups
     float fdx[NAF * NBF], fdy[NAF * NBF];
+    float hcos[NBF], hsin[NBF];
     int list_n[2];
     int n_hyp, m_keep, q_kind, n_speeds;
     float wth;
@@ -268,7 +268,7 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     b = b < NBF - 1 ? b : NBF - 1;
     // speed within the heading from the residual of the same uniform: given b,
     // (t - lo) is uniform on [0, H_b sum_a G_a e_b^a) (up to the 2^-24 resolution of u1)
-    const float e = ex2_approx(fmaf(A, P.hcos[b], fmaf(B, P.hsin[b], nkr)));
+    const float e = ex2_approx(fmaf(A, S.hcos[b], fmaf(B, S.hsin[b], nkr)));
     float w1 = G1 * e, w2 = G2 * e * e;
     if (WTH) {
         const float hb = ex2_approx(-S.wth * S.hb[h] * P.hth2[b]);
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             A.ady[k] = __ldg(&T.dispy[j]);
         }
     } else {
+        for (int i = tid; i < NBF; i += NT) { S.hcos[i] = P.hcos[i]; S.hsin[i] = P.hsin[i]; }
         for (int i = tid; i < NAF * NBF; i += NT) {
             const int a = i / NBF;
             const int j = a < T.n_speeds ? __ldg(&T.a_index[i]) : -1;
@@ -434,9 +435,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 // one Philox4x32-10 block per particle per four steps (one 24-bit uniform
                 // per step); the block counter is (particle, step/4, human stream, tag)
                 unsigned ua;
-                if (P.debug & 4) {
-                    ua = (unsigned)p * 0x9E3779B9u ^ (unsigned)t * 0x85EBCA6Bu;
-                } else if (((t - 1) & 3) == 0) {
+                if (((t - 1) & 3) == 0) {
                     const U4 o = philox4x32(U4{(unsigned)p, (unsigned)((t - 1) >> 2), sid, 0xA11CEu}, sk_lo, sk_hi);
                     ua = o.x; r1[k] = o.y; r2[k] = o.z; r3[k] = o.w;
                 } else {
@@ -456,7 +455,6 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 const bool inside = lx < (unsigned)ww && ly < (unsigned)wh;
                 if (valid && !inside && P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
                 local = (valid && inside) ? (int)(ly * ww + lx) : -1;
-                if (P.debug & 2) local = -1;
             } else if (valid) {
                 float x = px[k], y = py[k];
                 float u;
@@ -525,7 +523,6 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 const unsigned w = win[wi];
                 win[wi] = 0u;
                 const unsigned lo = w & 0xFFFFu, hi = w >> 16;
-                if (P.debug & 1) continue;
                 if (lo) atomicAdd(&gcount[2 * wi], lo);
                 if (hi) atomicAdd(&gcount[2 * wi + 1], hi);
             }
@@ -650,8 +647,6 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.cdf = a->d_cdf; P.log_w = a->d_log_w;
     P.seed = (const unsigned long long *)a->d_seed; P.prefix = a->d_prefix; P.prefix_len = a->d_prefix_len;
     P.stream_id = a->d_stream_id;
-    static const int dbg = [] { const char *e = getenv("GC_PREDICT_DEBUG"); return e ? atoi(e) : 0; }();
-    P.debug = dbg;
     P.uniforms = a->rng_mode == GC_RNG_UNIFORMS ? a->d_uniforms : nullptr;
     P.hyp_u = a->rng_mode == GC_RNG_UNIFORMS ? a->d_hyp_u : nullptr;
     P.hyp_in = a->d_hyp_in;
