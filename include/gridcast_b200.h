@@ -173,7 +173,26 @@ typedef struct {
     int32_t *d_action;                /* (n_humans,) snapped action index or NULL */
 } gc_belief_args;
 
+/* Exact enumeration of the bootstrapped process (prediction.py:303-377): per-hypothesis
+ * cell distributions propagated through the cell-centre transition tables, layers =
+ * belief-weighted mixtures.  float64 throughout; workspaces are caller-allocated:
+ * d_pi (n_hyp*cells*m), d_landing (cells*m int32), d_p, d_nxt (n_hyp*cells), d_pi0
+ * (n_hyp*m); d_layers (steps, H, W). */
+typedef struct {
+    int32_t n_hyp, m, grid_w, grid_h, steps, q_kind;
+    double origin_x, origin_y, res, z0x, z0y;
+    const double *d_beta, *d_goal, *d_belief;   /* (|H|), (|H|, 2), (|H|) probabilities */
+    const double *d_sx, *d_sy, *d_at, *d_pen;   /* (m) float64 utility tables */
+    const double *d_dispx, *d_dispy;            /* (m) float64 displacements */
+    const uint8_t *d_masked;                    /* (m) or NULL */
+    const double *d_qtable, *d_qtable0;         /* GC_Q_TABLE: (|H|, cells, m), (|H|, m) */
+    double *d_pi, *d_p, *d_nxt, *d_pi0;
+    int32_t *d_landing;
+    double *d_layers;
+} gc_exact_args;
+
 gc_status gc_predict(const gc_predict_args *args, void *stream);
+gc_status gc_exact_predict(const gc_exact_args *args, void *stream);
 gc_status gc_grid_epilogue(const gc_epilogue_args *args, void *stream);
 gc_status gc_belief_update(const gc_belief_args *args, void *stream);
 

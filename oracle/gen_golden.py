@@ -315,6 +315,22 @@ def gen_exact(G):
     b = G.JointBelief.from_probs([0.35, 0.35, 0.15, 0.15])
     st = exact_predict(G.HumanState(4.5, 4.5), b, 3, 1.0, cs, q, space, spec)
     np.savez_compressed(os.path.join(OUT, "exact.npz"), log_w=b.log_weights, layers=st.layers)
+    # a grid control set on a 30x24 grid (largest instances within the 2e6 cap), goal
+    # progress, stationary mask and q_default
+    from gridcast.belief import mask_stationary
+    from oracle.model import control_grid
+    v, th = control_grid(3, 8, 1.2)
+    cs2 = G.ControlSet([G.ControlAction(float(a), float(t)) for a, t in zip(v, th)])
+    space2 = G.HypothesisSpace(G.RationalitySet((0.5, 3.0)), G.GoalSet(np.array([[2.5, 1.0], [0.4, 2.0]])))
+    spec2 = G.GridSpec(30, 24, 0.1)
+    r = np.random.default_rng(4)
+    b2 = G.JointBelief.from_probs(r.dirichlet(np.ones(4)))
+    out = {}
+    for tag, q2 in (("gp", G.q_goal_progress(0.5)), ("mask", mask_stationary(G.q_goal_progress(0.5), cs2, 0.7)),
+                    ("def", G.q_default((0.5, 0.2)))):
+        st2 = exact_predict(G.HumanState(1.43, 1.17), b2, 6, 0.2, cs2, q2, space2, spec2)
+        out[tag] = st2.layers
+    np.savez_compressed(os.path.join(OUT, "exact_grid.npz"), log_w=b2.log_weights, v=v, theta=th, **out)
 
 
 def gen_collision(G):

@@ -90,11 +90,22 @@ class BeliefArgs(ctypes.Structure):
     ]
 
 
+class ExactArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_hyp", I32), ("m", I32), ("grid_w", I32), ("grid_h", I32), ("steps", I32), ("q_kind", I32),
+        ("origin_x", F64), ("origin_y", F64), ("res", F64), ("z0x", F64), ("z0y", F64),
+        ("d_beta", P), ("d_goal", P), ("d_belief", P),
+        ("d_sx", P), ("d_sy", P), ("d_at", P), ("d_pen", P),
+        ("d_dispx", P), ("d_dispy", P), ("d_masked", P), ("d_qtable", P), ("d_qtable0", P),
+        ("d_pi", P), ("d_p", P), ("d_nxt", P), ("d_pi0", P), ("d_landing", P), ("d_layers", P),
+    ]
+
+
 EXPORTS = (
     "gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
     "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
     "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
-    "gc_collision_field",
+    "gc_collision_field", "gc_exact_predict",
 )
 
 _lib = None
@@ -122,8 +133,10 @@ def lib():
     L.gc_emplace_counts.argtypes = [P, I64, I32, I32, F32, F32, F32, P, P]
     L.gc_smooth_layers.argtypes = [P, P, I32, I32, I32, I32, P, P, P, P]
     L.gc_collision_field.argtypes = [P, I32, I32, I32, I32, P, I32, F64, P, P, P]
+    L.gc_exact_predict.argtypes = [ctypes.POINTER(ExactArgs), P]
     for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
-               "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field"):
+               "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field",
+               "gc_exact_predict"):
         getattr(L, fn).restype = ctypes.c_int
     L.gc_derive_seed.argtypes = [U64, P, I32]
     L.gc_derive_seed.restype = U64

@@ -366,5 +366,65 @@ def predict_multi(humans: Sequence[tuple], cfg: PredictionConfig, control_set: C
     return PredictionStack(grid_spec, out["union64"], base_time, cfg.dt)
 
 
+def exact_predict(z_t: HumanState, belief: JointBelief, steps: int, dt: float, control_set: ControlSet,
+                  q: QFunction, space: HypothesisSpace, grid_spec: GridSpec, max_table: Optional[int] = 2_000_000,
+                  base_time: float = 0.0) -> PredictionStack:
+    """Exact layers by enumerating the bootstrapped process (prediction.py:303-377), on the
+    GPU (gc_exact_predict).  Same cap semantics as the reference (EnumerationCapExceeded
+    above ``max_table`` entries, default 2e6); pass a larger ``max_table`` (or None) to
+    enumerate instances the host-RAM reference cannot -- the tables live in HBM."""
+    from .tables import f64_tables, recognise_q
+    cells = grid_spec.width * grid_spec.height
+    n_hyp = space.size
+    m = len(control_set)
+    if max_table is not None and cells * m * n_hyp > max_table:
+        raise EnumerationCapExceeded(f"{cells} cells x {m} actions x {n_hyp} hypotheses exceeds cap "
+                                     f"{max_table}; use the Monte-Carlo predictor")
+    if len(belief) != n_hyp:
+        raise ValueError("belief size does not match hypothesis space")
+    dev = device()
+    up = lambda a_, t_: torch.as_tensor(np.ascontiguousarray(np.asarray(a_, dtype=t_)), device=dev)
+    beta_of, goal_of = hypothesis_arrays(space)
+    v, th = np.asarray(control_set.v, float), np.asarray(control_set.theta, float)
+    lq = recognise_q(q)
+    a = _lib.ExactArgs()
+    keep = []
+    if lq is not None:
+        sx, sy, at, pen = f64_tables(v, th, lq)
+        a.q_kind = _lib.GC_Q_DEFAULT if lq.family == "default" else _lib.GC_Q_GOAL_PROGRESS_FULL
+    else:
+        sx = sy = at = pen = np.zeros(m)
+        a.q_kind = _lib.GC_Q_TABLE
+        centers = grid_spec.all_centers()
+        qt = np.stack([q.table(centers, np.tile(goal_of[h], (cells, 1)), control_set) for h in range(n_hyp)])
+        qt0 = q.table(np.tile([[z_t.x, z_t.y]], (n_hyp, 1)), goal_of, control_set)
+        keep += [up(qt, np.float64), up(qt0, np.float64)]
+        a.d_qtable, a.d_qtable0 = keep[-2].data_ptr(), keep[-1].data_ptr()
+    mask = q.action_mask(control_set)
+    disp = control_set.displacements(dt)
+    t_beta, t_goal, t_b = up(beta_of, np.float64), up(goal_of, np.float64), up(belief.probs(), np.float64)
+    t_sx, t_sy, t_at, t_pen = up(sx, np.float64), up(sy, np.float64), up(at, np.float64), up(pen, np.float64)
+    t_dx, t_dy = up(disp[:, 0], np.float64), up(disp[:, 1], np.float64)
+    t_mask = up(mask.astype(np.uint8), np.uint8) if mask is not None else None
+    pi = torch.empty(n_hyp * cells * m, dtype=torch.float64, device=dev)
+    land = torch.empty(cells * m, dtype=torch.int32, device=dev)
+    p = torch.empty(n_hyp * cells, dtype=torch.float64, device=dev)
+    nxt = torch.empty_like(p)
+    pi0 = torch.empty(n_hyp * m, dtype=torch.float64, device=dev)
+    layers = torch.empty((steps, grid_spec.height, grid_spec.width), dtype=torch.float64, device=dev)
+    a.n_hyp, a.m, a.grid_w, a.grid_h, a.steps = n_hyp, m, grid_spec.width, grid_spec.height, int(steps)
+    a.origin_x, a.origin_y, a.res = grid_spec.origin[0], grid_spec.origin[1], grid_spec.resolution
+    a.z0x, a.z0y = float(z_t.x), float(z_t.y)
+    a.d_beta, a.d_goal, a.d_belief = t_beta.data_ptr(), t_goal.data_ptr(), t_b.data_ptr()
+    a.d_sx, a.d_sy, a.d_at, a.d_pen = t_sx.data_ptr(), t_sy.data_ptr(), t_at.data_ptr(), t_pen.data_ptr()
+    a.d_dispx, a.d_dispy = t_dx.data_ptr(), t_dy.data_ptr()
+    a.d_masked = t_mask.data_ptr() if t_mask is not None else None
+    a.d_pi, a.d_p, a.d_nxt, a.d_pi0 = pi.data_ptr(), p.data_ptr(), nxt.data_ptr(), pi0.data_ptr()
+    a.d_landing, a.d_layers = land.data_ptr(), layers.data_ptr()
+    _lib.check(_lib.lib().gc_exact_predict(ctypes.byref(a), stream_handle()), "exact_predict")
+    torch.cuda.current_stream().synchronize()
+    return PredictionStack(grid_spec, layers, base_time, dt)
+
+
 def total_variation(a, b) -> float:
     return 0.5 * float(np.abs(np.asarray(a, dtype=float) - np.asarray(b, dtype=float)).sum())

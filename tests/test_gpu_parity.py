@@ -203,3 +203,37 @@ def test_gcst_save_from_device_stack(tmp_path):
     gridio.save_stack(st, tmp_path / "a.grd", chunk_layers=7)
     back = gridio.load_stack(tmp_path / "a.grd")
     np.testing.assert_array_equal(back.layers, host.astype(np.float32).astype(np.float64))
+
+
+def test_exact_predict_gpu_matches_reference():
+    """f4 row: GPU exact enumeration vs the reference's exact_predict (lattice + a grid
+    control set with goal-progress, stationary-masked and q_default utilities)."""
+    z = golden_io.load("exact.npz")
+    case = golden_io.PredictCase("lattice")
+    cs, space, q, spec = _objects(case)
+    st = G.exact_predict(G.HumanState(4.5, 4.5), G.JointBelief(z["log_w"]), 3, 1.0, cs, q, space, spec)
+    np.testing.assert_allclose(st.layers, z["layers"], rtol=0, atol=1e-14)
+    with pytest.raises(PR.EnumerationCapExceeded):
+        G.exact_predict(G.HumanState(4.5, 4.5), G.JointBelief(z["log_w"]), 2, 1.0, cs, q, space, spec, max_table=10)
+    zg = golden_io.load("exact_grid.npz")
+    cs2 = G.ControlSet([G.ControlAction(float(a), float(t)) for a, t in zip(zg["v"], zg["theta"])])
+    space2 = G.HypothesisSpace(G.RationalitySet((0.5, 3.0)), G.GoalSet(np.array([[2.5, 1.0], [0.4, 2.0]])))
+    spec2 = G.GridSpec(30, 24, 0.1)
+    b2 = G.JointBelief(zg["log_w"])
+    for tag, q2 in (("gp", G.q_goal_progress(0.5)), ("mask", G.mask_stationary(G.q_goal_progress(0.5), cs2, 0.7)),
+                    ("def", G.q_default((0.5, 0.2)))):
+        st2 = G.exact_predict(G.HumanState(1.43, 1.17), b2, 6, 0.2, cs2, q2, space2, spec2)
+        np.testing.assert_allclose(st2.layers, zg[tag], rtol=0, atol=1e-13)
+        np.testing.assert_allclose(st2.layers.sum(axis=(1, 2)), 1.0, atol=1e-12)
+
+
+def test_exact_predict_beyond_reference_cap():
+    """The HBM-resident tables enumerate a cfg1-sized instance (100x100 cells x 96 actions
+    x 10 hypotheses = 9.6e6 entries, 4.8x the reference's 2e6 cap)."""
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    space = G.HypothesisSpace(G.RationalitySet.log_spaced(5), G.GoalSet(np.array([[8.5, 5.0], [1.5, 7.0]])))
+    spec = G.GridSpec(100, 100, 0.1)
+    st = G.exact_predict(G.HumanState(5.05, 5.05), G.init_belief(space), 10, 0.1, cs, G.q_goal_progress(0.5),
+                         space, spec, max_table=None)
+    np.testing.assert_allclose(st.layers.sum(axis=(1, 2)), 1.0, atol=1e-12)
+    assert (st.layers >= 0).all()
