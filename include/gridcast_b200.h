@@ -131,8 +131,8 @@ typedef struct {
     int32_t grid_w, grid_h;
     int32_t radius;            /* ceil(3 sigma_cells); 0 = no smoothing */
     const double *d_kernel;    /* (2*radius+1,) exp(-0.5 (o/sigma_cells)^2) */
-    const double *d_zx;        /* (grid_w,) in-grid kernel mass per source column */
-    const double *d_zy;        /* (grid_h,) */
+    const double *d_zx;        /* (grid_w,) 1 / in-grid kernel mass per source column */
+    const double *d_zy;        /* (grid_h,) 1 / in-grid kernel mass per source row */
     float origin_x32, origin_y32, res32;
     int32_t n_tiles;           /* tiles per human (static geometry) */
     const float *d_start_xy;   /* (n_humans, 2) float32 start positions */
@@ -216,7 +216,8 @@ gc_status gc_emplace_counts(const float *d_xy, int64_t n, int32_t grid_w, int32_
                             float origin_x32, float origin_y32, float res32, uint32_t *d_counts,
                             void *stream);
 
-/* smooth_values (occupancy.py:139-154) on n_layers float64 (H, W) layers, d_in != d_out. */
+/* smooth_values (occupancy.py:139-154) on n_layers float64 (H, W) layers, d_in != d_out;
+ * d_zx / d_zy hold the reciprocal in-grid kernel masses (column normalisation). */
 gc_status gc_smooth_layers(const double *d_in, double *d_out, int32_t n_layers, int32_t grid_w,
                            int32_t grid_h, int32_t radius, const double *d_kernel,
                            const double *d_zx, const double *d_zy, void *stream);

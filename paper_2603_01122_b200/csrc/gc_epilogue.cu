@@ -43,12 +43,14 @@ __device__ __forceinline__ void cell_of_start(float x, float y, const EParams &P
     iy = fy < 0.f ? 0 : (fy > (float)(P.grid_h - 1) ? P.grid_h - 1 : (int)fy);
 }
 
+// RAD >= 0: compile-time smoothing radius (tile edges become constants); RAD < 0: runtime
+template <int RAD>
 __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
     extern __shared__ __align__(16) double esm[];
     const int h = blockIdx.y;
     const int4 tl = P.tiles[blockIdx.x];
     const int t = tl.x;
-    const int rad = P.radius;
+    const int rad = RAD >= 0 ? RAD : P.radius;
     const int E = ET + 2 * rad;
     double *vin = esm;            // E x E
     double *vmid = esm + E * E;   // ET x E
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
             const unsigned c = __ldg(&cnt[(Y - y0) * ww + (X - x0)]);
             if (c) {
                 v = (double)c / (double)P.n;  // exactly the reference's counts / n
-                if (rad > 0) v = v / __ldg(&P.zy[Y]) / __ldg(&P.zx[X]);
+                if (rad > 0) v = v * __ldg(&P.zy[Y]) * __ldg(&P.zx[X]);  // reciprocal in-grid masses
             }
         }
         vin[i] = v;
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(ENT) k_smooth(const double *in, double *out, i
         const int ly = i / E, lx = i - ly * E;
         const int X = X0 - rad + lx, Y = Y0 - rad + ly;
         double v = 0.0;
-        if (X >= 0 && X < W && Y >= 0 && Y < H) v = src[(long long)Y * W + X] / zy[Y] / zx[X];
+        if (X >= 0 && X < W && Y >= 0 && Y < H) v = src[(long long)Y * W + X] * zy[Y] * zx[X];  // reciprocal in-grid masses
         vin[i] = v;
     }
     __syncthreads();
@@ -230,10 +232,16 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
     const int E = ET + 2 * a->radius;
     const size_t smem = (size_t)(E * E + (a->radius > 0 ? ET * E : 0)) * sizeof(double);
     if (smem > 48 * 1024)
-        GC_CUDA(cudaFuncSetAttribute(k_epilogue, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GC_CUDA(cudaFuncSetAttribute(k_epilogue<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaStream_t st = (cudaStream_t)stream;
     dim3 grid(a->n_tiles, a->n_humans);
-    k_epilogue<<<grid, ENT, smem, st>>>(P);
+    switch (a->radius) {
+        case 0: k_epilogue<0><<<grid, ENT, smem, st>>>(P); break;
+        case 1: k_epilogue<1><<<grid, ENT, smem, st>>>(P); break;
+        case 2: k_epilogue<2><<<grid, ENT, smem, st>>>(P); break;
+        case 3: k_epilogue<3><<<grid, ENT, smem, st>>>(P); break;
+        default: k_epilogue<-1><<<grid, ENT, smem, st>>>(P); break;
+    }
     count_launch();
     GC_TRY(cuda_check(cudaGetLastError(), "k_epilogue launch"));
     if (a->time_union && a->steps > 1) {

@@ -51,6 +51,10 @@ class EngineConfig:
     union_dtype: str = "float32"       # fused union precision: float32 | float64
     time_union: bool = False
     per_human_layers: bool = False
+    # planner input (anastar.py:107-119, mppi.py:87-94): collision field of the fused
+    # union thresholded into a (T, H, W) uint8 blocked mask each cycle; None = off
+    robot_radius: Optional[float] = None
+    collision_threshold: float = 0.1
 
 
 class CycleEngine:
@@ -124,6 +128,11 @@ class CycleEngine:
         self.layers = (torch.zeros((H, T, Hh, W), dtype=torch.float64, device=dev)
                        if cfg.per_human_layers else None)
         self.d_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.blocked = None
+        if cfg.robot_radius is not None:
+            from .occupancy import disc_offsets
+            self._disc = np.ascontiguousarray(disc_offsets(grid_spec, cfg.robot_radius))
+            self.blocked = [torch.zeros((T, Hh, W), dtype=torch.uint8, device=dev) for _ in range(2)]
         self._tarr = (_lib.ActionTable * 2)(*[t.struct for t in self.tables])
         self.last_xy = None
         self.heading = np.zeros(H)
@@ -216,6 +225,11 @@ class CycleEngine:
             e.d_union64 = u.data_ptr()
         e.time_union = int(cfg.time_union)
         _lib.check(_lib.lib().gc_grid_epilogue(ctypes.byref(e), sh), "gc_grid_epilogue")
+        if self.blocked is not None:
+            _lib.check(_lib.lib().gc_collision_field(
+                ctypes.c_void_p(u.data_ptr()), u.element_size(), cfg.steps, self.spec.width, self.spec.height,
+                self._disc.ctypes.data_as(ctypes.c_void_p), len(self._disc), float(cfg.collision_threshold),
+                None, ctypes.c_void_p(self.blocked[buf].data_ptr()), sh), "gc_collision_field")
         if events is not None:
             events[2].record(stream)
 
@@ -252,6 +266,11 @@ class CycleEngine:
     def posterior(self, i: int) -> np.ndarray:
         a, b = self.hyp_off[i], self.hyp_off[i + 1]
         return self.d_logw[a:b].cpu().numpy()
+
+    def reset_belief(self, i: int):
+        """Uniform belief for human i (goal departure, sim.py:563-568; belief.py:120-123)."""
+        a, b = int(self.hyp_off[i]), int(self.hyp_off[i + 1])
+        self.d_logw[a:b] = -math.log(b - a)
 
     def check_errors(self):
         if int(self.d_err.item()) != 0:

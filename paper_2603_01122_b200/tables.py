@@ -252,8 +252,8 @@ class Geometry:
         self.d_step_off = dev(self.step_off)
         self.d_tiles = dev(np.asarray(tiles, dtype=np.int32))
         self.d_kernel = dev(k.astype(np.float64))
-        self.d_zx = dev(zmass(self.W))
-        self.d_zy = dev(zmass(self.H))
+        self.d_zx = dev(1.0 / zmass(self.W))  # reciprocal column masses (kernels multiply)
+        self.d_zy = dev(1.0 / zmass(self.H))
         del side
 
     def window(self, start_xy32, t):

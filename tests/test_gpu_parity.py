@@ -237,3 +237,39 @@ def test_exact_predict_beyond_reference_cap():
                          space, spec, max_table=None)
     np.testing.assert_allclose(st.layers.sum(axis=(1, 2)), 1.0, atol=1e-12)
     assert (st.layers >= 0).all()
+
+
+def test_engine_cycle_matches_reference_mode_and_blocked_mask():
+    """CycleEngine (sim.py:455-504 pattern) in reference mode: its fused union equals the
+    per-human reference-mode union of the same humans/prefixes/seed, its posteriors equal
+    update_belief, and its blocked mask equals collision_field(union) >= threshold."""
+    from paper_2603_01122_b200.engine import CycleEngine, EngineConfig
+    from paper_2603_01122_b200.scenario import make_scene
+    sc = make_scene("cfg1", cycles=3, humans=3)
+    cfg = EngineConfig(n=1500, steps=8, dt=0.1, smoothing_sigma=0.1, seed=5, mode="reference",
+                       union_dtype="float64", robot_radius=0.25, collision_threshold=0.05)
+    eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
+    eng.prime(sc.prev_xy)
+    eng.stage(sc.track[0], buf=0)
+    eng.run_cycle(buf=0)
+    torch.cuda.synchronize()
+    from paper_2603_01122_b200 import rng
+    seed = rng.derive_seed(5, 7, 0)
+    layers = []
+    for i, sp in enumerate(sc.spaces):
+        prior = G.init_belief(sp)
+        post = G.update_belief(prior, G.HumanState(*sc.prev_xy[i]), G.HumanState(*sc.track[0][i]), 0.1,
+                               sc.control_set, sc.q, sp, snap_tol=math.inf)
+        np.testing.assert_allclose(np.exp(eng.posterior(i)), post.probs(), rtol=1e-12, atol=1e-300)
+        moved = np.hypot(*(sc.track[0][i] - sc.prev_xy[i])) / 0.1
+        q = G.mask_stationary(sc.q, sc.control_set, 0.5) if moved < 0.05 else sc.q
+        pc = G.PredictionConfig(n=1500, steps=8, dt=0.1, smoothing_sigma=0.1, seed=seed)
+        layers.append(G.predict(G.HumanState(*sc.track[0][i]), post, pc, sc.control_set, q, sp, sc.spec,
+                                prefix=(2, i)).layers)
+    union = np.maximum.reduce(layers)
+    np.testing.assert_allclose(eng.unions[0].cpu().numpy(), union, rtol=0, atol=1e-15)
+    from paper_2603_01122_b200.occupancy import collision_layers_device
+    f, _ = collision_layers_device(torch.as_tensor(union, device="cuda"), sc.spec, 0.25)
+    np.testing.assert_array_equal(eng.blocked[0].cpu().numpy(), (f.cpu().numpy() >= 0.05).astype(np.uint8))
+    eng.reset_belief(1)
+    np.testing.assert_allclose(np.exp(eng.posterior(1)), 1.0 / sc.spaces[1].size)
