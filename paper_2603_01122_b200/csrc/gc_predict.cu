@@ -487,30 +487,19 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             // whole warp on one cell (early steps): one aggregated add; else per lane.
             // A word seen zero by its first add is appended to the touched list
             // (warp-aggregated: one shared atomic per warp).
-            const int l0 = __shfl_sync(0xffffffffu, local, 0);
-            const bool uni = __all_sync(0xffffffffu, local == l0);
             if (P.smem_window) {
                 bool first = false;
-                if (uni) {
-                    if (lane == 0 && l0 >= 0)
-                        first = atomicAdd(&win[l0 >> 1], 32u << ((l0 & 1) << 4)) == 0u;
-                } else if (local >= 0) {
-                    first = atomicAdd(&win[local >> 1], 1u << ((local & 1) << 4)) == 0u;
-                }
+                if (local >= 0) first = atomicAdd(&win[local >> 1], 1u << ((local & 1) << 4)) == 0u;
                 const unsigned m = __ballot_sync(0xffffffffu, first);
                 if (m) {
                     const int leader = __ffs(m) - 1;
                     int base = 0;
                     if (lane == leader) base = atomicAdd(&S.list_n[t & 1], __popc(m));
                     base = __shfl_sync(0xffffffffu, base, leader);
-                    if (first) list[base + __popc(m & ((1u << lane) - 1u))] = (uni ? l0 : local) >> 1;
+                    if (first) list[base + __popc(m & ((1u << lane) - 1u))] = local >> 1;
                 }
-            } else {
-                if (uni) {
-                    if (lane == 0 && l0 >= 0) atomicAdd(&gcount[l0], 32u);
-                } else if (local >= 0) {
-                    atomicAdd(&gcount[local], 1u);
-                }
+            } else if (local >= 0) {
+                atomicAdd(&gcount[local], 1u);
             }
         }
         if (P.smem_window) {
