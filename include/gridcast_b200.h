@@ -191,7 +191,28 @@ typedef struct {
     double *d_layers;
 } gc_exact_args;
 
+/* MPPI control update (planners/mppi.py:149-243) against a device blocked mask. */
+typedef struct {
+    int32_t n_rollouts, horizon;
+    double dt, temperature, std_a, std_w;
+    double q[4], qf[4], r[2];
+    double collision_penalty;
+    int32_t quadratic_control_cost;
+    double a_max, omega_max, v_max;
+    double z[4], goal[4];                 /* robot state and goal (x, y, v, theta) */
+    const double *d_nominal;              /* (K, 2) */
+    const double *d_noise;                /* (N, K, 2) perturbations (already x std), or NULL */
+    uint64_t seed;                        /* production noise (Philox4x32-10 + Box-Muller) */
+    const uint8_t *d_blocked;             /* (L, H, W) or NULL */
+    int32_t n_layers, grid_w, grid_h;
+    double origin_x, origin_y, res;
+    const int32_t *d_layer_of;            /* (K) blocked layer per horizon step */
+    double *d_noise_out;                  /* (N, K, 2) generated noise (when d_noise == NULL) */
+    double *d_costs, *d_controls, *d_weights, *d_diag; /* (N), (K, 2), (N), (3) */
+} gc_mppi_args;
+
 gc_status gc_predict(const gc_predict_args *args, void *stream);
+gc_status gc_mppi_step(const gc_mppi_args *args, void *stream);
 gc_status gc_exact_predict(const gc_exact_args *args, void *stream);
 gc_status gc_grid_epilogue(const gc_epilogue_args *args, void *stream);
 gc_status gc_belief_update(const gc_belief_args *args, void *stream);

@@ -361,6 +361,31 @@ def gen_gcst(G):
     save_stack(st, os.path.join(OUT, "stack_ref.grd"))
 
 
+def gen_mppi(G):
+    """mppi_step (planners/mppi.py:149-243) with and without a prediction stack."""
+    from gridcast.planners.mppi import MppiConfig, mppi_step
+    from gridcast.agents import RobotState
+    from gridcast.occupancy import GridSpec
+    from gridcast.prediction import PredictionStack
+    r = np.random.default_rng(8)
+    spec = GridSpec(60, 40, 0.1)
+    layers = np.zeros((12, 40, 60))
+    for k in range(12):
+        layers[k, 15:25, 20 + k:30 + k] = r.random((10, 10)) * 0.2
+    stack = PredictionStack(spec, layers, 0.0, 0.1)
+    z = RobotState(1.0, 2.0, 0.4, 0.3)
+    goal = RobotState(5.0, 2.2, 0.0, 0.0)
+    out = {}
+    for tag, st, qc, n in (("nostack", None, False, 512), ("stack", stack, False, 700), ("quad", stack, True, 300)):
+        cfg = MppiConfig(horizon=20, rollouts=n, dt=0.1, quadratic_control_cost=qc, seed=3)
+        nominal = r.normal(0, 0.2, (20, 2))
+        controls, diag = mppi_step(z, nominal, goal, st, cfg, seed=11)
+        out[tag + "_nominal"] = nominal
+        out[tag + "_controls"] = controls
+        out[tag + "_costs"] = diag.costs
+    np.savez_compressed(os.path.join(OUT, "mppi.npz"), layers=layers, **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     G = _ref()
@@ -373,6 +398,7 @@ def main():
     gen_exact(G)
     gen_collision(G)
     gen_gcst(G)
+    gen_mppi(G)
     import platform
     with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
         f.write(f"generated by oracle/gen_golden.py from {REF}\n")

@@ -101,11 +101,27 @@ class ExactArgs(ctypes.Structure):
     ]
 
 
+class MppiArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_rollouts", I32), ("horizon", I32),
+        ("dt", F64), ("temperature", F64), ("std_a", F64), ("std_w", F64),
+        ("q", F64 * 4), ("qf", F64 * 4), ("r", F64 * 2), ("collision_penalty", F64),
+        ("quadratic_control_cost", I32),
+        ("a_max", F64), ("omega_max", F64), ("v_max", F64),
+        ("z", F64 * 4), ("goal", F64 * 4),
+        ("d_nominal", P), ("d_noise", P), ("seed", U64), ("d_blocked", P),
+        ("n_layers", I32), ("grid_w", I32), ("grid_h", I32),
+        ("origin_x", F64), ("origin_y", F64), ("res", F64),
+        ("d_layer_of", P), ("d_noise_out", P),
+        ("d_costs", P), ("d_controls", P), ("d_weights", P), ("d_diag", P),
+    ]
+
+
 EXPORTS = (
     "gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
     "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
     "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
-    "gc_collision_field", "gc_exact_predict",
+    "gc_collision_field", "gc_exact_predict", "gc_mppi_step",
 )
 
 _lib = None
@@ -134,9 +150,10 @@ def lib():
     L.gc_smooth_layers.argtypes = [P, P, I32, I32, I32, I32, P, P, P, P]
     L.gc_collision_field.argtypes = [P, I32, I32, I32, I32, P, I32, F64, P, P, P]
     L.gc_exact_predict.argtypes = [ctypes.POINTER(ExactArgs), P]
+    L.gc_mppi_step.argtypes = [ctypes.POINTER(MppiArgs), P]
     for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
                "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field",
-               "gc_exact_predict"):
+               "gc_exact_predict", "gc_mppi_step"):
         getattr(L, fn).restype = ctypes.c_int
     L.gc_derive_seed.argtypes = [U64, P, I32]
     L.gc_derive_seed.restype = U64

@@ -273,3 +273,31 @@ def test_engine_cycle_matches_reference_mode_and_blocked_mask():
     np.testing.assert_array_equal(eng.blocked[0].cpu().numpy(), (f.cpu().numpy() >= 0.05).astype(np.uint8))
     eng.reset_belief(1)
     np.testing.assert_allclose(np.exp(eng.posterior(1)), 1.0 / sc.spaces[1].size)
+
+
+@pytest.mark.parametrize("tag,with_stack,quad,n", [("nostack", False, False, 512), ("stack", True, False, 700),
+                                                  ("quad", True, True, 300)])
+def test_mppi_step_matches_reference(tag, with_stack, quad, n):
+    """f3 row: GPU MPPI with the reference's noise streams vs the reference mppi_step."""
+    from paper_2603_01122_b200 import planners as PL
+    z = golden_io.load("mppi.npz")
+    spec = G.GridSpec(60, 40, 0.1)
+    stack = PR.PredictionStack(spec, z["layers"], 0.0, 0.1) if with_stack else None
+    cfg = PL.MppiConfig(horizon=20, rollouts=n, dt=0.1, quadratic_control_cost=quad, seed=3)
+    controls, diag = PL.mppi_step(PL.RobotState(1.0, 2.0, 0.4, 0.3), z[tag + "_nominal"],
+                                  PL.RobotState(5.0, 2.2, 0.0, 0.0), stack, cfg, seed=11)
+    np.testing.assert_allclose(diag.costs, z[tag + "_costs"], rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(controls, z[tag + "_controls"], rtol=1e-10, atol=1e-12)
+
+
+def test_mppi_production_noise_statistics():
+    """In-register Gaussian perturbations give the same control update (an MC estimate of
+    the same path integral) as the reference streams, within sampling noise."""
+    from paper_2603_01122_b200 import planners as PL
+    cfg = PL.MppiConfig(horizon=10, rollouts=65536, dt=0.1, seed=5, temperature=20.0)
+    args = (PL.RobotState(0.0, 0.0, 0.5, 0.0), np.zeros((10, 2)), PL.RobotState(3.0, 0.0, 0.0, 0.0), None, cfg)
+    cp, dp = PL.mppi_step(*args, noise="production")
+    cr, dr = PL.mppi_step(*args, noise="reference")
+    assert np.isfinite(cp).all() and dp.weight_entropy > 0
+    np.testing.assert_allclose(cp, cr, atol=0.02)
+    assert abs(dp.mean_cost - dr.mean_cost) < 0.01 * abs(dr.mean_cost)
