@@ -23,37 +23,42 @@ struct DiscOffsets {
     int2 o[CMAXOFF];
 };
 
-template <typename Tin>
-__global__ void __launch_bounds__(CNT) k_collision(const Tin *in, int W, int H, int rc, int n_off,
+// The tile is zero-padded outside the grid; adding +0.0 to a non-negative float64 partial
+// sum leaves it bit-unchanged, so summing every offset over the padded tile reproduces the
+// reference's in-grid-only sequential sum exactly, without per-offset bounds checks.
+template <typename Tin, int RC>
+__global__ void __launch_bounds__(CNT) k_collision(const Tin *in, int W, int H, int rc_rt, int n_off,
                                                    double threshold, double *field, unsigned char *blocked,
                                                    const __grid_constant__ DiscOffsets D) {
     extern __shared__ __align__(16) double tile[];
+    const int rc = RC >= 0 ? RC : rc_rt;
     const int E = CT + 2 * rc;
     const int L = blockIdx.z;
     const int X0 = blockIdx.x * CT, Y0 = blockIdx.y * CT;
     const Tin *src = in + (long long)L * W * H;
-    for (int i = threadIdx.x; i < E * E; i += CNT) {
-        const int ly = i / E, lx = i - ly * E;
-        const int X = X0 - rc + lx, Y = Y0 - rc + ly;
-        tile[i] = (X >= 0 && X < W && Y >= 0 && Y < H) ? (double)src[(long long)Y * W + X] : 0.0;
+    for (int ly = threadIdx.x / CT; ly < E; ly += CNT / CT) {
+        const int Y = Y0 - rc + ly;
+        for (int lx = threadIdx.x % CT; lx < E; lx += CT) {
+            const int X = X0 - rc + lx;
+            tile[ly * E + lx] = (X >= 0 && X < W && Y >= 0 && Y < H) ? (double)src[(long long)Y * W + X] : 0.0;
+        }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < CT * CT; i += CNT) {
-        const int yy = i / CT, xx = i - yy * CT;
-        const int X = X0 + xx, Y = Y0 + yy;
+    const int xx = threadIdx.x % CT;
+    const int X = X0 + xx;
+    for (int yy = threadIdx.x / CT; yy < CT; yy += CNT / CT) {
+        const int Y = Y0 + yy;
         if (X >= W || Y >= H) continue;
+        const double *base = tile + (yy + rc) * E + (xx + rc);
         double s = 0.0;
         for (int k = 0; k < n_off; ++k) {
             const int2 o = D.o[k];
-            const int sx = X + o.x, sy = Y + o.y;
-            // out-of-grid sources are skipped, not added as zero (keeps the reference's
-            // exact summation sequence; -0.0/+0.0 cannot differ for non-negative inputs)
-            if (sx >= 0 && sx < W && sy >= 0 && sy < H) s += tile[(yy + rc + o.y) * E + (xx + rc + o.x)];
+            s += base[o.y * E + o.x];
         }
         s = s < 1.0 ? s : 1.0;  // np.minimum(out, 1.0)
-        const long long o = (long long)L * W * H + (long long)Y * W + X;
-        if (field) field[o] = s;
-        if (blocked) blocked[o] = s >= threshold ? 1 : 0;
+        const long long oi = (long long)L * W * H + (long long)Y * W + X;
+        if (field) field[oi] = s;
+        if (blocked) blocked[oi] = s >= threshold ? 1 : 0;
     }
 }
 
@@ -83,17 +88,24 @@ extern "C" gc_status gc_collision_field(const void *d_layers, int32_t dtype_byte
     const int E = CT + 2 * rc;
     const size_t smem = (size_t)E * E * sizeof(double);
     dim3 grid((grid_w + CT - 1) / CT, (grid_h + CT - 1) / CT, n_layers);
+#define GC_COLL_LAUNCH(T, R)                                                                      \
+    do {                                                                                          \
+        if (smem > 48 * 1024)                                                                     \
+            GC_CUDA(cudaFuncSetAttribute(k_collision<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         (int)smem));                                             \
+        k_collision<T, R><<<grid, CNT, smem, st>>>((const T *)d_layers, grid_w, grid_h, rc, n_offsets,   \
+                                                    threshold, d_field, d_blocked, local);          \
+    } while (0)
     if (dtype_bytes == 4) {
-        if (smem > 48 * 1024)
-            GC_CUDA(cudaFuncSetAttribute(k_collision<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_collision<float><<<grid, CNT, smem, st>>>((const float *)d_layers, grid_w, grid_h, rc, n_offsets,
-                                                     threshold, d_field, d_blocked, local);
+        if (rc == 2) GC_COLL_LAUNCH(float, 2);
+        else if (rc == 3) GC_COLL_LAUNCH(float, 3);
+        else GC_COLL_LAUNCH(float, -1);
     } else {
-        if (smem > 48 * 1024)
-            GC_CUDA(cudaFuncSetAttribute(k_collision<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_collision<double><<<grid, CNT, smem, st>>>((const double *)d_layers, grid_w, grid_h, rc, n_offsets,
-                                                      threshold, d_field, d_blocked, local);
+        if (rc == 2) GC_COLL_LAUNCH(double, 2);
+        else if (rc == 3) GC_COLL_LAUNCH(double, 3);
+        else GC_COLL_LAUNCH(double, -1);
     }
+#undef GC_COLL_LAUNCH
     count_launch();
     return cuda_check(cudaGetLastError(), "k_collision launch");
 }

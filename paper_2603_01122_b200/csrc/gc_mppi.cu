@@ -132,14 +132,6 @@ __global__ void __launch_bounds__(1024) k_mppi_reduce(const MParams P) {
     __syncthreads();
     for (int n = tid; n < P.N; n += blockDim.x) P.weights[n] /= total;
     __syncthreads();
-    const double *noise = P.noise_in ? P.noise_in : P.noise_out;
-    for (int o = tid; o < 2 * P.K; o += blockDim.x) {
-        double acc = 0.0;
-        for (int n = 0; n < P.N; ++n) acc += P.weights[n] * noise[(long long)n * 2 * P.K + o];
-        double u = P.nominal[o] + acc;
-        const double lim = (o & 1) ? P.w_max : P.a_max;
-        P.controls[o] = fmin(fmax(u, -lim), lim);
-    }
     // diagnostics: best cost, mean finite cost, weight entropy
     double ent = 0.0, fin = 0.0, cnt = 0.0;
     for (int n = tid; n < P.N; n += blockDim.x) {
@@ -173,6 +165,27 @@ __global__ void __launch_bounds__(1024) k_mppi_reduce(const MParams P) {
     if (tid == 0) P.diag[1] = fsum / red[0];
 }
 
+// weighted perturbation average: one CTA per control output (t, component), fixed-tree
+// reduction over rollouts, then the actuation clamp
+__global__ void __launch_bounds__(256) k_mppi_average(const MParams P) {
+    __shared__ double red[256];
+    const int o = blockIdx.x;
+    const double *noise = P.noise_in ? P.noise_in : P.noise_out;
+    double acc = 0.0;
+    for (int n = threadIdx.x; n < P.N; n += blockDim.x) acc += P.weights[n] * noise[(long long)n * 2 * P.K + o];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double lim = (o & 1) ? P.w_max : P.a_max;
+        const double u = P.nominal[o] + red[0];
+        P.controls[o] = fmin(fmax(u, -lim), lim);
+    }
+}
+
 }  // namespace gc
 
 using namespace gc;
@@ -197,8 +210,9 @@ extern "C" gc_status gc_mppi_step(const gc_mppi_args *a, void *stream) {
     P.layer_of = a->d_layer_of; P.noise_out = a->d_noise_out; P.costs = a->d_costs; P.controls = a->d_controls;
     P.weights = a->d_weights; P.diag = a->d_diag;
     cudaStream_t st = (cudaStream_t)stream;
-    k_mppi_rollouts<<<(P.N + 127) / 128, 128, 0, st>>>(P);
+    k_mppi_rollouts<<<(P.N + 63) / 64, 64, 0, st>>>(P);
     k_mppi_reduce<<<1, 1024, 0, st>>>(P);
-    count_launch(2);
+    k_mppi_average<<<2 * P.K, 256, 0, st>>>(P);
+    count_launch(3);
     return cuda_check(cudaGetLastError(), "gc_mppi_step launch");
 }
