@@ -83,18 +83,17 @@ __device__ __forceinline__ void cell_ref(float x, float y, const KParams &P, int
 // compete with the exponentials): clamp to [-1, W], round with the 1.5*2^23 magic
 // constant, correct round-up to floor, clamp to the grid.  Differs from the IEEE
 // division form only for positions within an ulp of a cell edge.
-__device__ __forceinline__ int floor_clamp(float f, int n) {
-    f = fminf(fmaxf(f, -1.f), (float)n);
+__device__ __forceinline__ int floor_clamp(float f, float nm1) {
+    // clamp(floor(f), 0, n-1) == floor(clamp(f, 0, n-1)) for any f
+    f = fminf(fmaxf(f, 0.f), nm1);
     const float r = f + 12582912.f;
     const float fr = r - 12582912.f;
-    int i = __float_as_int(r) - 0x4B400000;
-    i -= (fr > f) ? 1 : 0;
-    return min(max(i, 0), n - 1);
+    return (__float_as_int(r) - 0x4B400000) - ((fr > f) ? 1 : 0);
 }
 
 __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, int &ix, int &iy) {
-    ix = floor_clamp((x - P.ox) * P.inv_res, P.grid_w);
-    iy = floor_clamp((y - P.oy) * P.inv_res, P.grid_h);
+    ix = floor_clamp((x - P.ox) * P.inv_res, (float)(P.grid_w - 1));
+    iy = floor_clamp((y - P.oy) * P.inv_res, (float)(P.grid_h - 1));
 }
 
 // MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
@@ -210,7 +209,9 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
                                           int h, float u1) {
     const float rx = x - S.hgx[h], ry = y - S.hgy[h];
     const float r2 = fmaf(rx, rx, ry * ry);
-    const float r = r2 * rsqrtf(fmaxf(r2, 1e-30f));
+    float rs;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(r2, 1e-30f)));
+    const float r = r2 * rs;
     const float kk = S.hk[h], c2 = S.hc2[h];
     const float kr = kk * r;
     const float A = -kk * rx, B = -kk * ry, nkr = -kr;
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     if (MODE == MODE_REF) { pool_step = pool_pre; ss_absorb(pool_step, 1u); }  // STEP_DRAWS
 
     const long long hbase = (long long)h * P.human_stride;
+    bool overflow = false;  // a particle outside its reachable window (reported once at exit)
     for (int t = 1; t <= P.steps; ++t) {
         const int R = __ldg(&P.step_r[t - 1]);
         const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 cell_fast(x, y, P, ix, iy);
                 const unsigned lx = (unsigned)(ix - x0), ly = (unsigned)(iy - y0);
                 const bool inside = lx < (unsigned)ww && ly < (unsigned)wh;
-                if (valid && !inside && P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
+                overflow |= valid && !inside;
                 local = (valid && inside) ? (int)(ly * ww + lx) : -1;
             } else if (valid) {
                 float x = px[k], y = py[k];
@@ -478,11 +480,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 int ix, iy;
                 cell_ref(x, y, P, ix, iy);
                 const int lx = ix - x0, ly = iy - y0;
-                if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) {
-                    if (P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
-                } else {
-                    local = ly * ww + lx;
-                }
+                if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) overflow = true;
+                else local = ly * ww + lx;
             }
             // whole warp on one cell (early steps): one aggregated add; else per lane.
             // A word seen zero by its first add is appended to the touched list
@@ -518,6 +517,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             __syncthreads();
         }
     }
+    if (overflow && P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
     if (P.xy_out) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
