@@ -373,6 +373,27 @@ def run_ours(args):
         },
         "clocks": clk,
     }
+    if args.mode == "production" and not args.no_ref_mode:
+        # the same cycle in deterministic (reference-RNG, bit-exact arithmetic) mode
+        import dataclasses
+        eng_r = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec,
+                            dataclasses.replace(cfg, mode="reference"),
+                            human_ids=list(range(8 * rank, 8 * rank + len(scene.spaces))))
+        eng_r.prime(scene.warmup_track[0])
+        eng_r.stage(scene.warmup_track[1], buf=0)
+        eng_r.run_cycle(buf=0)
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        for _ in range(2):
+            eng_r.run_cycle(buf=0, with_h2d=False)
+        r1.record()
+        torch.cuda.synchronize()
+        rms = max_over_ranks(r0.elapsed_time(r1) / 2)
+        line["reference_rng_mode"] = {"ms_per_step": rms, "hz": 1000.0 / rms, "value": psteps / (rms * 1e-3),
+                                      "note": "same cycle with the reference's Philox4x64 streams regenerated "
+                                              "in-register and its float32 step op for op (bit-exact counts)"}
+        del eng_r
     if world == 1 and not args.no_cpu_baseline and rank == 0:
         line["cpu_baseline"] = cpu_sample(scene, t_steps=args.cpu_t, reps=3)
     if rank == 0:
@@ -392,6 +413,7 @@ def main():
     ap.add_argument("--mode", default="production", choices=["production", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--no-ref-mode", action="store_true")
     ap.add_argument("--cpu-t", type=int, default=25)
     ap.add_argument("--ref-t", type=int, default=10)
     args = ap.parse_args()
