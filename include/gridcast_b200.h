@@ -121,6 +121,13 @@ typedef struct {
     int32_t *d_hyp_out;        /* (n_humans, n) sampled hypothesis indices or NULL */
     float *d_xy_out;           /* (n_humans, n, 2) final positions or NULL */
     uint32_t *d_error;         /* device status word (GC_WINDOW_OVERFLOW bit) or NULL */
+    /* horizon chunking: run steps [t_begin, t_end) (1-based; 0, 0 = the whole horizon).
+     * A chunk starting after step 1 resumes the particles saved by the previous chunk in
+     * d_state_xy (float2 per particle) / d_state_hyp (uint8 hypothesis index); chunk
+     * starts must satisfy (t_begin - 1) % 4 == 0 (Philox block phase). */
+    int32_t t_begin, t_end;
+    float *d_state_xy;
+    uint8_t *d_state_hyp;
 } gc_predict_args;
 
 /* Occupancy epilogue (prediction.py:251-254, occupancy.py:139-154, :162-192,
@@ -146,6 +153,8 @@ typedef struct {
     float *d_union32;          /* (steps, H, W) zero-filled max-union (float32) or NULL */
     double *d_union64;         /* (steps, H, W) zero-filled max-union (float64) or NULL */
     int32_t time_union;        /* running max over t of the union (sim.py:503-504) */
+    int32_t tile_begin, tile_end; /* sub-range of d_tiles (0, 0 = all; tiles are ordered by step) */
+    int32_t t_begin, t_end;    /* steps the time union covers (0-based, [t_begin, t_end); 0, 0 = all) */
 } gc_epilogue_args;
 
 /* Observation update of every human's joint belief (belief.py:159-198), one warp per

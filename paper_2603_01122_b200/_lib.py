@@ -64,6 +64,7 @@ class PredictArgs(ctypes.Structure):
         ("d_step_r", P), ("d_step_off", P), ("human_stride", I64),
         ("max_win_cells", I32), ("_pad2", I32), ("d_counts", P),
         ("d_hyp_out", P), ("d_xy_out", P), ("d_error", P),
+        ("t_begin", I32), ("t_end", I32), ("d_state_xy", P), ("d_state_hyp", P),
     ]
 
 
@@ -76,6 +77,7 @@ class EpilogueArgs(ctypes.Structure):
         ("d_start_xy", P), ("d_step_r", P), ("d_step_off", P), ("human_stride", I64),
         ("d_tiles", P), ("d_counts", P),
         ("d_layers64", P), ("d_union32", P), ("d_union64", P), ("time_union", I32),
+        ("tile_begin", I32), ("tile_end", I32), ("t_begin", I32), ("t_end", I32),
     ]
 
 

@@ -20,8 +20,8 @@ NVCC_FLAGS = [
     # the reference-arithmetic kernels rely on IEEE float32 semantics: keep denormals,
     # IEEE division and sqrt; the explicit __f*_rn intrinsics forbid contraction there
     "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
-    "-shared", "-cudart", "shared",
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "shared"]
 
 
 def sources():
@@ -40,13 +40,24 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return OUT
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    objdir = os.path.join(HERE, "_lib", "obj")
+    os.makedirs(objdir, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", OUT + ".tmp", *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
+        objs = list(pool.map(compile_one, sources()))
+    subprocess.run([nvcc, *LINK_FLAGS, "-o", OUT + ".tmp", *objs], check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

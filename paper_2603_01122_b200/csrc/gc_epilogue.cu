@@ -124,11 +124,12 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
 
 // conservative time union: layer t <- max over t' <= t (np.maximum.accumulate, axis 0)
 template <typename Tv>
-__global__ void k_time_union(Tv *u, int steps, long long cells) {
+__global__ void k_time_union(Tv *u, int t0, int t1, long long cells) {
     const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cells) return;
-    Tv run = u[c];
-    for (int t = 1; t < steps; ++t) {
+    const int ts = t0 > 0 ? t0 - 1 : 0;  // seeded by the (final) layer before the range
+    Tv run = u[(long long)ts * cells + c];
+    for (int t = ts + 1; t < t1; ++t) {
         const long long o = (long long)t * cells + c;
         const Tv v = u[o];
         if (v < run) u[o] = run; else run = v;
@@ -234,7 +235,11 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
     if (smem > 48 * 1024)
         GC_CUDA(cudaFuncSetAttribute(k_epilogue<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaStream_t st = (cudaStream_t)stream;
-    dim3 grid(a->n_tiles, a->n_humans);
+    const int tb = a->tile_end > 0 ? a->tile_begin : 0;
+    const int te = a->tile_end > 0 ? a->tile_end : a->n_tiles;
+    GC_CHECK_ARG(tb >= 0 && tb < te && te <= a->n_tiles, "gc_grid_epilogue: bad tile range");
+    P.tiles = (const int4 *)a->d_tiles + tb;
+    dim3 grid(te - tb, a->n_humans);
     switch (a->radius) {
         case 0: k_epilogue<0><<<grid, ENT, smem, st>>>(P); break;
         case 1: k_epilogue<1><<<grid, ENT, smem, st>>>(P); break;
@@ -244,11 +249,12 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
     }
     count_launch();
     GC_TRY(cuda_check(cudaGetLastError(), "k_epilogue launch"));
-    if (a->time_union && a->steps > 1) {
+    const int t0 = a->t_end > 0 ? a->t_begin : 0, t1 = a->t_end > 0 ? a->t_end : a->steps;
+    if (a->time_union && a->steps > 1 && t1 - (t0 > 0 ? t0 - 1 : 0) > 1) {
         const long long cells = (long long)a->grid_w * a->grid_h;
         const int blocks = (int)((cells + 255) / 256);
-        if (a->d_union32) { k_time_union<float><<<blocks, 256, 0, st>>>(a->d_union32, a->steps, cells); count_launch(); }
-        if (a->d_union64) { k_time_union<double><<<blocks, 256, 0, st>>>(a->d_union64, a->steps, cells); count_launch(); }
+        if (a->d_union32) { k_time_union<float><<<blocks, 256, 0, st>>>(a->d_union32, t0, t1, cells); count_launch(); }
+        if (a->d_union64) { k_time_union<double><<<blocks, 256, 0, st>>>(a->d_union64, t0, t1, cells); count_launch(); }
         GC_TRY(cuda_check(cudaGetLastError(), "k_time_union launch"));
     }
     return GC_OK;

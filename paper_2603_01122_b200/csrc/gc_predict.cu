@@ -64,6 +64,9 @@ struct KParams {
     unsigned *counts;
     int smem_window;
     int act_off;  // byte offset of SmemAct in dynamic shared memory (REF/GEN modes)
+    int t_begin, t_end;          // steps [t_begin, t_end) of this launch (1-based)
+    float2 *state_xy;            // particle state between horizon chunks
+    unsigned char *state_hyp;
     int *hyp_out;
     float *xy_out;
     unsigned *error;
@@ -393,6 +396,14 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             const int p = pbase + k * NT + tid;
             px[k] = sx0; py[k] = sy0; ph[k] = 0; r1[k] = r2[k] = r3[k] = 0u;
             if (p >= P.n || k * NT + tid >= P.ppc) continue;
+            if (P.t_begin > 1) {  // resume a chunked horizon
+                const long long g = (long long)h * P.n + p;
+                const float2 st = P.state_xy[g];
+                px[k] = st.x; py[k] = st.y;
+                ph[k] = P.state_hyp[g];
+                S.phyp[k * NT + tid] = (unsigned char)ph[k];
+                continue;
+            }
             int hi;
             if (P.hyp_in) {
                 hi = __ldg(&P.hyp_in[(long long)h * P.n + p]);
@@ -418,7 +429,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
 
     const long long hbase = (long long)h * P.human_stride;
     bool overflow = false;  // a particle outside its reachable window (reported once at exit)
-    for (int t = 1; t <= P.steps; ++t) {
+    for (int t = P.t_begin; t < P.t_end; ++t) {
         const int R = __ldg(&P.step_r[t - 1]);
         const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
         const int y0 = max(0, cy - R), y1 = min(P.grid_h - 1, cy + R);
@@ -518,6 +529,17 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         }
     }
     if (overflow && P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
+    if (P.t_end <= P.steps && P.state_xy) {  // hand the particles to the next chunk
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int p = pbase + k * NT + tid;
+            if (p < P.n && k * NT + tid < P.ppc) {
+                const long long g = (long long)h * P.n + p;
+                P.state_xy[g] = make_float2(px[k], py[k]);
+                P.state_hyp[g] = (unsigned char)ph[k];
+            }
+        }
+    }
     if (P.xy_out) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -671,6 +693,13 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.step_r = a->d_step_r; P.step_off = (const long long *)a->d_step_off;
     P.human_stride = a->human_stride; P.counts = a->d_counts;
     P.hyp_out = a->d_hyp_out; P.xy_out = a->d_xy_out; P.error = a->d_error;
+    P.t_begin = a->t_begin > 0 ? a->t_begin : 1;
+    P.t_end = a->t_end > 0 ? a->t_end : a->steps + 1;
+    GC_CHECK_ARG(P.t_begin < P.t_end && P.t_end <= a->steps + 1, "gc_predict: bad step range");
+    GC_CHECK_ARG((P.t_begin - 1) % 4 == 0, "gc_predict: chunk starts must be 1 + a multiple of 4");
+    GC_CHECK_ARG((P.t_begin == 1 && P.t_end == a->steps + 1) || (a->d_state_xy && a->d_state_hyp),
+                 "gc_predict: a chunked horizon needs particle state buffers");
+    P.state_xy = (float2 *)a->d_state_xy; P.state_hyp = a->d_state_hyp;
 
     // particles per thread K and particles per CTA: enough CTAs to fill 148 SMs x 3
     // resident CTAs, then grow K to amortise the per-step window flush

@@ -178,7 +178,24 @@ class CycleEngine:
         self.cycle += 1
 
     # ---- the device cycle ---------------------------------------------------------------
-    def _launch(self, buf: int, with_update: bool, stream, events=None):
+    def chunk_bounds(self, chunks: int):
+        """1-based [t0, t1) step ranges; chunk starts are 1 + a multiple of 4 (Philox phase)."""
+        T = self.cfg.steps
+        size = max(4, -(-T // max(1, chunks)))
+        size = -(-size // 4) * 4
+        return [(t0, min(T + 1, t0 + size)) for t0 in range(1, T + 1, size)]
+
+    def _ensure_state(self):
+        if getattr(self, "state_xy", None) is None:
+            N = self.n_humans * self.cfg.n
+            self.state_xy = torch.empty(N * 2, dtype=torch.float32, device=self.dev)
+            self.state_hyp = torch.empty(N, dtype=torch.uint8, device=self.dev)
+
+    def _launch(self, buf: int, with_update: bool, stream, events=None, chunks: int = 1,
+                d2h=None, copy_stream=None):
+        """One cycle.  With chunks > 1 the horizon runs as several K2+K3 launches that hand
+        particle state over; if ``d2h`` (pinned host tensor shaped like the union) is given,
+        each chunk's layers are copied to it on ``copy_stream`` while later chunks compute."""
         cfg, geo, H = self.cfg, self.geo, self.n_humans
         sh = ctypes.c_void_p(stream.cuda_stream)
         if with_update:
@@ -188,6 +205,11 @@ class CycleEngine:
         self.counts.zero_()
         u = self.unions[buf]
         u.zero_()
+        if self.layers is not None:
+            self.layers.zero_()
+        bounds = self.chunk_bounds(chunks) if chunks > 1 else [(1, cfg.steps + 1)]
+        if len(bounds) > 1:
+            self._ensure_state()
         a = _lib.PredictArgs()
         a.n_humans, a.n, a.steps, a.rng_mode = H, cfg.n, cfg.steps, MODES[cfg.mode]
         a.grid_w, a.grid_h = self.spec.width, self.spec.height
@@ -203,11 +225,8 @@ class CycleEngine:
         a.d_step_r, a.d_step_off = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr()
         a.human_stride, a.max_win_cells = geo.human_stride, geo.max_win_cells
         a.d_counts, a.d_error = self.counts.data_ptr(), self.d_err.data_ptr()
-        if events is not None:
-            events[0].record(stream)
-        _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")
-        if events is not None:
-            events[1].record(stream)
+        if len(bounds) > 1:
+            a.d_state_xy, a.d_state_hyp = self.state_xy.data_ptr(), self.state_hyp.data_ptr()
         e = _lib.EpilogueArgs()
         e.n_humans, e.n, e.steps = H, cfg.n, cfg.steps
         e.grid_w, e.grid_h, e.radius = self.spec.width, self.spec.height, geo.radius
@@ -217,50 +236,73 @@ class CycleEngine:
         e.d_step_r, e.d_step_off, e.human_stride = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr(), geo.human_stride
         e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), self.counts.data_ptr()
         if self.layers is not None:
-            self.layers.zero_()
             e.d_layers64 = self.layers.data_ptr()
         if u.dtype == torch.float32:
             e.d_union32 = u.data_ptr()
         else:
             e.d_union64 = u.data_ptr()
         e.time_union = int(cfg.time_union)
-        _lib.check(_lib.lib().gc_grid_epilogue(ctypes.byref(e), sh), "gc_grid_epilogue")
-        if self.blocked is not None:
-            _lib.check(_lib.lib().gc_collision_field(
-                ctypes.c_void_p(u.data_ptr()), u.element_size(), cfg.steps, self.spec.width, self.spec.height,
-                self._disc.ctypes.data_as(ctypes.c_void_p), len(self._disc), float(cfg.collision_threshold),
-                None, ctypes.c_void_p(self.blocked[buf].data_ptr()), sh), "gc_collision_field")
+        for ci, (t0, t1) in enumerate(bounds):
+            a.t_begin, a.t_end = (t0, t1) if len(bounds) > 1 else (0, 0)
+            if events is not None and ci == 0:
+                events[0].record(stream)
+            _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")
+            if events is not None and ci == len(bounds) - 1:
+                events[1].record(stream)
+            if len(bounds) > 1:
+                e.tile_begin, e.tile_end = int(geo.tile_start[t0 - 1]), int(geo.tile_start[t1 - 1])
+                e.t_begin, e.t_end = t0 - 1, t1 - 1
+            _lib.check(_lib.lib().gc_grid_epilogue(ctypes.byref(e), sh), "gc_grid_epilogue")
+            if self.blocked is not None:
+                L0, L1 = t0 - 1, t1 - 1
+                _lib.check(_lib.lib().gc_collision_field(
+                    ctypes.c_void_p(u[L0:L1].data_ptr()), u.element_size(), L1 - L0, self.spec.width,
+                    self.spec.height, self._disc.ctypes.data_as(ctypes.c_void_p), len(self._disc),
+                    float(cfg.collision_threshold), None,
+                    ctypes.c_void_p(self.blocked[buf][L0:L1].data_ptr()), sh), "gc_collision_field")
+            if d2h is not None:
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                copy_stream.wait_event(ev)
+                with torch.cuda.stream(copy_stream):
+                    d2h[t0 - 1:t1 - 1].copy_(u[t0 - 1:t1 - 1], non_blocking=True)
         if events is not None:
             events[2].record(stream)
+        if d2h is not None:
+            stream.wait_stream(copy_stream)  # the cycle ends when its layers are on the host
 
     def run_cycle(self, buf: int = 0, with_h2d: bool = True, with_update: bool = True, stream=None,
-                  events=None):
+                  events=None, chunks: int = 1, d2h=None, copy_stream=None):
         """Eager (uncaptured) cycle on ``stream``; ``events`` = 3 CUDA events recorded
         before K2, after K2 and after K3 (kernel timing on the launching stream)."""
         s = stream or torch.cuda.current_stream()
         with torch.cuda.stream(s):
             if with_h2d:
                 self.d_in.copy_(self.h_ins[buf], non_blocking=True)
-            self._launch(buf, with_update, s, events)
+            self._launch(buf, with_update, s, events, chunks=chunks, d2h=d2h, copy_stream=copy_stream)
         return self.unions[buf]
 
-    def capture(self, buf: int = 0, with_h2d: bool = True, with_update: bool = True):
-        """Capture one cycle into a CUDA graph (replay with ``replay``)."""
-        key = (buf, with_h2d, with_update)
+    def capture(self, buf: int = 0, with_h2d: bool = True, with_update: bool = True, chunks: int = 1,
+                d2h=None):
+        """Capture one cycle into a CUDA graph (replay with ``replay``).  With ``d2h`` (a
+        pinned host tensor shaped like the union) the chunked D2H copies are part of the
+        graph, on a forked copy stream."""
+        key = (buf, with_h2d, with_update, chunks, None if d2h is None else d2h.data_ptr())
         if key in self.graphs:
-            return self.graphs[key]
+            return self.graphs[key][0]
         s = torch.cuda.Stream()
+        cp = torch.cuda.Stream() if d2h is not None else None
         s.wait_stream(torch.cuda.current_stream())
         # warm the library once outside capture (function attributes, lazy loading)
-        self.run_cycle(buf, with_h2d, with_update, stream=s)
+        self.run_cycle(buf, with_h2d, with_update, stream=s, chunks=chunks, d2h=d2h, copy_stream=cp)
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             if with_h2d:
                 self.d_in.copy_(self.h_ins[buf], non_blocking=True)
-            self._launch(buf, with_update, s)
-        self.graphs[key] = g
+            self._launch(buf, with_update, s, chunks=chunks, d2h=d2h, copy_stream=cp)
+        self.graphs[key] = (g, cp)  # keep the copy stream alive with the graph
         return g
 
     def posterior(self, i: int) -> np.ndarray:

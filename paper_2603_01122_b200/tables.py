@@ -241,11 +241,14 @@ class Geometry:
             return z
 
         tiles = []
+        self.tile_start = np.zeros(steps + 1, dtype=np.int64)  # first tile of step t (0-based)
         for ti in range(steps):
+            self.tile_start[ti] = len(tiles)
             nt = -(-(2 * int(r[ti]) + 1 + 2 * self.radius) // self.TILE)
             for ty in range(nt):
                 for tx in range(nt):
                     tiles.append((ti, tx, ty, 0))
+        self.tile_start[steps] = len(tiles)
         self.n_tiles = len(tiles)
         dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=device)
         self.d_step_r = dev(self.step_r)

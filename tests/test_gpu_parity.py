@@ -301,3 +301,29 @@ def test_mppi_production_noise_statistics():
     assert np.isfinite(cp).all() and dp.weight_entropy > 0
     np.testing.assert_allclose(cp, cr, atol=0.02)
     assert abs(dp.mean_cost - dr.mean_cost) < 0.01 * abs(dr.mean_cost)
+
+
+@pytest.mark.parametrize("mode", ["reference", "production"])
+def test_chunked_horizon_is_bit_identical(mode):
+    """Horizon chunking (K2 state hand-over + per-chunk K3/time union/blocked mask + chunked
+    D2H inside a CUDA graph) reproduces the single-launch cycle bit-for-bit."""
+    from paper_2603_01122_b200.engine import CycleEngine, EngineConfig
+    from paper_2603_01122_b200.scenario import make_scene
+    sc = make_scene("cfg1", cycles=2, humans=3)
+    cfg = EngineConfig(n=3000, steps=22, dt=0.1, smoothing_sigma=0.1, seed=9, mode=mode, time_union=True,
+                       robot_radius=0.25, collision_threshold=0.02)
+    out = {}
+    for chunks in (1, 3):
+        eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
+        eng.prime(sc.prev_xy)
+        eng.stage(sc.track[0], buf=0)
+        host = torch.empty(eng.unions[0].shape, dtype=eng.unions[0].dtype).pin_memory()
+        g = eng.capture(buf=0, chunks=chunks, d2h=host if chunks > 1 else None)
+        g.replay()
+        torch.cuda.synchronize()
+        eng.check_errors()
+        out[chunks] = (eng.unions[0].cpu().numpy(), eng.blocked[0].cpu().numpy(), host.numpy().copy())
+    np.testing.assert_array_equal(out[1][0], out[3][0])
+    np.testing.assert_array_equal(out[1][1], out[3][1])
+    np.testing.assert_array_equal(out[3][2], out[1][0])
+    assert out[1][0].max() > 0
