@@ -718,7 +718,10 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
     const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4 + (size_t)ppc * 4;
-    P.smem_window = win_bytes <= 64 * 1024 ? 1 : 0;
+    // shared-memory windows whenever they fit (robust to coherent particle clouds);
+    // GC_PREDICT_GLOBAL_HIST=1 forces direct global reductions (tuning knob)
+    static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();
+    P.smem_window = (win_bytes <= 64 * 1024 && !force_global) ? 1 : 0;
     P.act_off = P.smem_window ? (int)win_bytes : 0;
     const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;
     const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : 0);
