@@ -127,6 +127,32 @@ def predict_cases():
                         goals=[[17.0, 10.0], [10.0, 17.0], [3.0, 10.0], [10.0, 3.0]], q=gp,
                         grid=[200, 200, 0.1, [0.0, 0.0]], z0=[10.0, 10.0], n=65536, steps=30, dt=0.02,
                         sigma=0.0, seed=2, prefix=[2, 0], belief="posterior"),
+        # edge cases: one particle, one step, a 1x1 grid, a start outside the grid
+        "one_particle": dict(v=v, theta=th, betas=[1.0, 5.0], goals=[[2.0, 2.0]], q=gp,
+                             grid=[30, 30, 0.1, [0.0, 0.0]], z0=[1.5, 1.5], n=1, steps=7, dt=0.1,
+                             sigma=0.0, seed=123, prefix=[2, 9], belief="random"),
+        "one_step": dict(v=v, theta=th, betas=[0.5, 2.0], goals=[[3.0, 0.0], [0.0, 3.0]], q=gp,
+                         grid=[40, 40, 0.1, [0.0, 0.0]], z0=[2.0, 2.0], n=777, steps=1, dt=0.1,
+                         sigma=0.1, seed=5, prefix=[], belief="random"),
+        "grid1x1": dict(v=v, theta=th, betas=[1.0], goals=[[0.5, 0.5]], q=gp,
+                        grid=[1, 1, 0.1, [0.0, 0.0]], z0=[0.05, 0.05], n=300, steps=4, dt=0.1,
+                        sigma=0.0, seed=8, prefix=[], belief="uniform"),
+        "outside": dict(v=v, theta=th, betas=[0.3, 3.0], goals=[[1.0, 1.0], [-2.0, 0.5]], q=gp,
+                        grid=[25, 20, 0.1, [0.0, 0.0]], z0=[-0.7, 2.6], n=2000, steps=9, dt=0.1,
+                        sigma=0.1, seed=31, prefix=[2, 3], belief="random"),
+        # zero-probability hypotheses (log weight -inf) and the maximum sizes: 128
+        # hypotheses (8 betas x 16 goals) and 256 actions (8 speeds x 32 headings)
+        "zero_hyps": dict(v=v, theta=th, betas=list(np.geomspace(0.1, 10, 5)),
+                          goals=[[8.0, 5.0], [2.0, 5.0], [5.0, 8.0], [5.0, 2.0]], q=gp,
+                          grid=[100, 100, 0.1, [0.0, 0.0]], z0=[5.0, 5.0], n=4096, steps=6, dt=0.1,
+                          sigma=0.0, seed=77, prefix=[2, 1], belief="zeros"),
+        "max_sizes": dict(v=np.repeat(np.linspace(0, 1.4, 8), 32).tolist(),
+                          theta=[float((t + math.pi) % (2 * math.pi) - math.pi) for t in
+                                 np.tile(-np.pi + 2 * np.pi * np.arange(32) / 32, 8)],
+                          betas=list(np.geomspace(0.1, 10, 8)),
+                          goals=[[5.0 + 3.0 * math.cos(a), 5.0 + 3.0 * math.sin(a)] for a in np.linspace(0, 6.0, 16)],
+                          q=gp, grid=[100, 100, 0.1, [0.0, 0.0]], z0=[5.0, 5.0], n=2500, steps=5, dt=0.1,
+                          sigma=0.1, seed=4, prefix=[2, 2], belief="random"),
         # the reference's lattice instance (test_prediction.py:32-50)
         "lattice": dict(v=lat_v, theta=lat_th, betas=[0.5, 2.0], goals=[[8.5, 4.5], [0.5, 4.5]],
                         q=dict(family="goal_progress", tau=1.0, w_v=0.0, w_th=0.0, v_threshold=None),
@@ -142,6 +168,10 @@ def _belief_for(G, space, cs, kind, seed):
     r = np.random.default_rng(seed)
     if kind == "random":
         return G.JointBelief.from_probs(r.dirichlet(np.ones(space.size)))
+    if kind == "zeros":
+        p = r.dirichlet(np.ones(space.size))
+        p[::3] = 0.0
+        return G.JointBelief.from_probs(p)
     # posterior after 10 synthetic observations of a Boltzmann walker
     from gridcast.belief import update_belief
     b = G.init_belief(space)
