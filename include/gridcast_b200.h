@@ -128,6 +128,13 @@ typedef struct {
     int32_t t_begin, t_end;
     float *d_state_xy;
     uint8_t *d_state_hyp;
+    /* particle-block sharding of one human over GPUs: this call runs particles
+     * [p_offset, p_offset + n) of each human (every random stream is keyed by the global
+     * particle index, so the draws do not depend on the partition); the u32 count
+     * windows of all shards sum (ncclReduce/AllReduce sum) to the single-GPU counts and
+     * the epilogue then divides by the total particle count. */
+    int32_t p_offset;
+    int32_t _pad3;
 } gc_predict_args;
 
 /* Occupancy epilogue (prediction.py:251-254, occupancy.py:139-154, :162-192,

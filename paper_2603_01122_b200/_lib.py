@@ -65,6 +65,7 @@ class PredictArgs(ctypes.Structure):
         ("max_win_cells", I32), ("_pad2", I32), ("d_counts", P),
         ("d_hyp_out", P), ("d_xy_out", P), ("d_error", P),
         ("t_begin", I32), ("t_end", I32), ("d_state_xy", P), ("d_state_hyp", P),
+        ("p_offset", I32), ("_pad3", I32),
     ]
 
 

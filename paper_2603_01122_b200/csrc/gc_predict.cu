@@ -65,6 +65,7 @@ struct KParams {
     int smem_window;
     int act_off;  // byte offset of SmemAct in dynamic shared memory (REF/GEN modes)
     int t_begin, t_end;          // steps [t_begin, t_end) of this launch (1-based)
+    int p_offset;                // global index of this launch's first particle (particle sharding)
     float2 *state_xy;            // particle state between horizon chunks
     unsigned char *state_hyp;
     int *hyp_out;
@@ -410,9 +411,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             } else {
                 double u;
                 if (P.hyp_u) u = __ldg(&P.hyp_u[(long long)h * P.n + p]);
-                else if (MODE == MODE_REF) u = philox64_f64(hk0, hk1, (uint64_t)p);
+                else if (MODE == MODE_REF) u = philox64_f64(hk0, hk1, (uint64_t)(p + P.p_offset));
                 else {
-                    const U4 o = philox4x32(U4{(unsigned)p, 0xFFFFFFFFu, sid, 0x5EEDu}, sk_lo, sk_hi);
+                    const U4 o = philox4x32(U4{(unsigned)(p + P.p_offset), 0xFFFFFFFFu, sid, 0x5EEDu}, sk_lo, sk_hi);
                     u = ((double)(o.x >> 5) * 67108864.0 + (double)(o.y >> 6)) * (1.0 / 9007199254740992.0);
                 }
                 hi = 0;
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 // per step); the block counter is (particle, step/4, human stream, tag)
                 unsigned ua;
                 if (((t - 1) & 3) == 0) {
-                    const U4 o = philox4x32(U4{(unsigned)p, (unsigned)((t - 1) >> 2), sid, 0xA11CEu}, sk_lo, sk_hi);
+                    const U4 o = philox4x32(U4{(unsigned)(p + P.p_offset), (unsigned)((t - 1) >> 2), sid, 0xA11CEu}, sk_lo, sk_hi);
                     ua = o.x; r1[k] = o.y; r2[k] = o.z; r3[k] = o.w;
                 } else {
                     ua = r1[k]; r1[k] = r2[k]; r2[k] = r3[k];
@@ -474,7 +475,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 if (P.uniforms) {
                     u = __ldg(&P.uniforms[((long long)h * P.steps + (t - 1)) * P.n + p]);
                 } else {
-                    const int c = p >> 10;
+                    const int pg = p + P.p_offset;  // global particle index keys the stream
+                    const int c = pg >> 10;
                     if (c != key_chunk) {
                         SSPool s = pool_step;
                         ss_absorb(s, (unsigned)t);
@@ -482,7 +484,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                         ss_key(s, sk0, sk1);
                         key_chunk = c;
                     }
-                    u = philox64_f32(sk0, sk1, (uint64_t)(p & 1023));
+                    u = philox64_f32(sk0, sk1, (uint64_t)(pg & 1023));
                 }
                 const int a = ref_pick(S, A, x, y, ph[k], u);
                 x = __fadd_rn(x, A.adx[a]);
@@ -700,6 +702,8 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     GC_CHECK_ARG((P.t_begin == 1 && P.t_end == a->steps + 1) || (a->d_state_xy && a->d_state_hyp),
                  "gc_predict: a chunked horizon needs particle state buffers");
     P.state_xy = (float2 *)a->d_state_xy; P.state_hyp = a->d_state_hyp;
+    GC_CHECK_ARG(a->p_offset >= 0 && (long long)a->p_offset + a->n < (1ll << 31), "gc_predict: bad particle offset");
+    P.p_offset = a->p_offset;
 
     // particles per thread K and particles per CTA: enough CTAs to fill 148 SMs x 3
     // resident CTAs, then grow K to amortise the per-step window flush

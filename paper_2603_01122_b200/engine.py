@@ -55,14 +55,26 @@ class EngineConfig:
     # union thresholded into a (T, H, W) uint8 blocked mask each cycle; None = off
     robot_radius: Optional[float] = None
     collision_threshold: float = 0.1
+    # particle-block sharding of every human over GPUs: (shard index, shard count); this
+    # engine runs particles [i*n/k, (i+1)*n/k) of each human and its u32 counts must be
+    # summed over the shards (``counts_reduce``) before the epilogue divides by n
+    particle_shard: Optional[tuple] = None
 
 
 class CycleEngine:
     def __init__(self, control_set, q_model, spaces: Sequence, grid_spec, cfg: EngineConfig,
                  initial_log_weights: Optional[Sequence[np.ndarray]] = None,
-                 human_ids: Optional[Sequence[int]] = None):
+                 human_ids: Optional[Sequence[int]] = None, counts_reduce=None):
         self.dev = device()
         self.cfg = cfg
+        self.counts_reduce = counts_reduce
+        if cfg.particle_shard is not None:
+            i, k = cfg.particle_shard
+            if not (0 <= i < k) or cfg.n % k:
+                raise ValueError("particle_shard (i, k) needs 0 <= i < k and k | n")
+            self.n_local, self.p_offset = cfg.n // k, i * (cfg.n // k)
+        else:
+            self.n_local, self.p_offset = cfg.n, 0
         self.spec = grid_spec
         self.n_humans = len(spaces)
         self.control_set = control_set
@@ -187,7 +199,7 @@ class CycleEngine:
 
     def _ensure_state(self):
         if getattr(self, "state_xy", None) is None:
-            N = self.n_humans * self.cfg.n
+            N = self.n_humans * self.n_local
             self.state_xy = torch.empty(N * 2, dtype=torch.float32, device=self.dev)
             self.state_hyp = torch.empty(N, dtype=torch.uint8, device=self.dev)
 
@@ -208,10 +220,13 @@ class CycleEngine:
         if self.layers is not None:
             self.layers.zero_()
         bounds = self.chunk_bounds(chunks) if chunks > 1 else [(1, cfg.steps + 1)]
+        if self.counts_reduce is not None and len(bounds) > 1:
+            raise NotImplementedError("particle sharding runs the horizon in one chunk")
         if len(bounds) > 1:
             self._ensure_state()
         a = _lib.PredictArgs()
-        a.n_humans, a.n, a.steps, a.rng_mode = H, cfg.n, cfg.steps, MODES[cfg.mode]
+        a.n_humans, a.n, a.steps, a.rng_mode = H, self.n_local, cfg.steps, MODES[cfg.mode]
+        a.p_offset = self.p_offset
         a.grid_w, a.grid_h = self.spec.width, self.spec.height
         a.origin_x32 = float(np.float32(self.spec.origin[0]))
         a.origin_y32 = float(np.float32(self.spec.origin[1]))
@@ -249,6 +264,8 @@ class CycleEngine:
             _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")
             if events is not None and ci == len(bounds) - 1:
                 events[1].record(stream)
+            if self.counts_reduce is not None:
+                self.counts_reduce(self.counts)  # e.g. NCCL all-reduce(sum) over the shards
             if len(bounds) > 1:
                 e.tile_begin, e.tile_end = int(geo.tile_start[t0 - 1]), int(geo.tile_start[t1 - 1])
                 e.t_begin, e.t_end = t0 - 1, t1 - 1

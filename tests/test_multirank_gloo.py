@@ -88,3 +88,36 @@ def test_scene_shards_are_disjoint_and_sized():
     assert len(a.spaces) == len(b.spaces) == 8
     assert not np.allclose(a.starts, b.starts)
     assert a.n == 262144 and a.steps == 250
+
+
+def _shard_worker(rank, world, port, result_path):
+    """Each rank runs its block of one human's particles (streams keyed by the global
+    particle index) and the u32 counts are summed across ranks (the particle-sharded
+    path of engine.CycleEngine(particle_shard=...), counts_reduce = all_reduce(sum))."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, DT, model.QSpec())
+    s, lw, b, g = humans()[0]
+    n_total = 3000
+    hyp = OP.sample_hypotheses(lw, n_total, SEED, prefix=(2, 0))
+    lo, hi = rank * n_total // world, (rank + 1) * n_total // world
+    uni = np.stack([OP.step_uniforms(SEED, (2, 0), t, n_total)[lo:hi] for t in range(1, T + 1)])
+    part = OP.predict(s, lw, hi - lo, T, DT, 0.0, SEED, tb, b, g, GRID, prefix=(2, 0), uniforms=uni,
+                      hyp=hyp[lo:hi])["counts"]
+    c = torch.from_numpy(part.astype(np.int64))
+    dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        np.save(result_path, c.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_particle_sharded_counts_sum_to_single_process(tmp_path):
+    path = str(tmp_path / "counts.npy")
+    mp.spawn(_shard_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, DT, model.QSpec())
+    s, lw, b, g = humans()[0]
+    full = OP.predict(s, lw, 3000, T, DT, 0.0, SEED, tb, b, g, GRID, prefix=(2, 0))["counts"]
+    np.testing.assert_array_equal(np.load(path), full)
