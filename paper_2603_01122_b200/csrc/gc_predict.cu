@@ -107,13 +107,15 @@ struct SmemAct {
 };
 
 struct SmemTabs {
+    // production: (goal x, goal y, k log2e, c log2e) per hypothesis -- one LDS.128
+    float4 hp[MAXH];
+    // production: displacement of (a, b) and heading (cos, sin) -- one LDS.64 each
+    float2 fd[NAF * NBF];
+    float2 hcs[NBF];
     // hypotheses of this CTA's human
     double cdf[MAXH];
     float hb[MAXH], hgx[MAXH], hgy[MAXH];
-    float hk[MAXH], hc2[MAXH], hsumH[MAXH];
-    // MODE_FACT displacement of (a, b); heading cos/sin for per-lane (divergent) lookups
-    float fdx[NAF * NBF], fdy[NAF * NBF];
-    float hcos[NBF], hsin[NBF];
+    float hsumH[MAXH];
     int list_n[2];
     int n_hyp, m_keep, q_kind, n_speeds;
     float wth;
@@ -211,12 +213,13 @@ static const float hStdSin[NBF] = GC_STD_SIN;
 template <bool STDH, bool WTH>
 __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, float &x, float &y,
                                           int h, float u1) {
-    const float rx = x - S.hgx[h], ry = y - S.hgy[h];
+    const float4 hp = S.hp[h];
+    const float rx = x - hp.x, ry = y - hp.y;
     const float r2 = fmaf(rx, rx, ry * ry);
     float rs;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(r2, 1e-30f)));
     const float r = r2 * rs;
-    const float kk = S.hk[h], c2 = S.hc2[h];
+    const float kk = hp.z, c2 = hp.w;
     const float kr = kk * r;
     const float A = -kk * rx, B = -kk * ry, nkr = -kr;
     const int na = S.n_speeds;
@@ -273,7 +276,8 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     b = b < NBF - 1 ? b : NBF - 1;
     // speed within the heading from the residual of the same uniform: given b,
     // (t - lo) is uniform on [0, H_b sum_a G_a e_b^a) (up to the 2^-24 resolution of u1)
-    const float e = ex2_approx(fmaf(A, S.hcos[b], fmaf(B, S.hsin[b], nkr)));
+    const float2 cs = S.hcs[b];
+    const float e = ex2_approx(fmaf(A, cs.x, fmaf(B, cs.y, nkr)));
     float w1 = G1 * e, w2 = G2 * e * e;
     if (WTH) {
         const float hb = ex2_approx(-S.wth * S.hb[h] * P.hth2[b]);
@@ -285,9 +289,9 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     a = a < na - 1 ? a : na - 1;
     // stay (rr < Z0): every zero-speed action has displacement 0 -- branch-free select
     const bool stay = rr < Z0;
-    const float dx = S.fdx[a * NBF + b], dy = S.fdy[a * NBF + b];
-    x += stay ? 0.f : dx;
-    y += stay ? 0.f : dy;
+    const float2 d = S.fd[a * NBF + b];
+    x += stay ? 0.f : d.x;
+    y += stay ? 0.f : d.y;
 }
 
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
@@ -324,12 +328,11 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             A.ady[k] = __ldg(&T.dispy[j]);
         }
     } else {
-        for (int i = tid; i < NBF; i += NT) { S.hcos[i] = P.hcos[i]; S.hsin[i] = P.hsin[i]; }
+        for (int i = tid; i < NBF; i += NT) S.hcs[i] = make_float2(P.hcos[i], P.hsin[i]);
         for (int i = tid; i < NAF * NBF; i += NT) {
             const int a = i / NBF;
             const int j = a < T.n_speeds ? __ldg(&T.a_index[i]) : -1;
-            S.fdx[i] = j >= 0 ? __ldg(&T.dispx[j]) : 0.f;
-            S.fdy[i] = j >= 0 ? __ldg(&T.dispy[j]) : 0.f;
+            S.fd[i] = j >= 0 ? make_float2(__ldg(&T.dispx[j]), __ldg(&T.dispy[j])) : make_float2(0.f, 0.f);
         }
     }
     for (int i = tid; i < nh; i += NT) {
@@ -339,8 +342,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         S.hgy[i] = __ldg(&P.goal32[2 * (h0 + i) + 1]);
         if (MODE == MODE_FACT || MODE == MODE_FACTS) {
             const float L2E = 1.4426950408889634f;
-            S.hk[i] = 2.f * b * T.tau * T.dv * L2E;
-            S.hc2[i] = b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E;
+            S.hp[i] = make_float4(S.hgx[i], S.hgy[i], 2.f * b * T.tau * T.dv * L2E,
+                                  b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E);
             float sh = 0.f;
             for (int q = 0; q < T.n_headings; ++q)
                 sh += (T.w_th != 0.f) ? exp2f(-T.w_th * b * P.hth2[q] * L2E) : 1.f;
