@@ -6,8 +6,9 @@
 //   snap (agents.py:114-120): argmin_j |v_j - v| + |wrap(theta_j - theta)|, first index on
 //       ties (warp shuffle argmin over actions); > tol -> GC_SNAP_MISMATCH;
 //   observation_log_likelihood (belief.py:145-156) via policy_log_table (agents.py:299-323):
-//       per hypothesis (one lane each) the full-base utility q.table in float64, beta *,
-//       max shift over finite logits, log-sum-exp -> log pi(u_obs | z; beta, g);
+//       per hypothesis the full-base utility q.table in float64 with the warp's lanes over
+//       the actions (<= 8 per lane), beta *, shuffle max shift over finite logits, shuffle
+//       log-sum-exp -> log pi(u_obs | z; beta, g);
 //   posterior = prior + loglik, finite entries floored at -745, -inf kept (belief.py:194-197),
 //       normalised by a warp-shuffle logsumexp (scipy.special.logsumexp semantics).
 #include "gc_common.cuh"
@@ -83,48 +84,84 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
     }
     const int idx = bidx;
 
-    // ---- per-hypothesis log-likelihood (lanes over hypotheses) ----
+    // ---- per-hypothesis log-likelihood: lanes over actions, warp-shuffle max / sum ----
     const int h0 = P.hyp_off[h], nh = P.hyp_off[h + 1] - h0;
     double post[BMAXH / 32];
+#pragma unroll
+    for (int s = 0; s < BMAXH / 32; ++s) post[s] = NEG_INF;
     bool empty = false;
+    // per-action tables of this lane's actions, loaded once (<= 8 per lane)
+    double ax[8], ay[8], aat[8];
+    bool amask[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int j = lane + 32 * s;
+        const bool ok = j < P.m;
+        amask[s] = !ok || (P.masked && P.masked[j]);
+        ax[s] = ok ? P.sx[j] : 0.0;
+        ay[s] = ok ? P.sy[j] : 0.0;
+        aat[s] = ok ? (P.q_kind == GC_Q_DEFAULT ? P.pen[j] : P.at[j]) : 0.0;
+    }
+    // hypothesis parameters: lane i%32 loads hypothesis i, broadcast by shuffle
+    double hb_l[BMAXH / 32], hgx_l[BMAXH / 32], hgy_l[BMAXH / 32];
 #pragma unroll
     for (int s = 0; s < BMAXH / 32; ++s) {
         const int i = lane + 32 * s;
-        post[s] = NEG_INF;
-        if (i >= nh) continue;
-        const double beta = P.beta[h0 + i];
-        const double rx = zx - P.goal[2 * (h0 + i)], ry = zy - P.goal[2 * (h0 + i) + 1];
+        hb_l[s] = i < nh ? P.beta[h0 + i] : 0.0;
+        hgx_l[s] = i < nh ? P.goal[2 * (h0 + i)] : 0.0;
+        hgy_l[s] = i < nh ? P.goal[2 * (h0 + i) + 1] : 0.0;
+    }
+    for (int i = 0; i < nh; ++i) {
+        double b_s = 0.0, gx_s = 0.0, gy_s = 0.0;
+#pragma unroll
+        for (int s = 0; s < BMAXH / 32; ++s)
+            if (s == (i >> 5)) { b_s = hb_l[s]; gx_s = hgx_l[s]; gy_s = hgy_l[s]; }
+        const double beta = __shfl_sync(0xffffffffu, b_s, i & 31);
+        const double rx = zx - __shfl_sync(0xffffffffu, gx_s, i & 31);
+        const double ry = zy - __shfl_sync(0xffffffffu, gy_s, i & 31);
         const double d2 = __dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry));
-        auto logit = [&](int j) -> double {
-            if (P.masked && P.masked[j]) return NEG_INF;
+        auto logit_s = [&](int s, int j) -> double {
+            if (amask[s]) return NEG_INF;
             double q;
             if (P.q_kind == GC_Q_TABLE) {
                 q = P.qtable[(long long)(h0 + i) * P.m + j];
             } else if (P.q_kind == GC_Q_DEFAULT) {
-                q = __dsub_rn(-d2, P.pen[j]);
+                q = __dsub_rn(-d2, aat[s]);
             } else {
-                q = __dmul_rn(__fma_rn(ry, P.sy[j], __dmul_rn(rx, P.sx[j])), -2.0);
-                q = __dsub_rn(q, P.at[j]);
+                q = __dmul_rn(__fma_rn(ry, ay[s], __dmul_rn(rx, ax[s])), -2.0);
+                q = __dsub_rn(q, aat[s]);
                 q = __dsub_rn(q, d2);
             }
             return __dmul_rn(beta, q);
         };
+        double Lj[8];  // m <= 256 actions: 8 per lane
         double mx = NEG_INF;
-        for (int j = 0; j < P.m; ++j) {
-            const double L = logit(j);
-            if (L > mx) mx = L;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            const int j = lane + 32 * s;
+            Lj[s] = logit_s(s, j);
+            mx = fmax(mx, Lj[s]);
         }
-        if (!(mx > NEG_INF)) { empty = true; continue; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (!(mx > NEG_INF)) { empty = true; break; }
         double ssum = 0.0;
-        for (int j = 0; j < P.m; ++j) {
-            const double L = logit(j);
-            if (L > NEG_INF) ssum += exp(L - mx);
-        }
-        const double Li = logit(idx);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) if (Lj[s] > NEG_INF) ssum += exp(Lj[s] - mx);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+        // the observed action's logit lives in lane idx % 32, slot idx / 32
+        double Lmine = NEG_INF;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) if (s == (idx >> 5)) Lmine = Lj[s];
+        const double Li = __shfl_sync(0xffffffffu, Lmine, idx & 31);
         const double ll = (Li > NEG_INF) ? (Li - mx) - log(ssum) : NEG_INF;
-        const double pr = P.prior[h0 + i];
-        if (pr == NEG_INF) post[s] = NEG_INF;
-        else post[s] = fmax(pr + ll, -745.0);  // LOG_WEIGHT_FLOOR (belief.py:32)
+        if (lane == (i & 31)) {
+            const double pr = P.prior[h0 + i];
+            const double v = (pr == NEG_INF) ? NEG_INF : fmax(pr + ll, -745.0);  // LOG_WEIGHT_FLOOR
+#pragma unroll
+            for (int s = 0; s < BMAXH / 32; ++s) if (s == (i >> 5)) post[s] = v;
+        }
     }
     if (__any_sync(0xffffffffu, empty)) {
         if (lane == 0) P.status[h] = GC_EMPTY_CONTROL_SET;
@@ -157,7 +194,7 @@ using namespace gc;
 
 extern "C" gc_status gc_belief_update(const gc_belief_args *a, void *stream) {
     GC_CHECK_ARG(a != nullptr, "gc_belief_update: null args");
-    GC_CHECK_ARG(a->n_humans >= 1 && a->m >= 1, "gc_belief_update: bad sizes");
+    GC_CHECK_ARG(a->n_humans >= 1 && a->m >= 1 && a->m <= 256, "gc_belief_update: 1..256 actions");
     GC_CHECK_ARG(a->d_v && a->d_theta && a->d_hyp_off && a->d_beta && a->d_goal && a->d_obs &&
                  a->d_fallback_theta && a->d_prior && a->d_post && a->d_status,
                  "gc_belief_update: missing device buffers");
