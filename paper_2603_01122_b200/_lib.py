@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgridcast_b200.so")
+# GC_LIB_PATH: load another build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("GC_LIB_PATH") or os.path.join(_HERE, "_lib", "libgridcast_b200.so")
 
 GC_OK = 0
 GC_BAD_ARG = 1

@@ -31,6 +31,8 @@ constexpr int MAXH = 128;      // max hypotheses per human
 constexpr int NBF = 24;        // headings of the factorised sampler (ControlSet.grid default)
 constexpr int NAF = 4;         // max speeds of the factorised sampler
 
+constexpr unsigned PHK0 = 0xA4093822u, PHK1 = 0x299F31D0u;  // production Philox key
+
 enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2, MODE_FACTS = 3 };  // FACTS: standard headings
 
 struct KTable {
@@ -84,15 +86,13 @@ __device__ __forceinline__ void cell_ref(float x, float y, const KParams &P, int
 }
 
 // production cell index: floor((x - ox) / res) without the XU pipe (FRND/F2I would
-// compete with the exponentials): clamp to [-1, W], round with the 1.5*2^23 magic
-// constant, correct round-up to floor, clamp to the grid.  Differs from the IEEE
-// division form only for positions within an ulp of a cell edge.
+// compete with the exponentials): clamp to [0, n-1], then one round-toward-minus-infinity
+// add of 2^23 puts floor(f) in the low mantissa bits.  Differs from the IEEE division
+// form only for positions within an ulp of a cell edge.
 __device__ __forceinline__ int floor_clamp(float f, float nm1) {
-    // clamp(floor(f), 0, n-1) == floor(clamp(f, 0, n-1)) for any f
+    // clamp(floor(f), 0, n-1) == floor(clamp(f, 0, n-1)) for any f; NaN -> 0
     f = fminf(fmaxf(f, 0.f), nm1);
-    const float r = f + 12582912.f;
-    const float fr = r - 12582912.f;
-    return (__float_as_int(r) - 0x4B400000) - ((fr > f) ? 1 : 0);
+    return __float_as_int(__fadd_rd(f, 8388608.f)) - 0x4B000000;
 }
 
 __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, int &ix, int &iy) {
@@ -287,11 +287,12 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     const float res = t - lo;
     int a = 1 + ((w1 <= res) ? 1 : 0) + ((w1 + w2 <= res) ? 1 : 0);
     a = a < na - 1 ? a : na - 1;
-    // stay (rr < Z0): every zero-speed action has displacement 0 -- branch-free select
-    const bool stay = rr < Z0;
+    // stay (rr < Z0): every zero-speed action has displacement 0 -- row a = 0 of fd is
+    // (0, 0) for every heading, so staying is just a = 0
+    a = (rr < Z0) ? 0 : a;
     const float2 d = S.fd[a * NBF + b];
-    x += stay ? 0.f : d.x;
-    y += stay ? 0.f : d.y;
+    x += d.x;
+    y += d.y;
 }
 
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         for (int i = tid; i < NBF; i += NT) S.hcs[i] = make_float2(P.hcos[i], P.hsin[i]);
         for (int i = tid; i < NAF * NBF; i += NT) {
             const int a = i / NBF;
-            const int j = a < T.n_speeds ? __ldg(&T.a_index[i]) : -1;
+            const int j = (a > 0 && a < T.n_speeds) ? __ldg(&T.a_index[i]) : -1;  // a = 0: stay
             S.fd[i] = j >= 0 ? make_float2(__ldg(&T.dispx[j]), __ldg(&T.dispy[j])) : make_float2(0.f, 0.f);
         }
     }
@@ -377,6 +378,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     const unsigned long long seed = __ldg(&P.seed[h]);
     const unsigned sk_lo = (unsigned)seed, sk_hi = (unsigned)(seed >> 32);
     const unsigned sid = P.stream_id ? __ldg(&P.stream_id[h]) : (unsigned)h;
+    // production streams: Philox4x32-10 under a fixed key; (seed, human stream) live in
+    // the counter's upper words, so the key schedule folds into immediates
+    const unsigned sc2 = sk_lo ^ (sid * 0x85EBCA77u);
     SSPool pool_pre;
     if (MODE == MODE_REF) {
         pool_pre = ss_pool_init(seed);
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 if (P.hyp_u) u = __ldg(&P.hyp_u[(long long)h * P.n + p]);
                 else if (MODE == MODE_REF) u = philox64_f64(hk0, hk1, (uint64_t)(p + P.p_offset));
                 else {
-                    const U4 o = philox4x32(U4{(unsigned)(p + P.p_offset), 0xFFFFFFFFu, sid, 0x5EEDu}, sk_lo, sk_hi);
+                    const U4 o = philox4x32(U4{(unsigned)(p + P.p_offset), 0xFFFFFFFFu, sc2, sk_hi ^ 0x5EEDu}, PHK0, PHK1);
                     u = ((double)(o.x >> 5) * 67108864.0 + (double)(o.y >> 6)) * (1.0 / 9007199254740992.0);
                 }
                 hi = 0;
@@ -453,7 +457,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 // per step); the block counter is (particle, step/4, human stream, tag)
                 unsigned ua;
                 if (((t - 1) & 3) == 0) {
-                    const U4 o = philox4x32(U4{(unsigned)(p + P.p_offset), (unsigned)((t - 1) >> 2), sid, 0xA11CEu}, sk_lo, sk_hi);
+                    const U4 o = philox4x32(U4{(unsigned)(p + P.p_offset), (unsigned)((t - 1) >> 2), sc2, sk_hi ^ 0xA11CEu}, PHK0, PHK1);
                     ua = o.x; r1[k] = o.y; r2[k] = o.z; r3[k] = o.w;
                 } else {
                     ua = r1[k]; r1[k] = r2[k]; r2[k] = r3[k];

@@ -21,17 +21,23 @@ def main():
     ap.add_argument("--humans", type=int, default=8)
     ap.add_argument("--n", type=int, default=262144)
     ap.add_argument("--cycles", type=int, default=2)
+    ap.add_argument("--summary", action="store_true", help="one line: mean K2 ms over cycles 1..")
     a = ap.parse_args()
     sc = make_scene("cfg3", cycles=4, humans=a.humans)
     eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec,
                       EngineConfig(n=a.n, steps=a.steps, dt=sc.dt, mode=a.mode))
     eng.prime(sc.warmup_track[0])
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    k2 = []
     for k in range(a.cycles):
         eng.stage(sc.warmup_track[1 + k], buf=0)
         eng.run_cycle(buf=0, events=ev)
         torch.cuda.synchronize()
-        print(f"cycle {k}: k_predict {ev[0].elapsed_time(ev[1]):.3f} ms, epilogue {ev[1].elapsed_time(ev[2]):.3f} ms")
+        k2.append(ev[0].elapsed_time(ev[1]))
+        if not a.summary:
+            print(f"cycle {k}: k_predict {k2[-1]:.3f} ms, epilogue {ev[1].elapsed_time(ev[2]):.3f} ms")
+    if a.summary:
+        print(f"k_predict mean {sum(k2[1:]) / max(1, len(k2) - 1):.4f} ms  " + " ".join(f"{v:.3f}" for v in k2[1:]))
     eng.check_errors()
 
 
