@@ -305,6 +305,9 @@ template <int MODE, int K, bool WTH>
 __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ SmemTabs S;
+    // the factorised sampler keeps particles in grid units u = (x - origin) / res: the
+    // cell is floor(u), and the utility is rescaled (k -> k res) so the weights are unchanged
+    constexpr bool GRIDU = MODE == MODE_FACT || MODE == MODE_FACTS;
     const int tid = threadIdx.x, lane = tid & 31;
     const int h = blockIdx.x / P.ctas_per_human;
     const int blk = blockIdx.x - h * P.ctas_per_human;
@@ -333,7 +336,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         for (int i = tid; i < NAF * NBF; i += NT) {
             const int a = i / NBF;
             const int j = (a > 0 && a < T.n_speeds) ? __ldg(&T.a_index[i]) : -1;  // a = 0: stay
-            S.fd[i] = j >= 0 ? make_float2(__ldg(&T.dispx[j]), __ldg(&T.dispy[j])) : make_float2(0.f, 0.f);
+            S.fd[i] = j >= 0 ? make_float2(__fdiv_rn(__ldg(&T.dispx[j]), P.res), __fdiv_rn(__ldg(&T.dispy[j]), P.res))
+                             : make_float2(0.f, 0.f);
         }
     }
     for (int i = tid; i < nh; i += NT) {
@@ -343,7 +347,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         S.hgy[i] = __ldg(&P.goal32[2 * (h0 + i) + 1]);
         if (MODE == MODE_FACT || MODE == MODE_FACTS) {
             const float L2E = 1.4426950408889634f;
-            S.hp[i] = make_float4(S.hgx[i], S.hgy[i], 2.f * b * T.tau * T.dv * L2E,
+            S.hp[i] = make_float4(__fdiv_rn(S.hgx[i] - P.ox, P.res), __fdiv_rn(S.hgy[i] - P.oy, P.res),
+                                  2.f * b * T.tau * T.dv * L2E * P.res,
                                   b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E);
             float sh = 0.f;
             for (int q = 0; q < T.n_headings; ++q)
@@ -402,7 +407,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
-            px[k] = sx0; py[k] = sy0; ph[k] = 0; r1[k] = r2[k] = r3[k] = 0u;
+            px[k] = GRIDU ? __fdiv_rn(sx0 - P.ox, P.res) : sx0;
+            py[k] = GRIDU ? __fdiv_rn(sy0 - P.oy, P.res) : sy0;
+            ph[k] = 0; r1[k] = r2[k] = r3[k] = 0u;
             if (p >= P.n || k * NT + tid >= P.ppc) continue;
             if (P.t_begin > 1) {  // resume a chunked horizon
                 const long long g = (long long)h * P.n + p;
@@ -471,7 +478,12 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 }
                 px[k] = x; py[k] = y;
                 int ix, iy;
-                cell_fast(x, y, P, ix, iy);
+                if (GRIDU) {
+                    ix = floor_clamp(x, (float)(P.grid_w - 1));
+                    iy = floor_clamp(y, (float)(P.grid_h - 1));
+                } else {
+                    cell_fast(x, y, P, ix, iy);
+                }
                 const unsigned lx = (unsigned)(ix - x0), ly = (unsigned)(iy - y0);
                 const bool inside = lx < (unsigned)ww && ly < (unsigned)wh;
                 overflow |= valid && !inside;
@@ -554,8 +566,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
             if (p < P.n && k * NT + tid < P.ppc) {
-                P.xy_out[((long long)h * P.n + p) * 2] = px[k];
-                P.xy_out[((long long)h * P.n + p) * 2 + 1] = py[k];
+                P.xy_out[((long long)h * P.n + p) * 2] = GRIDU ? fmaf(px[k], P.res, P.ox) : px[k];
+                P.xy_out[((long long)h * P.n + p) * 2 + 1] = GRIDU ? fmaf(py[k], P.res, P.oy) : py[k];
             }
         }
     }
