@@ -46,6 +46,7 @@ struct KParams {
     int n_humans, n, steps, ppc, ctas_per_human, rng_mode;
     int grid_w, grid_h;
     float ox, oy, res, inv_res;
+    float wm1f, hm1f;            // (float)(grid_w - 1), (float)(grid_h - 1)
     const float *start_xy;
     const int *hyp_off;
     const float *beta32, *goal32;
@@ -96,8 +97,8 @@ __device__ __forceinline__ int floor_clamp(float f, float nm1) {
 }
 
 __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, int &ix, int &iy) {
-    ix = floor_clamp((x - P.ox) * P.inv_res, (float)(P.grid_w - 1));
-    iy = floor_clamp((y - P.oy) * P.inv_res, (float)(P.grid_h - 1));
+    ix = floor_clamp((x - P.ox) * P.inv_res, P.wm1f);
+    iy = floor_clamp((y - P.oy) * P.inv_res, P.hm1f);
 }
 
 // MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
@@ -297,10 +298,6 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
 
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
 // particles, so a per-CTA cell count cannot overflow its half-word)
-__device__ __forceinline__ void win_add(unsigned *win, int local, unsigned cnt) {
-    atomicAdd(&win[local >> 1], cnt << ((local & 1) << 4));
-}
-
 template <int MODE, int K, bool WTH>
 __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
@@ -479,8 +476,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 px[k] = x; py[k] = y;
                 int ix, iy;
                 if (GRIDU) {
-                    ix = floor_clamp(x, (float)(P.grid_w - 1));
-                    iy = floor_clamp(y, (float)(P.grid_h - 1));
+                    ix = floor_clamp(x, P.wm1f);
+                    iy = floor_clamp(y, P.hm1f);
                 } else {
                     cell_fast(x, y, P, ix, iy);
                 }
@@ -520,7 +517,12 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             // (warp-aggregated: one shared atomic per warp).
             if (P.smem_window) {
                 bool first = false;
-                if (local >= 0) first = atomicAdd(&win[local >> 1], 1u << ((local & 1) << 4)) == 0u;
+                if (local >= 0) {
+                    // u16 counter `local`: byte offset 2 local, in word (2 local) & ~3
+                    const unsigned off = 2u * (unsigned)local;
+                    first = atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
+                                      (off & 2u) ? 0x10000u : 1u) == 0u;
+                }
                 const unsigned m = __ballot_sync(0xffffffffu, first);
                 if (m) {
                     const int leader = __ffs(m) - 1;
@@ -675,6 +677,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.n_humans = a->n_humans; P.n = a->n; P.steps = a->steps; P.rng_mode = a->rng_mode;
     P.grid_w = a->grid_w; P.grid_h = a->grid_h;
     P.ox = a->origin_x32; P.oy = a->origin_y32; P.res = a->res32; P.inv_res = 1.0f / a->res32;
+    P.wm1f = (float)(a->grid_w - 1); P.hm1f = (float)(a->grid_h - 1);
     P.start_xy = a->d_start_xy; P.hyp_off = a->d_hyp_off; P.beta32 = a->d_beta32; P.goal32 = a->d_goal32;
     P.cdf = a->d_cdf; P.log_w = a->d_log_w;
     P.seed = (const unsigned long long *)a->d_seed; P.prefix = a->d_prefix; P.prefix_len = a->d_prefix_len;
