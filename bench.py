@@ -195,7 +195,7 @@ def run_ours(args):
     K, W = args.steps, args.warmup
     scene = make_scene(args.config, cycles=W + K + 4, humans=8, human_offset=8 * rank)
     cfg = EngineConfig(n=scene.n, steps=scene.steps, dt=scene.dt, smoothing_sigma=0.1, seed=0,
-                       mode=args.mode, time_union=False)
+                       mode=args.mode, time_union=False, chunk_taper=args.chunk_taper)
     eng = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec, cfg,
                       human_ids=list(range(8 * rank, 8 * rank + len(scene.spaces))))
     # posterior after 10 observations (also warms every kernel)
@@ -298,7 +298,8 @@ def run_ours(args):
         evs = e2e_loop(K, W)
         e_end.record(stream)
         barrier()
-        e2e_note = (f"per cycle: pinned obs H2D + update + predict in {args.chunks} horizon chunks, each "
+        e2e_note = (f"per cycle: pinned obs H2D + update + predict in {args.chunks} horizon chunks "
+                    f"(sizes {[b - a for a, b in eng.chunk_bounds(args.chunks)]}), each "
                     f"chunk's f32 union layers D2H on a copy stream while the next computes; cycles strictly "
                     f"sequential (latency = cycle time), one CUDA graph")
     else:
@@ -450,7 +451,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
     ap.add_argument("--no-ref-mode", action="store_true")
-    ap.add_argument("--chunks", type=int, default=8, help="horizon chunks of the e2e cycle (D2H overlap)")
+    ap.add_argument("--chunks", type=int, default=6, help="horizon chunks of the e2e cycle (D2H overlap)")
+    ap.add_argument("--chunk-taper", type=float, default=0.5, help="chunk size ratio (1.0 = uniform chunks)")
     ap.add_argument("--cpu-t", type=int, default=25)
     ap.add_argument("--ref-t", type=int, default=10)
     args = ap.parse_args()

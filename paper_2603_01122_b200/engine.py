@@ -59,6 +59,9 @@ class EngineConfig:
     # engine runs particles [i*n/k, (i+1)*n/k) of each human and its u32 counts must be
     # summed over the shards (``counts_reduce``) before the epilogue divides by n
     particle_shard: Optional[tuple] = None
+    # horizon chunking (chunks > 1): chunk c spans ~ chunk_taper^c of the horizon, so the
+    # last chunks -- whose D2H cannot overlap later compute -- are short; 1.0 = uniform
+    chunk_taper: float = 0.5
 
 
 class CycleEngine:
@@ -191,11 +194,19 @@ class CycleEngine:
 
     # ---- the device cycle ---------------------------------------------------------------
     def chunk_bounds(self, chunks: int):
-        """1-based [t0, t1) step ranges; chunk starts are 1 + a multiple of 4 (Philox phase)."""
+        """1-based [t0, t1) step ranges of ``chunks`` horizon chunks; every chunk start is
+        1 + a multiple of 4 (Philox phase of the production streams).  Chunk sizes shrink
+        geometrically (``cfg.chunk_taper``) toward the end of the horizon."""
         T = self.cfg.steps
-        size = max(4, -(-T // max(1, chunks)))
-        size = -(-size // 4) * 4
-        return [(t0, min(T + 1, t0 + size)) for t0 in range(1, T + 1, size)]
+        chunks = max(1, min(chunks, (T + 3) // 4))
+        w = [self.cfg.chunk_taper ** c for c in range(chunks)]
+        starts, acc = [1], 0.0
+        for c in range(chunks - 1):
+            acc += w[c]
+            s = 1 + 4 * int(round(T * acc / sum(w) / 4))
+            if starts[-1] < s <= T:
+                starts.append(s)
+        return [(t0, t1) for t0, t1 in zip(starts, starts[1:] + [T + 1])]
 
     def _ensure_state(self):
         if getattr(self, "state_xy", None) is None:
