@@ -1,6 +1,7 @@
 #!/bin/bash
 # ncu evidence for profiles/: launch list of one bench run + full captures of K2/K3/K1 and
-# of the f-row kernels (collision field, MPPI, exact enumeration).
+# of the f-row kernels (collision field, MPPI, exact enumeration).  Then, here:
+#   python tools/write_profiles.py --tag rNN   (profiles/ + ncu_summary.json)
 set -x
 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_bench.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
@@ -8,10 +9,12 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python tools/profile_predict.py --steps 250 --cycles 3 > gpurun_out/plain_prof.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_predict|k_epilogue|k_belief" -s 3 -c 3 \
     -o gpurun_out/cycle_cfg3 python tools/profile_predict.py --steps 250 --cycles 3 > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
+    -o gpurun_out/k2_cfg3 python tools/profile_predict.py --steps 250 --cycles 2 > gpurun_out/ncu_k2.log 2>&1
 python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/plain_ref.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
     -o gpurun_out/k2_refmode python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/ncu_ref.log 2>&1
 python tools/profile_extras.py > gpurun_out/plain_extras.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_collision|k_mppi|k_exact" -s 2 -c 6 \
     -o gpurun_out/extras python tools/profile_extras.py > gpurun_out/ncu_extras.log 2>&1
-tail -n 2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_ref.log gpurun_out/ncu_extras.log
+tail -n 2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_k2.log gpurun_out/ncu_ref.log gpurun_out/ncu_extras.log
