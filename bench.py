@@ -38,6 +38,7 @@ METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "particle-steps/s"
 # reference-algorithm work per particle-step: 9m+10 FP32 ops, m = 96
 REF_OPS_PER_PSTEP = 9 * 96 + 10
+LAT_CYCLES = 1000  # p50/p99 latencies are taken over at least this many cycles
 
 
 def peaks():
@@ -255,6 +256,18 @@ def run_ours(args):
     ms = t_start.elapsed_time(t_end) / K
     ms = max_over_ranks(ms)
     per_cycle = [a.elapsed_time(b) for a, b in cyc_ev]
+    # latency percentiles over >= LAT_CYCLES cycles: extra untimed-for-value replays
+    n_lat = max(LAT_CYCLES, K)
+    extra = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_lat - K)]
+    with torch.cuda.stream(stream):
+        for a_, b_ in extra:
+            a_.record(stream)
+            g.replay()
+            if fused:
+                fused_reduce(eng.unions[0], dst=0)
+            b_.record(stream)
+    barrier()
+    per_cycle += [a.elapsed_time(b) for a, b in extra]
     p99 = max_over_ranks(float(np.percentile(per_cycle, 99)))
     p50 = max_over_ranks(float(np.percentile(per_cycle, 50)))
     # graph replays do not pass through the C ABI launch counter: 3 kernels per cycle
@@ -297,6 +310,8 @@ def run_ours(args):
         e_start.record(stream)
         evs = e2e_loop(K, W)
         e_end.record(stream)
+        barrier()
+        evs += e2e_loop(n_lat - K, W + K)  # latency samples only
         barrier()
         e2e_note = (f"per cycle: pinned obs H2D + update + predict in {args.chunks} horizon chunks "
                     f"(sizes {[b - a for a, b in eng.chunk_bounds(args.chunks)]}), each "
@@ -343,6 +358,9 @@ def run_ours(args):
         evs = e2e_loop(K, W)
         stream.wait_stream(copy)
         e_end.record(stream)
+        barrier()
+        evs += e2e_loop(n_lat - K, W + K)  # latency samples only
+        stream.wait_stream(copy)
         barrier()
         e2e_note = "pinned obs H2D + NCCL fused union + rank-0 f32 D2H each cycle, D2H overlapped with the next cycle"
     clocks.__exit__(None, None, None)
@@ -401,7 +419,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "hz": 1000.0 / ms, "p50_ms": p50, "p99_ms": p99,
+        "hz": 1000.0 / ms, "p50_ms": p50, "p99_ms": p99, "latency_cycles": n_lat,
         "config": {
             "workload": (f"{args.config}: {len(scene.spaces)} humans/GPU x {scene.n} particles x {scene.steps} "
                          f"steps dt {scene.dt}, |H|=20, |U|=96, 400x400 @0.1 m union, sigma 0.1 m, "
