@@ -207,6 +207,28 @@ typedef struct {
     double *d_layers;
 } gc_exact_args;
 
+/* predict_naive (prediction.py:258-300): the reference's serial float64 per-particle loop,
+ * one thread per particle.  Positions start at (start_x, start_y) in float64; per step
+ * the particle's q.table row over the kept actions (GC_Q_GOAL_PROGRESS_FULL or
+ * GC_Q_DEFAULT; float64 tables as q.table evaluates them, agents.py:222-224), beta x,
+ * max shift, exp, sequential cumsum, #(cdf < u * cdf[-1]) with u the float64 draw of
+ * rng.stream(seed, *prefix, 1, t, p >> 10) (rng.py:27-39); cells in float64
+ * (occupancy.py:43-51).  d_counts = (steps, H, W) uint32, zeroed by the caller. */
+typedef struct {
+    int32_t n, steps, n_hyp, m_keep;
+    int32_t q_kind, grid_w, grid_h, prefix_len;
+    uint64_t seed;
+    uint32_t prefix[4];
+    double start_x, start_y, origin_x, origin_y, res;
+    const int32_t *d_hyp;                       /* (n) hypothesis of each particle */
+    const double *d_beta, *d_goal;              /* (|H|), (|H|, 2) */
+    const int32_t *d_keep;                      /* (m_keep) kept action indices, ascending */
+    const double *d_sx, *d_sy, *d_at, *d_pen;   /* (m) float64 utility tables */
+    const double *d_dispx, *d_dispy;            /* (m) float64 displacements */
+    uint32_t *d_counts;                         /* (steps, H, W) */
+    double *d_xy_out;                           /* (n, 2) final positions or NULL */
+} gc_naive_args;
+
 /* MPPI control update (planners/mppi.py:149-243) against a device blocked mask. */
 typedef struct {
     int32_t n_rollouts, horizon;
@@ -230,6 +252,7 @@ typedef struct {
 gc_status gc_predict(const gc_predict_args *args, void *stream);
 gc_status gc_mppi_step(const gc_mppi_args *args, void *stream);
 gc_status gc_exact_predict(const gc_exact_args *args, void *stream);
+gc_status gc_predict_naive(const gc_naive_args *args, void *stream);
 gc_status gc_grid_epilogue(const gc_epilogue_args *args, void *stream);
 gc_status gc_belief_update(const gc_belief_args *args, void *stream);
 

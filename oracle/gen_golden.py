@@ -16,6 +16,7 @@ not exist on the GPU box).  Cases (reference file:line they exercise):
   multi.npz     sim-style per-human predict + union_max + time union
                                                                 sim.py:489-504
   exact.npz     exact_predict() on the lattice instance         prediction.py:303-377
+  naive_*.npz   predict_naive() float64 per-particle loop        prediction.py:258-300
 """
 
 from __future__ import annotations
@@ -233,6 +234,45 @@ def gen_predict(G):
         print("predict", name, "nnz", len(nz[0]))
 
 
+def naive_cases():
+    v, th = _grid_cs()
+    gp = dict(family="goal_progress", tau=0.5, w_v=0.0, w_th=0.0, v_threshold=None)
+    return {
+        # cfg1-like, two 1024-particle stream chunks (the second partial)
+        "gp": dict(v=v, theta=th, betas=list(np.geomspace(0.1, 10, 5)), goals=[[8.5, 5.0], [1.5, 7.0]],
+                   q=gp, grid=[100, 100, 0.1, [0.0, 0.0]], z0=[5.0, 5.0], n=1100, steps=10, dt=0.1,
+                   sigma=0.0, seed=4, belief="posterior"),
+        "masked_s01": dict(v=v, theta=th, betas=[0.5, 3.0], goals=[[4.0, 9.0], [9.0, 1.0]],
+                           q=dict(family="goal_progress", tau=0.5, w_v=0.0, w_th=0.0, v_threshold=0.5),
+                           grid=[60, 60, 0.1, [0.0, 0.0]], z0=[3.0, 3.0], n=400, steps=6, dt=0.1,
+                           sigma=0.1, seed=9, belief="random"),
+        "qdefault": dict(v=v, theta=th, betas=[0.3, 1.0, 3.0], goals=[[1.0, 1.0], [2.0, 3.0]],
+                         q=dict(family="default", tau=0.5, w_v=0.3, w_th=2.0, v_threshold=None),
+                         grid=[64, 48, 0.05, [-0.5, 0.25]], z0=[1.1, 1.3], n=300, steps=5, dt=0.05,
+                         sigma=0.0, seed=11, belief="uniform"),
+        # weights, start near the origin corner (edge clamping)
+        "weights_edge": dict(v=v, theta=th, betas=[0.5, 2.0, 8.0], goals=[[-1.0, 0.3], [3.0, 2.9]],
+                             q=dict(family="goal_progress", tau=0.3, w_v=0.2, w_th=0.1, v_threshold=None),
+                             grid=[40, 30, 0.1, [0.0, 0.0]], z0=[0.35, 0.2], n=700, steps=8, dt=0.1,
+                             sigma=0.0, seed=99, belief="random"),
+    }
+
+
+def gen_naive(G):
+    from gridcast.prediction import PredictionConfig, predict_naive
+    for name, case in naive_cases().items():
+        cs, space, q, spec = _spec(G, case)
+        b = _belief_for(G, space, cs, case["belief"], 17)
+        cfg = PredictionConfig(n=case["n"], steps=case["steps"], dt=case["dt"],
+                               smoothing_sigma=case["sigma"], seed=case["seed"])
+        st = predict_naive(G.HumanState(*case["z0"]), b, cfg, cs, q, space, spec)
+        L = st.layers
+        nz = np.nonzero(L)
+        np.savez_compressed(os.path.join(OUT, f"naive_{name}.npz"), meta=json.dumps(case), log_w=b.log_weights,
+                            idx=np.stack(nz, axis=1).astype(np.int32), val=L[nz], shape=np.array(L.shape))
+        print("naive", name, "nnz", len(nz[0]))
+
+
 def gen_belief(G):
     from gridcast.belief import update_belief, mask_stationary, ControlSnapMismatch
     from oracle.model import control_grid
@@ -429,6 +469,7 @@ def main():
     gen_collision(G)
     gen_gcst(G)
     gen_mppi(G)
+    gen_naive(G)
     import platform
     with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
         f.write(f"generated by oracle/gen_golden.py from {REF}\n")

@@ -5,6 +5,7 @@
   predict             prediction.py:223-255  (propagate -> emplace/n -> smooth per layer)
   smooth_dense        occupancy.py:122-154   (column-normalised truncated Gaussian)
   smooth_banded       SURVEY.md App. A.5     (same operator as a 7-tap-style banded stencil)
+  predict_naive       prediction.py:258-300  (float64 per-particle loop, f64 chunk streams)
   union_max/time_union occupancy.py:162-192, sim.py:500-504
   belief_update       belief.py:159-198 with agents.py:299-323, :355-371, :114-134
 """
@@ -136,6 +137,41 @@ def predict(z0, log_w, n, steps, dt, sigma, seed, tables: Tables, beta_of, goal_
     if keep_xy:
         out["xy"] = np.stack(xs)
     return out
+
+
+def predict_naive(z0, log_w, n, steps, dt, sigma, seed, v, theta, q: QSpec, beta_of, goal_xy_of, grid):
+    """predict_naive (prediction.py:258-300): one particle at a time in float64 -- q.table
+    of the particle's hypothesis (agents.py:222-224), beta x, max shift, exp, cumsum,
+    #(cdf < u cdf[-1]); u from the f64 chunk streams (seed, 1, t, chunk) (no prefix);
+    displacements v cos(theta) dt in f64 (agents.py:108-112); f64 cells_of."""
+    v = np.asarray(v, float)
+    theta = np.asarray(theta, float)
+    beta_of = np.asarray(beta_of, float)
+    goal_xy_of = np.asarray(goal_xy_of, float)
+    hyp = sample_hypotheses(log_w, n, seed)
+    xy = np.tile(np.array([z0[0], z0[1]], dtype=float), (n, 1))
+    disp = np.stack([v * np.cos(theta) * dt, v * np.sin(theta) * dt], axis=1)
+    keep = np.arange(len(v)) if not q.masked else np.flatnonzero(~(v > q.v_threshold))
+    layers = np.empty((steps, grid.height, grid.width))
+    for t in range(1, steps + 1):
+        for c, start in enumerate(range(0, n, CHUNK)):
+            stop = min(start + CHUNK, n)
+            u = philox.stream_random_f64(seed, (1, t, c), stop - start)
+            for i in range(start, stop):
+                h = hyp[i]
+                qt = q_table_f64(xy[i:i + 1], goal_xy_of[h:h + 1], v, theta, q)[0, keep]
+                logits = beta_of[h] * qt
+                logits -= logits.max()
+                cdf = np.cumsum(np.exp(logits))
+                j = min(int(np.sum(cdf < u[i - start] * cdf[-1])), len(keep) - 1)
+                xy[i] += disp[keep[j]]
+        ix = np.clip(np.floor((xy[:, 0] - grid.origin[0]) / grid.resolution).astype(np.int64), 0, grid.width - 1)
+        iy = np.clip(np.floor((xy[:, 1] - grid.origin[1]) / grid.resolution).astype(np.int64), 0, grid.height - 1)
+        vals = np.bincount(iy * grid.width + ix, minlength=grid.width * grid.height).reshape(grid.shape) / n
+        if sigma > 0:
+            vals = smooth_dense(vals, grid, sigma)
+        layers[t - 1] = vals
+    return dict(hyp=hyp, layers=layers, xy=xy)
 
 
 def union_max(stacks):

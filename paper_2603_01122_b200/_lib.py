@@ -105,6 +105,18 @@ class ExactArgs(ctypes.Structure):
     ]
 
 
+class NaiveArgs(ctypes.Structure):
+    _fields_ = [
+        ("n", I32), ("steps", I32), ("n_hyp", I32), ("m_keep", I32),
+        ("q_kind", I32), ("grid_w", I32), ("grid_h", I32), ("prefix_len", I32),
+        ("seed", U64), ("prefix", ctypes.c_uint32 * 4),
+        ("start_x", F64), ("start_y", F64), ("origin_x", F64), ("origin_y", F64), ("res", F64),
+        ("d_hyp", P), ("d_beta", P), ("d_goal", P), ("d_keep", P),
+        ("d_sx", P), ("d_sy", P), ("d_at", P), ("d_pen", P), ("d_dispx", P), ("d_dispy", P),
+        ("d_counts", P), ("d_xy_out", P),
+    ]
+
+
 class MppiArgs(ctypes.Structure):
     _fields_ = [
         ("n_rollouts", I32), ("horizon", I32),
@@ -125,7 +137,7 @@ EXPORTS = (
     "gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
     "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
     "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
-    "gc_collision_field", "gc_exact_predict", "gc_mppi_step",
+    "gc_collision_field", "gc_exact_predict", "gc_mppi_step", "gc_predict_naive",
 )
 
 _lib = None
@@ -155,9 +167,10 @@ def lib():
     L.gc_collision_field.argtypes = [P, I32, I32, I32, I32, P, I32, F64, P, P, P]
     L.gc_exact_predict.argtypes = [ctypes.POINTER(ExactArgs), P]
     L.gc_mppi_step.argtypes = [ctypes.POINTER(MppiArgs), P]
+    L.gc_predict_naive.argtypes = [ctypes.POINTER(NaiveArgs), P]
     for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
                "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field",
-               "gc_exact_predict", "gc_mppi_step"):
+               "gc_exact_predict", "gc_mppi_step", "gc_predict_naive"):
         getattr(L, fn).restype = ctypes.c_int
     L.gc_derive_seed.argtypes = [U64, P, I32]
     L.gc_derive_seed.restype = U64

@@ -346,6 +346,61 @@ def predict(z_history, belief: JointBelief, cfg: PredictionConfig, control_set: 
     return PredictionStack(grid_spec, out["layers"][0], base_time, cfg.dt)
 
 
+def predict_naive(z_history, belief: JointBelief, cfg: PredictionConfig, control_set: ControlSet, q: QFunction,
+                  space: HypothesisSpace, grid_spec: GridSpec, base_time: float = 0.0) -> PredictionStack:
+    """The reference's plain per-particle loop (prediction.py:258-300) on the GPU
+    (gc_predict_naive): float64 positions, the full q.table row of each particle's
+    hypothesis, the same chunk-keyed streams drawn in float64, float64 cells.  Its layers
+    equal the reference's (a decision could differ only if a uniform lands within an ulp
+    of a cdf entry, the float64 exp being CUDA's rather than numpy's)."""
+    from .agents import EmptyControlSetError
+    from .tables import f64_tables, recognise_q
+    z0 = _as_state(z_history)
+    if len(belief) != space.size:
+        raise ValueError("belief size does not match hypothesis space")
+    lq = recognise_q(q)
+    if lq is None:
+        raise NotImplementedError("predict_naive on the B200 implements q_goal_progress and q_default "
+                                  "(and their stationary-masked variants)")
+    v, th = np.asarray(control_set.v, float), np.asarray(control_set.theta, float)
+    mask = q.action_mask(control_set)
+    keep = np.arange(len(v)) if mask is None else np.flatnonzero(~mask)
+    if len(keep) == 0:
+        raise EmptyControlSetError("all actions are masked")
+    dev = device()
+    up = lambda a_, t_: torch.as_tensor(np.ascontiguousarray(np.asarray(a_, dtype=t_)), device=dev)  # noqa: E731
+    sx, sy, at, pen = f64_tables(v, th, lq)
+    disp = control_set.displacements(cfg.dt)
+    beta_of, goal_of = hypothesis_arrays(space)
+    hyp = up(sample_hypotheses(belief, cfg.n, cfg.seed), np.int32)
+    bufs = dict(beta=up(beta_of, np.float64), goal=up(goal_of, np.float64), keep=up(keep, np.int32),
+                sx=up(sx, np.float64), sy=up(sy, np.float64), at=up(at, np.float64), pen=up(pen, np.float64),
+                dx=up(disp[:, 0], np.float64), dy=up(disp[:, 1], np.float64))
+    T, H, W = cfg.steps, grid_spec.height, grid_spec.width
+    counts = torch.zeros(T * H * W, dtype=torch.int32, device=dev)
+    a = _lib.NaiveArgs()
+    a.n, a.steps, a.n_hyp, a.m_keep = cfg.n, T, len(beta_of), len(keep)
+    a.q_kind = _lib.GC_Q_DEFAULT if lq.family == "default" else _lib.GC_Q_GOAL_PROGRESS_FULL
+    a.grid_w, a.grid_h, a.prefix_len, a.seed = W, H, 0, int(cfg.seed) & _MASK64
+    a.start_x, a.start_y = float(z0.x), float(z0.y)
+    a.origin_x, a.origin_y, a.res = grid_spec.origin[0], grid_spec.origin[1], grid_spec.resolution
+    a.d_hyp, a.d_beta, a.d_goal, a.d_keep = (hyp.data_ptr(), bufs["beta"].data_ptr(), bufs["goal"].data_ptr(),
+                                             bufs["keep"].data_ptr())
+    a.d_sx, a.d_sy, a.d_at, a.d_pen = (bufs["sx"].data_ptr(), bufs["sy"].data_ptr(), bufs["at"].data_ptr(),
+                                       bufs["pen"].data_ptr())
+    a.d_dispx, a.d_dispy, a.d_counts = bufs["dx"].data_ptr(), bufs["dy"].data_ptr(), counts.data_ptr()
+    _lib.check(_lib.lib().gc_predict_naive(ctypes.byref(a), stream_handle()), "predict_naive")
+    # emplace_counts(...) / n as an elementwise IEEE division (a Python-scalar divisor would
+    # let torch multiply by the reciprocal instead, which is not numpy's rounding)
+    layers = counts.view(T, H, W).to(torch.float64)
+    layers = layers / torch.full_like(layers, float(cfg.n))
+    if cfg.smoothing_sigma > 0:
+        from .occupancy import smooth_layers_device
+        layers = smooth_layers_device(layers, grid_spec, cfg.smoothing_sigma)
+    torch.cuda.current_stream().synchronize()
+    return PredictionStack(grid_spec, layers, base_time, cfg.dt)
+
+
 def predict_multi(humans: Sequence[tuple], cfg: PredictionConfig, control_set: ControlSet, q: QFunction,
                   space: HypothesisSpace, grid_spec: GridSpec, workers: Optional[int] = None,
                   base_time: float = 0.0) -> PredictionStack:

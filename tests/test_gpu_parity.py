@@ -352,3 +352,30 @@ def test_particle_block_sharding_is_partition_independent(mode):
     run(dataclasses.replace(cfg, particle_shard=(0, 2)), reduce=lambda c: held.setdefault("c", c.clone()))
     merged = run(dataclasses.replace(cfg, particle_shard=(1, 2)), reduce=lambda c: c.add_(held["c"]))
     np.testing.assert_array_equal(merged, full)
+
+
+@pytest.mark.parametrize("name", golden_io.naive_case_names())
+def test_predict_naive_matches_reference(name):
+    """predict_naive (prediction.py:258-300) through gc_predict_naive: the float64
+    per-particle loop reproduces the reference's layers (counts/n exactly at sigma 0)."""
+    case = golden_io.NaiveCase(name)
+    cs, space, q, spec = _objects(case)
+    b = G.JointBelief(case.log_w)
+    cfg = G.PredictionConfig(n=case.n, steps=case.steps, dt=case.dt, smoothing_sigma=case.sigma,
+                             seed=case.seed)
+    st = G.predict_naive(G.HumanState(*case.z0), b, cfg, cs, q, space, spec)
+    if case.sigma == 0:
+        np.testing.assert_array_equal(st.layers, case.layers)
+    else:
+        np.testing.assert_allclose(st.layers, case.layers, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(st.layers.sum(axis=(1, 2)), 1.0, atol=1e-9)
+
+
+def test_predict_naive_abi_rejects_empty_control_set():
+    """m_keep = 0 (every action masked) -> GC_EMPTY_CONTROL_SET -> EmptyControlSetError."""
+    import ctypes
+    from paper_2603_01122_b200 import _lib
+    a = _lib.NaiveArgs()
+    a.n, a.steps, a.m_keep = 4, 1, 0
+    with pytest.raises(G.EmptyControlSetError):
+        _lib.check(_lib.lib().gc_predict_naive(ctypes.byref(a), None), "predict_naive")

@@ -135,3 +135,16 @@ def test_cpu_baseline_port_matches_reference(name):
     layers = port.predict(c.z0, c.log_w, c.n, c.steps, c.dt, c.sigma, c.seed, c.tables(),
                           c.beta_of, c.goal_xy_of, OP.Grid(W, H, res, org), prefix=c.prefix, workers=4)
     np.testing.assert_array_equal(layers[c.layer_steps], c.layers)
+
+
+@pytest.mark.parametrize("name", golden_io.naive_case_names())
+def test_oracle_predict_naive_matches_reference(name):
+    """float64 per-particle loop (prediction.py:258-300): layers identical to the reference's."""
+    c = golden_io.NaiveCase(name)
+    W, H, res, org = c.grid
+    out = OP.predict_naive(c.z0, c.log_w, c.n, c.steps, c.dt, c.sigma, c.seed, c.meta["v"], c.meta["theta"],
+                           c.qspec(), c.beta_of, c.goal_xy_of, OP.Grid(W, H, res, org))
+    if c.sigma == 0:
+        np.testing.assert_array_equal(out["layers"], c.layers)
+    else:
+        np.testing.assert_allclose(out["layers"], c.layers, rtol=0, atol=1e-15)
