@@ -253,6 +253,21 @@ gc_status gc_predict(const gc_predict_args *args, void *stream);
 gc_status gc_mppi_step(const gc_mppi_args *args, void *stream);
 gc_status gc_exact_predict(const gc_exact_args *args, void *stream);
 gc_status gc_predict_naive(const gc_naive_args *args, void *stream);
+
+/* Cell-wise union of k stacked layer sets (occupancy.py:162-192), in the reference's
+ * order and float64 arithmetic: input i starts at element i * stride of d_in and has
+ * `cells` elements (float32 when in_bytes == 4, float64 when 8); d_out has `cells`.
+ * GC_UNION_MAX: max_i p_i; GC_UNION_INDEPENDENT: 1 - prod_i (1 - clip(p_i, 0, 1));
+ * GC_UNION_MISS: prod_i (1 - clip(p_i, 0, 1)) (a partial for a cross-GPU product
+ * reduction); GC_UNION_COMPLEMENT: 1 - p_0 (finishes a reduced MISS). */
+enum { GC_UNION_MAX = 0, GC_UNION_INDEPENDENT = 1, GC_UNION_MISS = 2, GC_UNION_COMPLEMENT = 3 };
+gc_status gc_union_layers(const void *d_in, int32_t in_bytes, int32_t k, int64_t stride, int64_t cells,
+                          int32_t mode, void *d_out, int32_t out_bytes, void *stream);
+
+/* Conservative time union (sim.py:503-504, np.maximum.accumulate over layers) of layers
+ * [t_begin, t_end) of a (T, H, W) stack, seeded by layer t_begin - 1 when t_begin > 0. */
+gc_status gc_time_union(void *d_union, int32_t dtype_bytes, int32_t t_begin, int32_t t_end, int64_t cells,
+                        void *stream);
 gc_status gc_grid_epilogue(const gc_epilogue_args *args, void *stream);
 gc_status gc_belief_update(const gc_belief_args *args, void *stream);
 

@@ -370,12 +370,16 @@ def gen_multi(G):
         st = predict(G.HumanState(*s), b, cfg, cs, q, space, spec, prefix=(2, i))
         stacks.append(st)
         humans.append(dict(start=list(s), goals=goals.tolist(), log_w=b.log_weights.tolist()))
+    from gridcast.occupancy import union
     layers = np.stack([union_max([s.grid(k) for s in stacks]).values for k in range(cfg.steps)])
     tu = np.maximum.accumulate(layers, axis=0)
+    # the "independent" union 1 - prod(1 - p) (occupancy.py:180-184)
+    ind = np.stack([union([s.grid(k) for s in stacks], mode="independent").values for k in range(cfg.steps)])
     np.savez_compressed(os.path.join(OUT, "multi.npz"),
                         meta=json.dumps(dict(humans=humans, seed=str(seed), n=cfg.n, steps=cfg.steps,
                                              dt=cfg.dt, sigma=cfg.smoothing_sigma)),
-                        union=layers.astype(np.float64), time_union=tu)
+                        union=layers.astype(np.float64), time_union=tu,
+                        independent=ind, independent_tu=np.maximum.accumulate(ind, axis=0))
 
 
 def gen_exact(G):

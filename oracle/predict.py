@@ -6,7 +6,7 @@
   smooth_dense        occupancy.py:122-154   (column-normalised truncated Gaussian)
   smooth_banded       SURVEY.md App. A.5     (same operator as a 7-tap-style banded stencil)
   predict_naive       prediction.py:258-300  (float64 per-particle loop, f64 chunk streams)
-  union_max/time_union occupancy.py:162-192, sim.py:500-504
+  union_max/union_independent/time_union occupancy.py:162-192, sim.py:500-504
   belief_update       belief.py:159-198 with agents.py:299-323, :355-371, :114-134
 """
 
@@ -179,6 +179,14 @@ def union_max(stacks):
     for s in stacks[1:]:
         np.maximum(out, s, out=out)
     return out
+
+
+def union_independent(stacks):
+    """1 - prod(1 - clip(p, 0, 1)) in the reference's order (occupancy.py:180-184)."""
+    miss = 1.0 - np.clip(np.asarray(stacks[0], dtype=float), 0.0, 1.0)
+    for s in stacks[1:]:
+        miss = miss * (1.0 - np.clip(np.asarray(s, dtype=float), 0.0, 1.0))
+    return 1.0 - miss
 
 
 def time_union(layers):

@@ -27,6 +27,7 @@ GC_Q_GOAL_PROGRESS = 0
 GC_Q_GOAL_PROGRESS_FULL = 1
 GC_Q_DEFAULT = 2
 GC_Q_TABLE = 3
+GC_UNION_MAX, GC_UNION_INDEPENDENT, GC_UNION_MISS, GC_UNION_COMPLEMENT = 0, 1, 2, 3
 
 GC_RNG_REFERENCE = 0
 GC_RNG_UNIFORMS = 1
@@ -138,6 +139,7 @@ EXPORTS = (
     "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
     "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
     "gc_collision_field", "gc_exact_predict", "gc_mppi_step", "gc_predict_naive",
+    "gc_union_layers", "gc_time_union",
 )
 
 _lib = None
@@ -168,9 +170,12 @@ def lib():
     L.gc_exact_predict.argtypes = [ctypes.POINTER(ExactArgs), P]
     L.gc_mppi_step.argtypes = [ctypes.POINTER(MppiArgs), P]
     L.gc_predict_naive.argtypes = [ctypes.POINTER(NaiveArgs), P]
+    L.gc_union_layers.argtypes = [P, I32, I32, I64, I64, I32, P, I32, P]
+    L.gc_time_union.argtypes = [P, I32, I32, I32, I64, P]
     for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
                "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field",
-               "gc_exact_predict", "gc_mppi_step", "gc_predict_naive"):
+               "gc_exact_predict", "gc_mppi_step", "gc_predict_naive", "gc_union_layers",
+               "gc_time_union"):
         getattr(L, fn).restype = ctypes.c_int
     L.gc_derive_seed.argtypes = [U64, P, I32]
     L.gc_derive_seed.restype = U64

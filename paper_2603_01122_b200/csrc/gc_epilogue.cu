@@ -259,3 +259,66 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
     }
     return GC_OK;
 }
+
+// ---- ordered union of k stacked layer sets (occupancy.py:162-192) --------------------
+// input i = in + i * stride (elements), `cells` elements each; float64 arithmetic in the
+// reference's order: max, or miss = 1 - clip(p_0); miss *= 1 - clip(p_i); out = 1 - miss.
+namespace gc {
+template <typename Ti, typename To>
+__global__ void __launch_bounds__(256) k_union(const Ti *in, int k, long long stride, long long cells, int mode,
+                                               To *out) {
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+         c += (long long)gridDim.x * blockDim.x) {
+        double acc;
+        if (mode == GC_UNION_MAX) {
+            acc = (double)in[c];
+            for (int i = 1; i < k; ++i) acc = fmax(acc, (double)in[i * stride + c]);
+        } else if (mode == GC_UNION_COMPLEMENT) {
+            acc = __dsub_rn(1.0, (double)in[c]);
+        } else {
+            double miss = __dsub_rn(1.0, fmin(fmax((double)in[c], 0.0), 1.0));
+            for (int i = 1; i < k; ++i)
+                miss = __dmul_rn(miss, __dsub_rn(1.0, fmin(fmax((double)in[i * stride + c], 0.0), 1.0)));
+            acc = mode == GC_UNION_INDEPENDENT ? __dsub_rn(1.0, miss) : miss;
+        }
+        out[c] = (To)acc;
+    }
+}
+
+template <typename Ti, typename To>
+static void launch_union(const void *in, int k, long long stride, long long cells, int mode, void *out,
+                         cudaStream_t st) {
+    long long blocks = (cells + 255) / 256;
+    blocks = blocks < 148 * 16 ? blocks : 148 * 16;
+    k_union<Ti, To><<<(int)blocks, 256, 0, st>>>((const Ti *)in, k, stride, cells, mode, (To *)out);
+}
+}  // namespace gc
+
+extern "C" gc_status gc_union_layers(const void *d_in, int32_t in_bytes, int32_t k, int64_t stride, int64_t cells,
+                                     int32_t mode, void *d_out, int32_t out_bytes, void *stream) {
+    GC_CHECK_ARG(d_in && d_out && k >= 1 && cells >= 0 && stride >= 0, "gc_union_layers: bad arguments");
+    GC_CHECK_ARG((in_bytes == 4 || in_bytes == 8) && (out_bytes == 4 || out_bytes == 8),
+                 "gc_union_layers: float32 or float64 layers");
+    GC_CHECK_ARG(mode >= GC_UNION_MAX && mode <= GC_UNION_COMPLEMENT, "gc_union_layers: unknown mode");
+    if (cells == 0) return GC_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (in_bytes == 8 && out_bytes == 8) launch_union<double, double>(d_in, k, stride, cells, mode, d_out, st);
+    else if (in_bytes == 8) launch_union<double, float>(d_in, k, stride, cells, mode, d_out, st);
+    else if (out_bytes == 8) launch_union<float, double>(d_in, k, stride, cells, mode, d_out, st);
+    else launch_union<float, float>(d_in, k, stride, cells, mode, d_out, st);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_union launch");
+}
+
+extern "C" gc_status gc_time_union(void *d_union, int32_t dtype_bytes, int32_t t_begin, int32_t t_end,
+                                   int64_t cells, void *stream) {
+    GC_CHECK_ARG(d_union && (dtype_bytes == 4 || dtype_bytes == 8), "gc_time_union: float32 or float64 layers");
+    GC_CHECK_ARG(t_begin >= 0 && t_begin < t_end && cells >= 0, "gc_time_union: bad layer range");
+    if (cells == 0 || t_end - (t_begin > 0 ? t_begin - 1 : 0) < 2) return GC_OK;
+    const int blocks = (int)((cells + 255) / 256);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype_bytes == 4) k_time_union<float><<<blocks, 256, 0, st>>>((float *)d_union, t_begin, t_end, cells);
+    else k_time_union<double><<<blocks, 256, 0, st>>>((double *)d_union, t_begin, t_end, cells);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_time_union launch");
+}

@@ -49,6 +49,12 @@ class EngineConfig:
     stationary_speed: float = 0.05     # sim.py:480 (observed speed below -> masked Q)
     stationary_mask_v: float = 0.5     # mask_stationary threshold (sim.py:111)
     union_dtype: str = "float32"       # fused union precision: float32 | float64
+    # "max" (occupancy.union_max, the sim's union) or "independent" 1 - prod(1 - p)
+    # (occupancy.py:180-184); independent keeps per-human float64 layers and merges them
+    # in human order.  union_partial: keep prod(1 - p) of this rank's humans instead, for
+    # fused_reduce(..., mode="independent") across GPUs.
+    union_mode: str = "max"
+    union_partial: bool = False
     time_union: bool = False
     per_human_layers: bool = False
     # planner input (anastar.py:107-119, mppi.py:87-94): collision field of the fused
@@ -140,8 +146,12 @@ class CycleEngine:
         udt = torch.float32 if cfg.union_dtype == "float32" else torch.float64
         T, Hh, W = cfg.steps, grid_spec.height, grid_spec.width
         self.unions = [torch.zeros((T, Hh, W), dtype=udt, device=dev) for _ in range(2)]
+        if cfg.union_mode not in ("max", "independent"):
+            raise ValueError(f"unknown union mode {cfg.union_mode!r}")
+        if cfg.union_partial and cfg.union_mode != "independent":
+            raise ValueError("union_partial applies to the independent union")
         self.layers = (torch.zeros((H, T, Hh, W), dtype=torch.float64, device=dev)
-                       if cfg.per_human_layers else None)
+                       if cfg.per_human_layers or cfg.union_mode == "independent" else None)
         self.d_err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.blocked = None
         if cfg.robot_radius is not None:
@@ -263,11 +273,13 @@ class CycleEngine:
         e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), self.counts.data_ptr()
         if self.layers is not None:
             e.d_layers64 = self.layers.data_ptr()
-        if u.dtype == torch.float32:
-            e.d_union32 = u.data_ptr()
-        else:
-            e.d_union64 = u.data_ptr()
-        e.time_union = int(cfg.time_union)
+        ordered = cfg.union_mode == "independent"
+        if not ordered:  # max union by atomicMax inside K3
+            if u.dtype == torch.float32:
+                e.d_union32 = u.data_ptr()
+            else:
+                e.d_union64 = u.data_ptr()
+            e.time_union = int(cfg.time_union)
         for ci, (t0, t1) in enumerate(bounds):
             a.t_begin, a.t_end = (t0, t1) if len(bounds) > 1 else (0, 0)
             if events is not None and ci == 0:
@@ -281,6 +293,17 @@ class CycleEngine:
                 e.tile_begin, e.tile_end = int(geo.tile_start[t0 - 1]), int(geo.tile_start[t1 - 1])
                 e.t_begin, e.t_end = t0 - 1, t1 - 1
             _lib.check(_lib.lib().gc_grid_epilogue(ctypes.byref(e), sh), "gc_grid_epilogue")
+            if ordered:
+                # ordered merge of the per-human float64 layers of this chunk
+                L0, L1 = t0 - 1, t1 - 1
+                hw = self.spec.width * self.spec.height
+                mode = _lib.GC_UNION_MISS if cfg.union_partial else _lib.GC_UNION_INDEPENDENT
+                _lib.check(_lib.lib().gc_union_layers(
+                    ctypes.c_void_p(self.layers[0, L0].data_ptr()), 8, H, cfg.steps * hw, (L1 - L0) * hw, mode,
+                    ctypes.c_void_p(u[L0].data_ptr()), u.element_size(), sh), "gc_union_layers")
+                if cfg.time_union and not cfg.union_partial:
+                    _lib.check(_lib.lib().gc_time_union(ctypes.c_void_p(u.data_ptr()), u.element_size(), L0, L1,
+                                                        hw, sh), "gc_time_union")
             if self.blocked is not None:
                 L0, L1 = t0 - 1, t1 - 1
                 _lib.check(_lib.lib().gc_collision_field(
@@ -347,12 +370,44 @@ class CycleEngine:
             raise RuntimeError("gc_predict: a particle left its reachable-cell window")
 
 
-def fused_reduce(union: torch.Tensor, group=None, dst: Optional[int] = None):
-    """Merge per-rank unions into one fused grid with a max reduction over NCCL
-    (torch.distributed); all_reduce when dst is None."""
+def fused_reduce(union: torch.Tensor, group=None, dst: Optional[int] = None, mode: str = "max",
+                 time_union: bool = False, finish: bool = True):
+    """Merge per-rank unions into one fused grid over NCCL (torch.distributed); all_reduce
+    when dst is None.  mode "max": max reduction of the per-rank max unions.  mode
+    "independent": the ranks hold prod(1 - p) partials (EngineConfig(union_partial=True));
+    they are multiplied (ReduceOp.PRODUCT) and, when ``finish``, complemented on the
+    receiving rank(s) to 1 - prod (+ the conservative time union when ``time_union``).
+    The cross-rank product is taken in NCCL's order, so the independent fused grid equals
+    the single-GPU one up to float rounding (max is exact)."""
     import torch.distributed as dist
+    if mode == "max":
+        if dst is None:
+            dist.all_reduce(union, op=dist.ReduceOp.MAX, group=group)
+        else:
+            dist.reduce(union, dst=dst, op=dist.ReduceOp.MAX, group=group)
+        return union
+    if mode != "independent":
+        raise ValueError(f"unknown union mode {mode!r}")
     if dst is None:
-        dist.all_reduce(union, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(union, op=dist.ReduceOp.PRODUCT, group=group)
     else:
-        dist.reduce(union, dst=dst, op=dist.ReduceOp.MAX, group=group)
+        dist.reduce(union, dst=dst, op=dist.ReduceOp.PRODUCT, group=group)
+    if finish and (dst is None or dist.get_rank() == dst):
+        complement_layers(union, time_union=time_union)
+    return union
+
+
+def complement_layers(union: torch.Tensor, time_union: bool = False) -> torch.Tensor:
+    """In place 1 - miss (+ time union) of a (T, H, W) miss-product stack on the GPU
+    (gc_union_layers GC_UNION_COMPLEMENT, gc_time_union)."""
+    if union.device.type != "cuda":
+        raise RuntimeError("complement_layers needs a CUDA tensor (no CPU path)")
+    sh = ctypes.c_void_p(torch.cuda.current_stream(union.device).cuda_stream)
+    hw = union.shape[-1] * union.shape[-2]
+    _lib.check(_lib.lib().gc_union_layers(ctypes.c_void_p(union.data_ptr()), union.element_size(), 1, 0,
+                                          union.numel(), _lib.GC_UNION_COMPLEMENT, ctypes.c_void_p(union.data_ptr()),
+                                          union.element_size(), sh), "gc_union_layers")
+    if time_union:
+        _lib.check(_lib.lib().gc_time_union(ctypes.c_void_p(union.data_ptr()), union.element_size(), 0,
+                                            union.shape[0], hw, sh), "gc_time_union")
     return union

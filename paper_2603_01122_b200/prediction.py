@@ -198,8 +198,12 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
                 sigma: float, spec: GridSpec, mode: str, per_human_layers: bool = True,
                 union64: bool = False, union32: bool = False, time_union: bool = False,
                 uniforms: Optional[torch.Tensor] = None, hyp_in: Optional[torch.Tensor] = None,
-                want_hyp: bool = False, want_xy: bool = False, stream=None):
-    """Batched K2 + K3 launch; returns a dict of device tensors."""
+                want_hyp: bool = False, want_xy: bool = False, stream=None, union_mode: str = "max"):
+    """Batched K2 + K3 launch; returns a dict of device tensors.  union_mode "max" merges
+    the humans by atomicMax inside K3; "independent" (1 - prod(1 - p), occupancy.py:180-184)
+    merges the per-human float64 layers afterwards in human order (gc_union_layers)."""
+    if union_mode not in ("max", "independent"):
+        raise ValueError(f"unknown union mode {union_mode!r}")
     dev = device()
     H = len(jobs)
     max_step = max(t.max_step for t in tables)
@@ -264,17 +268,31 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     e.n_tiles, e.d_start_xy = geo.n_tiles, d_start.data_ptr()
     e.d_step_r, e.d_step_off, e.human_stride = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr(), geo.human_stride
     e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), counts.data_ptr()
-    if per_human_layers:
+    ordered = union_mode == "independent" and (union64 or union32)
+    if per_human_layers or ordered:
         out["layers"] = torch.zeros((H, steps, spec.height, spec.width), dtype=torch.float64, device=dev)
         e.d_layers64 = out["layers"].data_ptr()
     if union64:
         out["union64"] = torch.zeros((steps, spec.height, spec.width), dtype=torch.float64, device=dev)
-        e.d_union64 = out["union64"].data_ptr()
+        e.d_union64 = 0 if ordered else out["union64"].data_ptr()
     if union32:
         out["union32"] = torch.zeros((steps, spec.height, spec.width), dtype=torch.float32, device=dev)
-        e.d_union32 = out["union32"].data_ptr()
-    e.time_union = int(time_union)
+        e.d_union32 = 0 if ordered else out["union32"].data_ptr()
+    e.time_union = int(time_union and not ordered)
     _lib.check(_lib.lib().gc_grid_epilogue(ctypes.byref(e), sh), "gc_grid_epilogue")
+    if ordered:
+        cells = steps * spec.height * spec.width
+        for key in ("union64", "union32"):
+            if key in out:
+                u = out[key]
+                _lib.check(_lib.lib().gc_union_layers(
+                    ctypes.c_void_p(out["layers"].data_ptr()), 8, H, cells, cells, _lib.GC_UNION_INDEPENDENT,
+                    ctypes.c_void_p(u.data_ptr()), u.element_size(), sh), "gc_union_layers")
+                if time_union:
+                    _lib.check(_lib.lib().gc_time_union(ctypes.c_void_p(u.data_ptr()), u.element_size(), 0, steps,
+                                                        spec.height * spec.width, sh), "gc_time_union")
+        if not per_human_layers:
+            del out["layers"]
     if int(err.item()) != 0:
         raise RuntimeError("gc_predict: a particle left its reachable-cell window (internal error)")
     out["counts"] = counts
@@ -403,9 +421,11 @@ def predict_naive(z_history, belief: JointBelief, cfg: PredictionConfig, control
 
 def predict_multi(humans: Sequence[tuple], cfg: PredictionConfig, control_set: ControlSet, q: QFunction,
                   space: HypothesisSpace, grid_spec: GridSpec, workers: Optional[int] = None,
-                  base_time: float = 0.0) -> PredictionStack:
+                  base_time: float = 0.0, union_mode: str = "max") -> PredictionStack:
     """Per-human prediction merged layer-wise by pointwise max (prediction.py:380-409):
-    one batched launch, union by the epilogue's atomicMax."""
+    one batched launch, union by the epilogue's atomicMax.  ``union_mode="independent"``
+    (an extension; occupancy.union's 1 - prod(1 - p), occupancy.py:180-184) merges the
+    per-human layers in order instead."""
     if not humans:
         raise ValueError("need at least one human")
     dev = device()
@@ -417,7 +437,8 @@ def predict_multi(humans: Sequence[tuple], cfg: PredictionConfig, control_set: C
             raise ValueError("belief size does not match hypothesis space")
         jobs.append(HumanJob(_as_state(hist), b.log_weights, beta_of, goal_of, cfg.seed, (), 0))
     out = run_predict(jobs, [tab], cfg.n, cfg.steps, cfg.dt, cfg.smoothing_sigma, grid_spec,
-                      getattr(cfg, "mode", "reference"), per_human_layers=False, union64=True)
+                      getattr(cfg, "mode", "reference"), per_human_layers=False, union64=True,
+                      union_mode=union_mode)
     return PredictionStack(grid_spec, out["union64"], base_time, cfg.dt)
 
 

@@ -143,6 +143,19 @@ def test_multi_union_time_union():
     np.testing.assert_allclose(out["union64"].cpu().numpy(), z["time_union"], rtol=0, atol=1e-15)
     np.testing.assert_allclose(out["union32"].cpu().numpy(), z["time_union"].astype(np.float32), rtol=0,
                                atol=1e-7)
+    # the "independent" union 1 - prod(1 - p) (occupancy.py:180-184), ordered over humans
+    out = PR.run_predict(jobs, [tab], meta["n"], meta["steps"], meta["dt"], meta["sigma"], spec,
+                         "reference", per_human_layers=True, union64=True, union_mode="independent")
+    np.testing.assert_allclose(out["union64"].cpu().numpy(), z["independent"], rtol=0, atol=1e-15)
+    host = 1.0 - np.prod(1.0 - np.clip(out["layers"].cpu().numpy(), 0, 1), axis=0)
+    np.testing.assert_array_equal(out["union64"].cpu().numpy(), host)
+    out = PR.run_predict(jobs, [tab], meta["n"], meta["steps"], meta["dt"], meta["sigma"], spec,
+                         "reference", per_human_layers=False, union64=True, union32=True, time_union=True,
+                         union_mode="independent")
+    np.testing.assert_allclose(out["union64"].cpu().numpy(), z["independent_tu"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(out["union32"].cpu().numpy(), z["independent_tu"].astype(np.float32), rtol=0,
+                               atol=1e-7)
+    assert "layers" not in out
 
 
 def test_predict_multi_semantics():
@@ -273,6 +286,41 @@ def test_engine_cycle_matches_reference_mode_and_blocked_mask():
     np.testing.assert_array_equal(eng.blocked[0].cpu().numpy(), (f.cpu().numpy() >= 0.05).astype(np.uint8))
     eng.reset_belief(1)
     np.testing.assert_allclose(np.exp(eng.posterior(1)), 1.0 / sc.spaces[1].size)
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_engine_independent_union_and_partials(chunks):
+    """EngineConfig(union_mode="independent"): the union is 1 - prod(1 - p) of the engine's
+    own per-human layers in human order (+ time union), chunked or not; the union_partial
+    miss product completed by complement_layers gives the same float64 grid."""
+    from paper_2603_01122_b200.engine import CycleEngine, EngineConfig, complement_layers
+    from paper_2603_01122_b200.scenario import make_scene
+    sc = make_scene("cfg1", cycles=3, humans=3)
+    res = {}
+    for partial in (False, True):
+        cfg = EngineConfig(n=2000, steps=10, dt=0.1, smoothing_sigma=0.1, seed=5, mode="production",
+                           union_dtype="float64", union_mode="independent", union_partial=partial,
+                           time_union=True)
+        eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
+        eng.prime(sc.prev_xy)
+        eng.stage(sc.track[0], buf=0)
+        if chunks > 1:
+            host = torch.empty(eng.unions[0].shape, dtype=eng.unions[0].dtype).pin_memory()
+            eng.capture(buf=0, chunks=chunks, d2h=host).replay()
+        else:
+            eng.run_cycle(buf=0)
+        torch.cuda.synchronize()
+        eng.check_errors()
+        u = eng.unions[0]
+        if partial:
+            complement_layers(u, time_union=True)
+        res[partial] = (u.cpu().numpy(), eng.layers.cpu().numpy())
+    u, L = res[False]
+    ind = 1.0 - np.prod(1.0 - np.clip(L, 0, 1), axis=0)
+    np.testing.assert_array_equal(u, np.maximum.accumulate(ind, axis=0))
+    np.testing.assert_array_equal(res[True][1], L)  # same layers (same streams)
+    np.testing.assert_array_equal(res[True][0], u)
+    assert u.max() > 0 and np.all(u >= np.max(L, axis=0) - 1e-15)
 
 
 @pytest.mark.parametrize("tag,with_stack,quad,n", [("nostack", False, False, 512), ("stack", True, False, 700),

@@ -121,3 +121,31 @@ def test_particle_sharded_counts_sum_to_single_process(tmp_path):
     s, lw, b, g = humans()[0]
     full = OP.predict(s, lw, 3000, T, DT, 0.0, SEED, tb, b, g, GRID, prefix=(2, 0))["counts"]
     np.testing.assert_array_equal(np.load(path), full)
+
+
+def _independent_worker(rank, world, port, result_path):
+    """Independent union across ranks: each rank holds prod(1 - p) of its humans
+    (EngineConfig(union_partial=True)); fused_reduce(mode="independent") multiplies the
+    partials (ReduceOp.PRODUCT); the receiving rank finishes 1 - prod on the GPU."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_01122_b200.engine import fused_reduce
+    r = np.random.default_rng(7)
+    layers = r.uniform(0.0, 0.3, size=(5, T, 12, 12))
+    mine = layers[rank::world]
+    miss = np.prod(1.0 - np.clip(mine, 0.0, 1.0), axis=0)
+    u = torch.from_numpy(miss.copy())
+    fused_reduce(u, dst=0, mode="independent", finish=False)
+    if rank == 0:
+        np.save(result_path, u.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_independent_union_partials_multiply_across_ranks(tmp_path):
+    path = str(tmp_path / "miss.npy")
+    mp.spawn(_independent_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    r = np.random.default_rng(7)
+    layers = r.uniform(0.0, 0.3, size=(5, T, 12, 12))
+    ref = OP.union_independent(list(layers))
+    np.testing.assert_allclose(1.0 - np.load(path), ref, rtol=0, atol=1e-15)

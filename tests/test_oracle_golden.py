@@ -124,6 +124,9 @@ def test_multi_union_and_time_union():
     u = OP.union_max(stacks)
     np.testing.assert_array_equal(u, z["union"])
     np.testing.assert_array_equal(OP.time_union(u), z["time_union"])
+    ind = OP.union_independent(stacks)
+    np.testing.assert_array_equal(ind, z["independent"])
+    np.testing.assert_array_equal(OP.time_union(ind), z["independent_tu"])
 
 
 @pytest.mark.parametrize("name", ["cfg1_s0", "cfg1_s01", "ragged_w", "masked", "qdefault"])
