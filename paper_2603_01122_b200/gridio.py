@@ -81,3 +81,15 @@ def load_stack(path) -> PredictionStack:
             raise ValueError(f"{path}: truncated layer data")
     spec = GridSpec(width=width, height=height, resolution=res, origin=(ox, oy))
     return PredictionStack(spec, data.reshape(steps, height, width), base_time, dt)
+
+
+def grid_to_csv(grid, path) -> None:
+    """One grid as comma-separated rows, row 0 = lowest y, 17 significant digits
+    (gridio.py:75-77) -- a round trip reproduces every float64 exactly."""
+    np.savetxt(path, np.asarray(grid.values, dtype=float), delimiter=",", fmt="%.17g")
+
+
+def grid_from_csv(path, spec: GridSpec):
+    """Inverse of grid_to_csv (gridio.py:80-82)."""
+    from .occupancy import OccupancyGrid
+    return OccupancyGrid(spec, np.loadtxt(path, delimiter=",", ndmin=2))

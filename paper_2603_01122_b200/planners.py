@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .agents import wrap_angle
+from .agents import DEFAULT_ROBOT_LIMITS, RobotControl, RobotLimits, RobotState, wrap_angle  # noqa: F401
 from .device import device, stream_handle
 from .rng import MPPI_NOISE
 
@@ -34,43 +34,6 @@ ROLLOUT_CHUNK = 256
 
 class DegenerateRolloutError(RuntimeError):
     """Every rollout cost came out non-finite."""
-
-
-@dataclass(frozen=True)
-class RobotLimits:
-    v_max: float = 1.1
-    a_max: float = 1.0
-    omega_max: float = 1.0
-
-
-DEFAULT_ROBOT_LIMITS = RobotLimits()
-
-
-@dataclass(frozen=True)
-class RobotState:
-    x: float
-    y: float
-    v: float
-    theta: float
-
-    def __post_init__(self):
-        if not all(math.isfinite(f) for f in (self.x, self.y, self.v, self.theta)):
-            raise ValueError("non-finite robot state")
-        object.__setattr__(self, "theta", wrap_angle(self.theta))
-
-    @property
-    def array(self) -> np.ndarray:
-        return np.array([self.x, self.y, self.v, self.theta], dtype=float)
-
-
-@dataclass(frozen=True)
-class RobotControl:
-    a: float
-    omega: float
-
-    @property
-    def array(self) -> np.ndarray:
-        return np.array([self.a, self.omega], dtype=float)
 
 
 @dataclass(frozen=True)

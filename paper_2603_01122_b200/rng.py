@@ -36,6 +36,14 @@ def derive_seed(seed: int, *path: int) -> int:
     return int(_lib.lib().gc_derive_seed(int(seed) & _MASK64, arr, n))
 
 
+def stream(seed: int, *path: int) -> np.random.Generator:
+    """The generator of stream (seed, *path) (rng.py:27-31): numpy's Philox4x64-10 keyed by
+    SeedSequence(seed, spawn_key=path) -- the host-side object for callers that draw from
+    a stream directly; the kernels regenerate the same streams in-register."""
+    ss = np.random.SeedSequence(entropy=int(seed) & _MASK64, spawn_key=tuple(int(p) & 0xFFFFFFFF for p in path))
+    return np.random.Generator(np.random.Philox(ss))
+
+
 def stream_f32(seed: int, path, n: int) -> np.ndarray:
     """``rng.stream(seed, *path).random(n, dtype=float32)`` computed by the C ABI."""
     arr, k = _path(path)
