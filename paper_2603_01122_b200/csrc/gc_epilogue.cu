@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
     for (int i = threadIdx.x; i < 2 * rad + 1; i += ENT) kern[i] = P.kernel[i];
 
     // load inputs (counts/n, pre-divided by the source cell's in-grid kernel masses)
+    int any = 0;
     for (int i = threadIdx.x; i < E * E; i += ENT) {
         const int ly = i / E, lx = i - ly * E;
         const int X = X0 - rad + lx, Y = Y0 - rad + ly;
@@ -83,11 +84,14 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
             if (c) {
                 v = (double)c / (double)P.n;  // exactly the reference's counts / n
                 if (rad > 0) v = v * __ldg(&P.zy[Y]) * __ldg(&P.zx[X]);  // reciprocal in-grid masses
+                any = 1;
             }
         }
         vin[i] = v;
     }
-    __syncthreads();
+    // an all-zero tile (halo included) smooths to zeros: the outputs are zero-initialised
+    // by the caller, so there is nothing to write
+    if (!__syncthreads_or(any)) return;
     if (rad > 0) {
         // pass along y: vmid[yy][lx] = sum_o k[o] vin[yy + rad - o][lx]
         for (int i = threadIdx.x; i < ET * E; i += ENT) {
