@@ -31,6 +31,10 @@ constexpr int MAXH = 128;      // max hypotheses per human
 constexpr int NBF = 24;        // headings of the factorised sampler (ControlSet.grid default)
 constexpr int NAF = 4;         // max speeds of the factorised sampler
 
+#ifndef GC_FFMA2
+#define GC_FFMA2 1  // packed FP32x2 heading loop (sm_100 FFMA2)
+#endif
+
 constexpr unsigned PHK0 = 0xA4093822u, PHK1 = 0x299F31D0u;  // production Philox key
 
 enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2, MODE_FACTS = 3 };  // FACTS: standard headings
@@ -234,6 +238,27 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     const float G3 = na > 3 ? ex2_approx(s3 - Smax) : 0.f;
     float cum[NBF];
     float C = 0.f;
+#if GC_FFMA2
+    if (!WTH) {
+        // headings in pairs on the packed FP32x2 pipe (FFMA2: two FMAs per issue slot);
+        // the running sum stays scalar so cum[] keeps the same order of additions
+        const float2 AA = make_float2(A, A), BB = make_float2(B, B), NK = make_float2(nkr, nkr);
+        const float2 g3 = make_float2(G3, G3), g2 = make_float2(G2, G2), g1 = make_float2(G1, G1);
+#pragma unroll
+        for (int b = 0; b < NBF; b += 2) {
+            // heading pairs straight from the parameter bank (64-bit constant operands)
+            const float2 cs = make_float2(P.hcos[b], P.hcos[b + 1]);
+            const float2 sn = make_float2(P.hsin[b], P.hsin[b + 1]);
+            const float2 xe = __ffma2_rn(AA, cs, __ffma2_rn(BB, sn, NK));
+            const float2 e = make_float2(ex2_approx(xe.x), ex2_approx(xe.y));
+            const float2 poly = __ffma2_rn(e, __ffma2_rn(e, g3, g2), g1);
+            C = fmaf(e.x, poly.x, C);
+            cum[b] = C;
+            C = fmaf(e.y, poly.y, C);
+            cum[b + 1] = C;
+        }
+    } else
+#endif
 #pragma unroll
     for (int b = 0; b < NBF; ++b) {
         const float cb = STDH ? kStdCos[b] : P.hcos[b];
