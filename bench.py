@@ -257,7 +257,7 @@ def run_ours(args):
     ms = max_over_ranks(ms)
     per_cycle = [a.elapsed_time(b) for a, b in cyc_ev]
     # latency percentiles over >= LAT_CYCLES cycles: extra untimed-for-value replays
-    n_lat = max(LAT_CYCLES, K)
+    n_lat = max(args.lat_cycles, K)
     extra = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_lat - K)]
     with torch.cuda.stream(stream):
         for a_, b_ in extra:
@@ -479,6 +479,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
     ap.add_argument("--no-ref-mode", action="store_true")
+    ap.add_argument("--lat-cycles", type=int, default=LAT_CYCLES,
+                    help="cycles the p50/p99 latencies are taken over (at least --steps)")
     ap.add_argument("--chunks", type=int, default=6, help="horizon chunks of the e2e cycle (D2H overlap)")
     ap.add_argument("--chunk-taper", type=float, default=0.5, help="chunk size ratio (1.0 = uniform chunks)")
     ap.add_argument("--cpu-t", type=int, default=25)

@@ -3,18 +3,21 @@
 # of the f-row kernels (collision field, MPPI, exact enumeration).  Then, here:
 #   python tools/write_profiles.py --tag rNN   (profiles/ + ncu_summary.json)
 set -x
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_bench.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+# launch list of the bench's cycle (latency percentiles over --steps only: under ncu every
+# launch is serialised and replayed, so the default 1000 latency cycles would take an hour)
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-ref-mode --lat-cycles 0"
+$B > gpurun_out/plain_bench.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    $B > gpurun_out/ncu_launch.log 2>&1
 python tools/profile_predict.py --steps 250 --cycles 3 > gpurun_out/plain_prof.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_predict|k_epilogue|k_belief" -s 3 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_predict|k_epilogue|k_belief" -s 3 -c 3 \
     -o gpurun_out/cycle_cfg3 python tools/profile_predict.py --steps 250 --cycles 3 > gpurun_out/ncu_full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
     -o gpurun_out/k2_cfg3 python tools/profile_predict.py --steps 250 --cycles 2 > gpurun_out/ncu_k2.log 2>&1
 python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/plain_ref.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
     -o gpurun_out/k2_refmode python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/ncu_ref.log 2>&1
 python tools/profile_extras.py > gpurun_out/plain_extras.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_collision|k_mppi|k_exact" -s 2 -c 6 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collision|k_mppi|k_exact" -s 2 -c 6 \
     -o gpurun_out/extras python tools/profile_extras.py > gpurun_out/ncu_extras.log 2>&1
 tail -n 2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_k2.log gpurun_out/ncu_ref.log gpurun_out/ncu_extras.log

@@ -5,7 +5,7 @@ import re
 import subprocess
 import sys
 
-KEY = ("MUFU.EX2", "MUFU.RSQ", "MUFU.RCP", "ATOMS", "REDG", "ATOMG", "VOTE", "SHFL", "BAR.SYNC", "LDS", "STS",
+KEY = ("MUFU.EX2", "MUFU.RSQ", "MUFU.RCP", "ATOMS", "REDG", "ATOMG", "VOTE", "SHFL", "BAR.SYNC", "LDS", "STS", "FFMA2",
        "DFMA", "DADD", "DMUL", "FFMA", "LDG", "STG", "UTMALDG", "UTCHMMA", "HMMA")
 
 

@@ -62,7 +62,8 @@ def main():
     shutil.copy(os.path.join(src, "launches.csv"), os.path.join(prof, f"{a.tag}_launches_cfg3.csv"))
     with open(os.path.join(prof, f"{a.tag}_launch_shares.txt"), "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 3 "
-                "--warmup 3 --no-cpu-baseline\n# (cold-cache, serialised launches: compare shares, not absolutes)\n")
+                "--warmup 3 --no-cpu-baseline --no-ref-mode --lat-cycles 0\n# (the bench's device cycles + its "
+                "chunked e2e cycles; cold-cache, serialised launches: compare shares, not absolutes)\n")
         for k, n, ms, pct in shares:
             f.write(f"{k[:60]:60s} n={n:4d} total={ms:9.3f} ms share={pct:5.1f}%\n")
     k2_share = next((p for k, n, ms, p in shares if "k_predict" in k), None)
