@@ -223,7 +223,8 @@ def update_belief(belief: JointBelief, z_t: HumanState, z_next: HumanState, dt: 
     H = len(beta_of)
     if H > 128:
         raise NotImplementedError("at most 128 hypotheses per human")
-    up = lambda a, dt_: torch.as_tensor(np.ascontiguousarray(a, dtype=dt_), device=dev)
+    # np.array copies: the belief's log weights are read-only (immutable snapshots)
+    up = lambda a, dt_: torch.as_tensor(np.array(a, dtype=dt_, order="C"), device=dev)  # noqa: E731
     d_qtable = None
     if bt.kind == _lib.GC_Q_TABLE:
         xy = np.tile(np.array([[z_t.x, z_t.y]], dtype=float), (H, 1))
