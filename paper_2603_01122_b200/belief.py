@@ -151,7 +151,7 @@ class BeliefTables:
         self.q = q
         self.control_set = control_set
         mask = q.action_mask(control_set)
-        up = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+        up = lambda a: torch.as_tensor(np.array(a, order="C"), device=dev)
         self.d_v, self.d_theta = up(v), up(th)
         self.d_masked = up(mask.astype(np.uint8)) if mask is not None else None
         if self.lq is not None:

@@ -105,7 +105,7 @@ class CycleEngine:
             goals.append(g)
             off.append(off[-1] + len(b))
         self.hyp_off = np.array(off, dtype=np.int32)
-        up = lambda a, t: torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=t)), device=dev)
+        up = lambda a, t: torch.as_tensor(np.array(a, dtype=t, order="C"), device=dev)
         self.d_hyp_off = up(self.hyp_off, np.int32)
         self.d_beta64 = up(np.concatenate(betas), np.float64)
         self.d_goal64 = up(np.concatenate(goals), np.float64)

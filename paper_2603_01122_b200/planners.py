@@ -130,7 +130,7 @@ def mppi_step(z: RobotState, nominal, goal: RobotState, stack, cfg: MppiConfig, 
     if nominal.shape != (K, 2):
         raise ValueError(f"nominal sequence must be ({K}, 2)")
     dev = device()
-    up = lambda a_, t_: torch.as_tensor(np.ascontiguousarray(np.asarray(a_, dtype=t_)), device=dev)
+    up = lambda a_, t_: torch.as_tensor(np.array(a_, dtype=t_, order="C"), device=dev)  # noqa: E731
     if blocked is None:
         blocked = blocked_mask_device(stack, cfg)
     spec = stack.spec if stack is not None else static_spec

@@ -121,7 +121,10 @@ class PredictionStack:
     @property
     def layers_device(self) -> torch.Tensor:
         if self._dev is None:
-            self._dev = torch.as_tensor(self._host, device=device())
+            import warnings
+            with warnings.catch_warnings():  # a host->device copy never writes the read-only array
+                warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+                self._dev = torch.as_tensor(self._host, device=device())
         return self._dev
 
     @property
@@ -213,7 +216,7 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
         if len(j.beta_of) > 128:
             raise NotImplementedError("at most 128 hypotheses per human")
         hyp_off[i + 1] = hyp_off[i] + len(j.beta_of)
-    up = lambda a, dt_: torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=dt_)), device=dev)
+    up = lambda a, dt_: torch.as_tensor(np.array(a, dtype=dt_, order="C"), device=dev)
     d_start = up([[np.float32(j.z0.x), np.float32(j.z0.y)] for j in jobs], np.float32)
     d_hyp_off = up(hyp_off, np.int32)
     d_beta = up(np.concatenate([j.beta_of for j in jobs]).astype(np.float32), np.float32)
@@ -337,7 +340,7 @@ def propagate_step(batch: ParticleBatch, control_set: ControlSet, q: QFunction, 
     xy = torch.as_tensor(batch.xy.copy(), device=dev)
     hyp = torch.as_tensor(batch.hypothesis_idx, device=dev)
     db = torch.as_tensor(beta_of.astype(np.float32), device=dev)
-    dg = torch.as_tensor(np.ascontiguousarray(goal_of.astype(np.float32)), device=dev)
+    dg = torch.as_tensor(np.array(goal_of, dtype=np.float32, order="C"), device=dev)
     words = _prefix_words(prefix)
     arr = (ctypes.c_uint32 * max(1, len(words)))(*words)
     _lib.check(_lib.lib().gc_propagate_step(
@@ -386,7 +389,7 @@ def predict_naive(z_history, belief: JointBelief, cfg: PredictionConfig, control
     if len(keep) == 0:
         raise EmptyControlSetError("all actions are masked")
     dev = device()
-    up = lambda a_, t_: torch.as_tensor(np.ascontiguousarray(np.asarray(a_, dtype=t_)), device=dev)  # noqa: E731
+    up = lambda a_, t_: torch.as_tensor(np.array(a_, dtype=t_, order="C"), device=dev)  # noqa: E731
     sx, sy, at, pen = f64_tables(v, th, lq)
     disp = control_set.displacements(cfg.dt)
     beta_of, goal_of = hypothesis_arrays(space)
@@ -459,7 +462,7 @@ def exact_predict(z_t: HumanState, belief: JointBelief, steps: int, dt: float, c
     if len(belief) != n_hyp:
         raise ValueError("belief size does not match hypothesis space")
     dev = device()
-    up = lambda a_, t_: torch.as_tensor(np.ascontiguousarray(np.asarray(a_, dtype=t_)), device=dev)
+    up = lambda a_, t_: torch.as_tensor(np.array(a_, dtype=t_, order="C"), device=dev)
     beta_of, goal_of = hypothesis_arrays(space)
     v, th = np.asarray(control_set.v, float), np.asarray(control_set.theta, float)
     lq = recognise_q(q)

@@ -159,7 +159,7 @@ class ActionTables:
         self.disp_np = disp
         self.max_step = float(np.max(np.abs(disp[keep]))) if len(keep) else 0.0
         sx, sy, at, pen = f32_tables(v, th, lq) if lq else (np.zeros(self.m, np.float32),) * 4
-        dev = lambda a, dt_=None: torch.as_tensor(np.ascontiguousarray(a), device=device)
+        dev = lambda a, dt_=None: torch.as_tensor(np.array(a, order="C"), device=device)
         self._keep_alive = []
         self.d_sx, self.d_sy, self.d_at, self.d_pen = dev(sx), dev(sy), dev(at), dev(pen)
         self.d_dispx = dev(disp[:, 0].copy())
@@ -250,7 +250,7 @@ class Geometry:
                     tiles.append((ti, tx, ty, 0))
         self.tile_start[steps] = len(tiles)
         self.n_tiles = len(tiles)
-        dev = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=device)
+        dev = lambda a: torch.as_tensor(np.array(a, order="C"), device=device)
         self.d_step_r = dev(self.step_r)
         self.d_step_off = dev(self.step_off)
         self.d_tiles = dev(np.asarray(tiles, dtype=np.int32))
