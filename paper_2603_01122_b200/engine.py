@@ -231,15 +231,27 @@ class CycleEngine:
         each chunk's layers are copied to it on ``copy_stream`` while later chunks compute."""
         cfg, geo, H = self.cfg, self.geo, self.n_humans
         sh = ctypes.c_void_p(stream.cuda_stream)
+        # the output fills run on a side stream concurrently with K1 (K1 occupies one warp
+        # per human; the fills are HBM-bound): fork from, and join back into, `stream`
+        u = self.unions[buf]
+        if getattr(self, "_fill_stream", None) is None:
+            self._fill_stream = torch.cuda.Stream(device=self.dev)
+        fill = self._fill_stream
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        fill.wait_event(fork)
+        with torch.cuda.stream(fill):
+            self.counts.zero_()
+            u.zero_()
+            if self.layers is not None:
+                self.layers.zero_()
+        join = torch.cuda.Event()
+        join.record(fill)
         if with_update:
             launch_belief_update(self.btab, self.d_hyp_off, self.d_beta64, self.d_goal64, self.d_obs,
                                  self.d_fallback, self.d_logw, self.d_logw, self.d_status, cfg.obs_dt,
                                  math.inf, 1, H, stream=stream)
-        self.counts.zero_()
-        u = self.unions[buf]
-        u.zero_()
-        if self.layers is not None:
-            self.layers.zero_()
+        stream.wait_event(join)
         bounds = self.chunk_bounds(chunks) if chunks > 1 else [(1, cfg.steps + 1)]
         if self.counts_reduce is not None and len(bounds) > 1:
             raise NotImplementedError("particle sharding runs the horizon in one chunk")
