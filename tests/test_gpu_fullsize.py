@@ -1,0 +1,105 @@
+"""GPU, BASELINE.json full sizes: size-independent properties of the whole cycle.
+
+The oracle cannot run these sizes in seconds, so the checks are the properties the domain
+guarantees for any size: every particle lands in exactly one cell per step (the u32 count
+windows of each (human, step) sum to n -- nothing lost or double-counted by the shared-
+memory windows, the touched-word flush or the global-atomics path), the horizon chunking
+is bit-identical to one launch, unions are finite and within [0, 1], and a stationary
+human propagates with the stationary-masked table.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_01122_b200.engine import CycleEngine, EngineConfig  # noqa: E402
+from paper_2603_01122_b200.scenario import make_scene  # noqa: E402
+
+
+def window_sums(eng):
+    """(humans, steps) sums of the windowed u32 counts."""
+    geo = eng.geo
+    c = eng.counts.cpu().numpy().view(np.uint32).astype(np.int64)
+    out = np.zeros((eng.n_humans, eng.cfg.steps), dtype=np.int64)
+    start = eng.d_start.cpu().numpy().reshape(-1, 2)
+    for h in range(eng.n_humans):
+        for t in range(eng.cfg.steps):
+            _, _, w, hh = geo.window(start[h], t)
+            base = h * geo.human_stride + geo.step_off[t]
+            out[h, t] = c[base:base + w * hh].sum()
+    return out
+
+
+def run(name, mode="production", chunks=0, humans=8, n=None, stationary=()):
+    sc = make_scene(name, cycles=2, humans=humans)
+    n = n or sc.n
+    cfg = EngineConfig(n=n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, seed=3, mode=mode)
+    eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
+    eng.prime(sc.prev_xy)
+    obs = sc.track[0].copy()
+    for i in stationary:
+        obs[i] = sc.prev_xy[i]  # did not move -> stationary-masked Q (sim.py:480, :495)
+    eng.stage(obs, buf=0)
+    if chunks > 0:
+        # capture() runs one warm-up cycle before capturing, so the replayed cycle is the
+        # second belief update -- the same for every chunk count
+        host = torch.empty(eng.unions[0].shape, dtype=eng.unions[0].dtype).pin_memory() if chunks > 1 else None
+        eng.capture(buf=0, chunks=chunks, d2h=host).replay()
+    else:
+        eng.run_cycle(buf=0)
+    torch.cuda.synchronize()
+    eng.check_errors()
+    return eng
+
+
+def test_cfg3_production_cycle_conserves_particles_and_bounds():
+    """cfg3: 8 humans x 262,144 particles x 250 steps (shared-memory window path)."""
+    eng = run("cfg3")
+    np.testing.assert_array_equal(window_sums(eng), eng.cfg.n)
+    u = eng.unions[0]
+    assert torch.isfinite(u).all() and float(u.min()) >= 0.0 and float(u.max()) <= 1.0
+    # every layer holds mass: the max union of 8 normalised layers has sum in [1, 8]
+    s = u.double().sum(dim=(1, 2)).cpu().numpy()
+    assert np.all(s > 0.99) and np.all(s < 8.01)
+
+
+@pytest.mark.parametrize("mode", ["production", "reference"])
+def test_cfg3_chunked_equals_single_launch(mode):
+    """Full-size horizon chunking (6 tapered chunks) is bit-identical to one launch."""
+    kw = dict(humans=2) if mode == "reference" else {}
+    a = run("cfg3", mode=mode, chunks=1, **kw)
+    ua = a.unions[0].cpu().numpy()
+    del a
+    b = run("cfg3", mode=mode, chunks=6, **kw)
+    np.testing.assert_array_equal(b.unions[0].cpu().numpy(), ua)
+
+
+def test_cfg4_shard_global_histogram_path_conserves_particles():
+    """cfg4's per-GPU shard (8 humans x 1,048,576 particles x 500 steps): the reachable
+    windows exceed shared memory, so K2 adds straight into the L2 count windows."""
+    eng = run("cfg4_rank")
+    np.testing.assert_array_equal(window_sums(eng), eng.cfg.n)
+    u = eng.unions[0]
+    assert torch.isfinite(u).all() and float(u.max()) <= 1.0
+
+
+def test_stationary_human_uses_masked_table_and_ragged_n():
+    """A human who did not move propagates with mask_stationary(v <= 0.5) in the same
+    launch as moving humans (per-human table ids); ragged n (partial CTA)."""
+    eng = run("cfg3", humans=3, n=3333, stationary=(1,))
+    assert list(eng.h_tid) == [0, 1, 0]
+    np.testing.assert_array_equal(window_sums(eng), 3333)
+    # with v <= 0.467 m/s the stationary human covers at most 0.467 * 5 s = 2.3 m
+    geo = eng.geo
+    c = eng.counts.cpu().numpy().view(np.uint32)
+    start = eng.d_start.cpu().numpy().reshape(-1, 2)
+    t = eng.cfg.steps - 1
+    x0, y0, w, hh = geo.window(start[1], t)
+    base = 1 * geo.human_stride + geo.step_off[t]
+    win = c[base:base + w * hh].reshape(hh, w)
+    ys, xs = np.nonzero(win)
+    cx, cy = start[1] / 0.1
+    reach = np.hypot(xs + x0 + 0.5 - cx, ys + y0 + 0.5 - cy).max() * 0.1
+    assert reach < 0.467 * eng.cfg.steps * eng.cfg.dt + 0.3
