@@ -148,19 +148,38 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
     const int mk = H.m_keep, qk = H.q_kind;
     float M = -__int_as_float(0x7f800000);
     for (int k = 0; k < mk; ++k) M = fmaxf(M, ref_logit(S, k, rx, ry, d2, beta, qk));
+    // pass 2: the sequential cumsum, remembering it at the end of each of NBLK blocks of
+    // B actions -- values of the same chain, so the search below is bit-identical to a
+    // scan from the first action but recomputes only the one block that holds r
+    constexpr int NBLK = 12;
+    const int B = (mk + NBLK - 1) / NBLK;
+    float blk[NBLK];
     float c = 0.f;
-    for (int k = 0; k < mk; ++k) {
-        const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
-        c = (k == 0) ? w : __fadd_rn(c, w);
+#pragma unroll
+    for (int j = 0; j < NBLK; ++j) {
+        const int k1 = min(mk, (j + 1) * B);
+        for (int k = j * B; k < k1; ++k) {
+            const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
+            c = (k == 0) ? w : __fadd_rn(c, w);
+        }
+        blk[j] = c;
     }
     const float r = __fmul_rn(u, c);
+    // first block whose running sum reaches r (all earlier cdf entries are < r)
+    int jb = 0;
     float cc = 0.f;
-    int k = 0;
-    for (; k < mk; ++k) {
+#pragma unroll
+    for (int j = 0; j < NBLK - 1; ++j) {
+        if (blk[j] < r) { jb = j + 1; cc = blk[j]; }
+    }
+    int k = jb * B;
+    const int kend = min(mk, (jb + 1) * B);
+    for (; k < kend; ++k) {
         const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
         cc = (k == 0) ? w : __fadd_rn(cc, w);
         if (!(cc < r)) break;
     }
+    if (k == kend && kend < mk) k = mk;  // cannot happen for a monotone chain: keep the clamp semantics
     return k < mk - 1 ? k : mk - 1;
 }
 
