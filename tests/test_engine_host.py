@@ -26,3 +26,25 @@ def test_chunk_bounds_partition_the_horizon_on_philox_phase(steps, chunks, taper
 def test_tapered_chunks_shrink_toward_the_end():
     sizes = [t1 - t0 for t0, t1 in CycleEngine.chunk_bounds(_Cfg(250, 0.5), 6)]
     assert sizes == sorted(sizes, reverse=True) and sizes[-1] <= 8 and sum(sizes) == 250
+
+
+def test_bench_reference_arm_json_contract():
+    """`bench.py --impl reference` (the driver's reference arm) prints one JSON line with the
+    contract's keys; tiny sample (1 step of one human) so it runs in seconds on CPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "3", "--ref-t", "1"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["warmup"] >= 3
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
