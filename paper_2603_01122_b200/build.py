@@ -21,6 +21,9 @@ NVCC_FLAGS = [
     # IEEE division and sqrt; the explicit __f*_rn intrinsics forbid contraction there
     "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
 ]
+# per-file extra flags: the reference-arithmetic translation unit forbids FMA contraction
+# (ptxas would fuse packed f32x2 mul+add pairs, changing numpy-exact results)
+FILE_FLAGS = {"gc_predict_ref.cu": ["--fmad=false"]}
 LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "shared"]
 
 
@@ -48,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, src]
+        cmd = [nvcc, *NVCC_FLAGS, *FILE_FLAGS.get(os.path.basename(src), []), "-c", "-o", obj, src]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd))

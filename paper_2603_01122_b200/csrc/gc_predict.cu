@@ -107,7 +107,7 @@ __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, in
 
 // MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
 // after the window and the touched list; absent from the production kernel)
-struct SmemAct {
+struct alignas(16) SmemAct {
     float ax[MAXM], ay[MAXM], aat[MAXM], adx[MAXM], ady[MAXM];
 };
 
@@ -141,26 +141,60 @@ __device__ __forceinline__ float ref_logit(const SmemAct &S, int k, float rx, fl
     return __fmul_rn(L, beta);
 }
 
+// logits of the action pair (k, k + 1), k even (8-byte aligned rows): ref_logit per lane
+__device__ __forceinline__ float2 ref_logit2(const SmemAct &S, int k, float rx, float ry, float d2, float beta,
+                                             int qk) {
+    const float2 at = *reinterpret_cast<const float2 *>(&S.aat[k]);
+    float2 L;
+    if (qk == GC_Q_DEFAULT) {
+        L = px_add(px2(-d2), make_float2(-at.x, -at.y));  // -d2 - at
+    } else {
+        const float2 ax = *reinterpret_cast<const float2 *>(&S.ax[k]);
+        const float2 ay = *reinterpret_cast<const float2 *>(&S.ay[k]);
+        L = px_fma(px2(ry), ay, px_mul(px2(rx), ax));
+        // (L * -2) - at: a contraction of this product into the add would be exact (the
+        // product by -2 is exact), so the packed pair is safe here
+        L = px_mul(L, px2(-2.0f));
+        L = px_add(L, make_float2(-at.x, -at.y));
+        if (qk == GC_Q_GOAL_PROGRESS_FULL) L = px_add(L, px2(-d2));
+    }
+    // beta * L feeds the subtraction of the max: scalar __fmul_rn, which ptxas never fuses
+    return make_float2(__fmul_rn(L.x, beta), __fmul_rn(L.y, beta));
+}
+
 __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
     const float rx = __fsub_rn(x, H.hgx[h]), ry = __fsub_rn(y, H.hgy[h]);
     const float d2 = __fadd_rn(__fmul_rn(rx, rx), __fmul_rn(ry, ry));
     const float beta = H.hb[h];
     const int mk = H.m_keep, qk = H.q_kind;
     float M = -__int_as_float(0x7f800000);
-    for (int k = 0; k < mk; ++k) M = fmaxf(M, ref_logit(S, k, rx, ry, d2, beta, qk));
+    int k = 0;
+    for (; k + 1 < mk; k += 2) {  // action pairs on the packed FP32x2 pipe
+        const float2 L = ref_logit2(S, k, rx, ry, d2, beta, qk);
+        M = fmaxf(M, fmaxf(L.x, L.y));
+    }
+    if (k < mk) M = fmaxf(M, ref_logit(S, k, rx, ry, d2, beta, qk));
     // pass 2: the sequential cumsum, remembering it at the end of each of NBLK blocks of
     // B actions -- values of the same chain, so the search below is bit-identical to a
-    // scan from the first action but recomputes only the one block that holds r
+    // scan from the first action but recomputes only the one block that holds r.  B is
+    // even so the action pairs stay 8-byte aligned; the sum itself stays sequential.
     constexpr int NBLK = 12;
-    const int B = (mk + NBLK - 1) / NBLK;
+    const int B = 2 * ((mk + 2 * NBLK - 1) / (2 * NBLK));
     float blk[NBLK];
     float c = 0.f;
 #pragma unroll
     for (int j = 0; j < NBLK; ++j) {
         const int k1 = min(mk, (j + 1) * B);
-        for (int k = j * B; k < k1; ++k) {
-            const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
-            c = (k == 0) ? w : __fadd_rn(c, w);
+        int kk = j * B;
+        for (; kk + 1 < k1; kk += 2) {
+            const float2 L = ref_logit2(S, kk, rx, ry, d2, beta, qk);
+            const float2 w = exp_np2(px_add(L, px2(-M)));
+            c = (kk == 0) ? w.x : __fadd_rn(c, w.x);
+            c = __fadd_rn(c, w.y);
+        }
+        if (kk < k1) {
+            const float w = exp_np(__fsub_rn(ref_logit(S, kk, rx, ry, d2, beta, qk), M));
+            c = (kk == 0) ? w : __fadd_rn(c, w);
         }
         blk[j] = c;
     }
@@ -172,7 +206,7 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
     for (int j = 0; j < NBLK - 1; ++j) {
         if (blk[j] < r) { jb = j + 1; cc = blk[j]; }
     }
-    int k = jb * B;
+    k = jb * B;
     const int kend = min(mk, (jb + 1) * B);
     for (; k < kend; ++k) {
         const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
@@ -619,6 +653,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     }
 }
 
+#ifdef GC_PREDICT_REF_TU
 // ---- one explicit propagate_step (prediction.py:165-211) ------------------------------
 __global__ void __launch_bounds__(NT) k_propagate_step(float *xy, const int *hyp, int n,
                                                        const float *beta32, const float *goal32,
@@ -662,6 +697,9 @@ __global__ void __launch_bounds__(NT) k_propagate_step(float *xy, const int *hyp
     xy[2 * p + 1] = __fadd_rn(y, A.ady[a]);
 }
 
+#endif  // GC_PREDICT_REF_TU
+
+#ifndef GC_PREDICT_REF_TU
 // ---- sample_hypotheses (prediction.py:124-131) ----------------------------------------
 __global__ void k_sample_hyp(const double *cdf, int n_hyp, int n, uint64_t k0, uint64_t k1, int *out) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -671,6 +709,7 @@ __global__ void k_sample_hyp(const double *cdf, int n_hyp, int n, uint64_t k0, u
     for (int i = 0; i < n_hyp; ++i) hi += (cdf[i] <= u) ? 1 : 0;
     out[p] = hi < n_hyp - 1 ? hi : n_hyp - 1;
 }
+#endif
 
 static KTable to_ktable(const gc_action_table &a) {
     KTable t;
@@ -682,7 +721,7 @@ static KTable to_ktable(const gc_action_table &a) {
 }
 
 template <int MODE, int K, bool WTH>
-static gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t st) {
+gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t st) {
     auto fn = k_predict<MODE, K, WTH>;
     static bool configured = false;  // per instantiation: raise the dynamic limit once
     if (!configured) {
@@ -693,6 +732,20 @@ static gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStr
     count_launch();
     return cuda_check(cudaGetLastError(), "k_predict launch");
 }
+
+// The reference-arithmetic kernels (MODE_REF, k_propagate_step) are compiled in their own
+// translation unit, gc_predict_ref.cu, with --fmad=false: ptxas otherwise contracts a
+// packed mul.rn.f32x2 feeding an add.rn.f32x2 into one FFMA2 (single rounding), which
+// would break numpy's bit-exact arithmetic; the production kernels keep contraction.
+#ifdef GC_PREDICT_REF_TU
+template gc_status launch_predict<MODE_REF, 1, false>(const KParams &, int, size_t, cudaStream_t);
+template gc_status launch_predict<MODE_REF, 2, false>(const KParams &, int, size_t, cudaStream_t);
+template gc_status launch_predict<MODE_REF, 4, false>(const KParams &, int, size_t, cudaStream_t);
+#else
+extern template gc_status launch_predict<MODE_REF, 1, false>(const KParams &, int, size_t, cudaStream_t);
+extern template gc_status launch_predict<MODE_REF, 2, false>(const KParams &, int, size_t, cudaStream_t);
+extern template gc_status launch_predict<MODE_REF, 4, false>(const KParams &, int, size_t, cudaStream_t);
+#endif
 
 template <int MODE, bool WTH>
 static gc_status dispatch_k(const KParams &P, int K, int grid, size_t smem, cudaStream_t st) {
@@ -707,6 +760,7 @@ static gc_status dispatch_k(const KParams &P, int K, int grid, size_t smem, cuda
 
 using namespace gc;
 
+#ifndef GC_PREDICT_REF_TU
 extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     GC_CHECK_ARG(a != nullptr, "gc_predict: null args");
     GC_CHECK_ARG(a->n_humans >= 1 && a->n >= 1 && a->steps >= 1, "gc_predict: need n_humans, n, steps >= 1");
@@ -792,7 +846,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     // GC_PREDICT_GLOBAL_HIST=1 forces direct global reductions (tuning knob)
     static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();
     P.smem_window = (win_bytes <= 64 * 1024 && !force_global) ? 1 : 0;
-    P.act_off = P.smem_window ? (int)win_bytes : 0;
+    P.act_off = P.smem_window ? (int)((win_bytes + 15) & ~(size_t)15) : 0;  // 16-byte aligned rows
     const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;
     const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : 0);
     cudaStream_t st = (cudaStream_t)stream;
@@ -812,6 +866,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     return dispatch_k<MODE_GEN, false>(P, K, (int)grid, smem, st);
 }
 
+#else
 extern "C" gc_status gc_propagate_step(float *d_xy, const int32_t *d_hyp, int32_t n, const float *d_beta32,
                                        const float *d_goal32, int32_t n_hyp, const gc_action_table *h_table,
                                        const float *d_u01, uint64_t seed, const uint32_t *h_prefix,
@@ -830,6 +885,9 @@ extern "C" gc_status gc_propagate_step(float *d_xy, const int32_t *d_hyp, int32_
     return cuda_check(cudaGetLastError(), "k_propagate_step launch");
 }
 
+#endif  // GC_PREDICT_REF_TU
+
+#ifndef GC_PREDICT_REF_TU
 extern "C" gc_status gc_sample_hypotheses(const double *d_cdf, int32_t n_hyp, int32_t n, uint64_t seed,
                                           const uint32_t *h_prefix, int32_t prefix_len, int32_t *d_out,
                                           void *stream) {
@@ -843,3 +901,4 @@ extern "C" gc_status gc_sample_hypotheses(const double *d_cdf, int32_t n_hyp, in
     count_launch();
     return cuda_check(cudaGetLastError(), "k_sample_hyp launch");
 }
+#endif  // GC_PREDICT_REF_TU
