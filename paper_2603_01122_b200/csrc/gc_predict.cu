@@ -218,27 +218,67 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
 }
 
 // ---- production generic per-action softmax ------------------------------------------
+// logits (log2 units) of the action pair (k, k + 1), k even, on the packed FP32x2 pipe
+__device__ __forceinline__ float2 gen_logit2(const SmemAct &S, int k, float rx, float ry, float d2, float bl,
+                                             int qk) {
+    const float2 at = *reinterpret_cast<const float2 *>(&S.aat[k]);
+    float2 q;
+    if (qk == GC_Q_DEFAULT) {
+        q = __fadd2_rn(make_float2(-d2, -d2), make_float2(-at.x, -at.y));
+    } else {
+        const float2 ax = *reinterpret_cast<const float2 *>(&S.ax[k]);
+        const float2 ay = *reinterpret_cast<const float2 *>(&S.ay[k]);
+        const float2 t = __ffma2_rn(make_float2(ry, ry), ay, __fmul2_rn(make_float2(rx, rx), ax));
+        q = __ffma2_rn(make_float2(-2.f, -2.f), t, make_float2(-at.x, -at.y));
+    }
+    return __fmul2_rn(q, make_float2(bl, bl));
+}
+
+// exact-in-distribution softmax sample over any control set: max pass, one pass of the
+// running sum that keeps it at 12 block ends, then only the block holding r is rescanned.
+// The action tables are padded to an even count (pairs), padded weights are not summed.
 __device__ __forceinline__ int gen_pick(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
     const float rx = x - H.hgx[h], ry = y - H.hgy[h];
     const float d2 = fmaf(rx, rx, ry * ry);
     const float bl = H.hb[h] * 1.4426950408889634f;
     const int mk = H.m_keep, qk = H.q_kind;
-    auto L = [&](int k) {
-        float q;
-        if (qk == GC_Q_DEFAULT) q = -d2 - S.aat[k];
-        else q = fmaf(-2.f, fmaf(ry, S.ay[k], rx * S.ax[k]), -S.aat[k]);
-        return q * bl;
-    };
     float M = -__int_as_float(0x7f800000);
-    for (int k = 0; k < mk; ++k) M = fmaxf(M, L(k));
-    float W = 0.f;
-    for (int k = 0; k < mk; ++k) W += ex2_approx(L(k) - M);
-    const float r = u * W;
+    for (int k = 0; k < mk; k += 2) {
+        const float2 L = gen_logit2(S, k, rx, ry, d2, bl, qk);
+        M = fmaxf(M, k + 1 < mk ? fmaxf(L.x, L.y) : L.x);
+    }
+    constexpr int NBLK = 12;
+    const int B = 2 * ((mk + 2 * NBLK - 1) / (2 * NBLK));
+    float blk[NBLK];
     float c = 0.f;
-    int k = 0;
-    for (; k < mk; ++k) {
-        c += ex2_approx(L(k) - M);
-        if (c > r) break;
+#pragma unroll
+    for (int j = 0; j < NBLK; ++j) {
+        const int k1 = min(mk, (j + 1) * B);
+        for (int k = j * B; k < k1; k += 2) {
+            const float2 L = gen_logit2(S, k, rx, ry, d2, bl, qk);
+            c += ex2_approx(L.x - M);
+            if (k + 1 < k1) c += ex2_approx(L.y - M);
+        }
+        blk[j] = c;
+    }
+    const float r = u * c;
+    // first action whose running sum exceeds r: skip the blocks that end at or below r
+    int jb = 0;
+    float cc = 0.f;
+#pragma unroll
+    for (int j = 0; j < NBLK - 1; ++j) {
+        if (blk[j] <= r) { jb = j + 1; cc = blk[j]; }
+    }
+    const int k1 = min(mk, (jb + 1) * B);
+    int k = jb * B;
+    for (; k < k1; k += 2) {
+        const float2 L = gen_logit2(S, k, rx, ry, d2, bl, qk);
+        cc += ex2_approx(L.x - M);
+        if (cc > r) break;
+        if (k + 1 < k1) {
+            cc += ex2_approx(L.y - M);
+            if (cc > r) { ++k; break; }
+        }
     }
     return k < mk - 1 ? k : mk - 1;
 }
