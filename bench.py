@@ -187,7 +187,10 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    # --force-dist: run the multi-GPU code path (NCCL process group, fused reduce) even
+    # at world size 1 -- a one-rank smoke test of the N > 1 branch on a single GPU
+    distributed = world > 1 or args.force_dist
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2603_01122_b200 import _lib
     from paper_2603_01122_b200.engine import CycleEngine, EngineConfig, fused_reduce
@@ -206,15 +209,15 @@ def run_ours(args):
         eng.run_cycle(buf=k % 2)
     torch.cuda.synchronize()
     eng.check_errors()
-    fused = world > 1 and not args.no_fused
+    fused = distributed and not args.no_fused
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if world == 1:
+        if not distributed:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -463,7 +466,7 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_sample(scene, t_steps=args.cpu_t, reps=3)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
     return 0
 
@@ -478,6 +481,8 @@ def main():
     ap.add_argument("--mode", default="production", choices=["production", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="take the multi-GPU path (NCCL group, fused reduce) even with one rank")
     ap.add_argument("--no-ref-mode", action="store_true")
     ap.add_argument("--lat-cycles", type=int, default=LAT_CYCLES,
                     help="cycles the p50/p99 latencies are taken over (at least --steps)")
