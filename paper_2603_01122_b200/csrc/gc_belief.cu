@@ -1,4 +1,5 @@
-// gc_belief.cu -- K1: Bayesian (beta, goal) belief update, one warp per human.
+// gc_belief.cu -- K1: Bayesian (beta, goal) belief update, one CTA per human (its warps
+// share the hypotheses).
 //
 // Restates update_belief (belief.py:159-198) in float64:
 //   recover_control (agents.py:355-371): v = |dz|/dt, theta = atan2 (fallback if |dz|<1e-6),
@@ -16,7 +17,7 @@
 
 namespace gc {
 
-constexpr int BT = 128;      // 4 humans per CTA
+constexpr int BT = 256;      // one CTA (8 warps) per human
 constexpr int BMAXH = 128;   // hypotheses per human (4 per lane)
 
 struct BParams {
@@ -47,11 +48,16 @@ __device__ __forceinline__ double wrap_angle(double th) {
 }
 
 __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
-    const int h = (blockIdx.x * BT + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (h >= P.n_humans) return;
+    // one CTA per human: every warp recovers/snaps the control (identical results), then
+    // warp w takes hypotheses w, w + NW, ...; warp 0 normalises from shared memory
+    __shared__ double spost[BMAXH];
+    __shared__ int sempty;
+    const int h = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = BT / 32;
     const double PI = 3.141592653589793, TWO_PI = 6.283185307179586;
     const double NEG_INF = -__longlong_as_double(0x7ff0000000000000ll);
+    if (threadIdx.x == 0) sempty = 0;
 
     // ---- recover_control ----
     const double zx = P.obs[4 * h], zy = P.obs[4 * h + 1];
@@ -77,19 +83,13 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
     int status = GC_OK;
     if (best > P.snap_tol) {
         status = GC_SNAP_MISMATCH;
-        if (!P.clamp) {
-            if (lane == 0) { P.status[h] = status; if (P.action) P.action[h] = bidx; }
+        if (!P.clamp) {  // uniform over the CTA: every warp takes this branch
+            if (threadIdx.x == 0) { P.status[h] = status; if (P.action) P.action[h] = bidx; }
             return;
         }
     }
     const int idx = bidx;
-
-    // ---- per-hypothesis log-likelihood: lanes over actions, warp-shuffle max / sum ----
     const int h0 = P.hyp_off[h], nh = P.hyp_off[h + 1] - h0;
-    double post[BMAXH / 32];
-#pragma unroll
-    for (int s = 0; s < BMAXH / 32; ++s) post[s] = NEG_INF;
-    bool empty = false;
     // per-action tables of this lane's actions, loaded once (<= 8 per lane)
     double ax[8], ay[8], aat[8];
     bool amask[8];
@@ -102,49 +102,42 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
         ay[s] = ok ? P.sy[j] : 0.0;
         aat[s] = ok ? (P.q_kind == GC_Q_DEFAULT ? P.pen[j] : P.at[j]) : 0.0;
     }
-    // hypothesis parameters: lane i%32 loads hypothesis i, broadcast by shuffle
-    double hb_l[BMAXH / 32], hgx_l[BMAXH / 32], hgy_l[BMAXH / 32];
-#pragma unroll
-    for (int s = 0; s < BMAXH / 32; ++s) {
-        const int i = lane + 32 * s;
-        hb_l[s] = i < nh ? P.beta[h0 + i] : 0.0;
-        hgx_l[s] = i < nh ? P.goal[2 * (h0 + i)] : 0.0;
-        hgy_l[s] = i < nh ? P.goal[2 * (h0 + i) + 1] : 0.0;
-    }
-    for (int i = 0; i < nh; ++i) {
-        double b_s = 0.0, gx_s = 0.0, gy_s = 0.0;
-#pragma unroll
-        for (int s = 0; s < BMAXH / 32; ++s)
-            if (s == (i >> 5)) { b_s = hb_l[s]; gx_s = hgx_l[s]; gy_s = hgy_l[s]; }
-        const double beta = __shfl_sync(0xffffffffu, b_s, i & 31);
-        const double rx = zx - __shfl_sync(0xffffffffu, gx_s, i & 31);
-        const double ry = zy - __shfl_sync(0xffffffffu, gy_s, i & 31);
+    __syncthreads();  // sempty initialised
+
+    // ---- per-hypothesis log-likelihood: lanes over actions, warp-shuffle max / sum ----
+    for (int i = warp; i < nh; i += NW) {
+        const double beta = P.beta[h0 + i];
+        const double rx = zx - P.goal[2 * (h0 + i)];
+        const double ry = zy - P.goal[2 * (h0 + i) + 1];
         const double d2 = __dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry));
-        auto logit_s = [&](int s, int j) -> double {
-            if (amask[s]) return NEG_INF;
-            double q;
-            if (P.q_kind == GC_Q_TABLE) {
-                q = P.qtable[(long long)(h0 + i) * P.m + j];
-            } else if (P.q_kind == GC_Q_DEFAULT) {
-                q = __dsub_rn(-d2, aat[s]);
-            } else {
-                q = __dmul_rn(__fma_rn(ry, ay[s], __dmul_rn(rx, ax[s])), -2.0);
-                q = __dsub_rn(q, aat[s]);
-                q = __dsub_rn(q, d2);
-            }
-            return __dmul_rn(beta, q);
-        };
         double Lj[8];  // m <= 256 actions: 8 per lane
         double mx = NEG_INF;
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
             const int j = lane + 32 * s;
-            Lj[s] = logit_s(s, j);
-            mx = fmax(mx, Lj[s]);
+            double L = NEG_INF;
+            if (!amask[s]) {
+                double q;
+                if (P.q_kind == GC_Q_TABLE) {
+                    q = P.qtable[(long long)(h0 + i) * P.m + j];
+                } else if (P.q_kind == GC_Q_DEFAULT) {
+                    q = __dsub_rn(-d2, aat[s]);
+                } else {
+                    q = __dmul_rn(__fma_rn(ry, ay[s], __dmul_rn(rx, ax[s])), -2.0);
+                    q = __dsub_rn(q, aat[s]);
+                    q = __dsub_rn(q, d2);
+                }
+                L = __dmul_rn(beta, q);
+            }
+            Lj[s] = L;
+            mx = fmax(mx, L);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (!(mx > NEG_INF)) { empty = true; break; }
+        if (!(mx > NEG_INF)) {
+            if (lane == 0) sempty = 1;
+            continue;
+        }
         double ssum = 0.0;
 #pragma unroll
         for (int s = 0; s < 8; ++s) if (Lj[s] > NEG_INF) ssum += exp(Lj[s] - mx);
@@ -156,18 +149,24 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
         for (int s = 0; s < 8; ++s) if (s == (idx >> 5)) Lmine = Lj[s];
         const double Li = __shfl_sync(0xffffffffu, Lmine, idx & 31);
         const double ll = (Li > NEG_INF) ? (Li - mx) - log(ssum) : NEG_INF;
-        if (lane == (i & 31)) {
+        if (lane == 0) {
             const double pr = P.prior[h0 + i];
-            const double v = (pr == NEG_INF) ? NEG_INF : fmax(pr + ll, -745.0);  // LOG_WEIGHT_FLOOR
-#pragma unroll
-            for (int s = 0; s < BMAXH / 32; ++s) if (s == (i >> 5)) post[s] = v;
+            spost[i] = (pr == NEG_INF) ? NEG_INF : fmax(pr + ll, -745.0);  // LOG_WEIGHT_FLOOR
         }
     }
-    if (__any_sync(0xffffffffu, empty)) {
+    __syncthreads();
+    if (warp != 0) return;
+    if (sempty) {
         if (lane == 0) P.status[h] = GC_EMPTY_CONTROL_SET;
         return;
     }
     // ---- logsumexp over hypotheses ----
+    double post[BMAXH / 32];
+#pragma unroll
+    for (int s = 0; s < BMAXH / 32; ++s) {
+        const int i = lane + 32 * s;
+        post[s] = i < nh ? spost[i] : NEG_INF;
+    }
     double mx = NEG_INF;
 #pragma unroll
     for (int s = 0; s < BMAXH / 32; ++s) mx = fmax(mx, post[s]);
@@ -209,8 +208,7 @@ extern "C" gc_status gc_belief_update(const gc_belief_args *a, void *stream) {
     P.beta = a->d_beta; P.goal = a->d_goal; P.obs = a->d_obs; P.fallback = a->d_fallback_theta;
     P.dt = a->dt; P.snap_tol = a->snap_tol; P.prior = a->d_prior; P.post = a->d_post;
     P.status = a->d_status; P.action = a->d_action;
-    const int blocks = (a->n_humans * 32 + BT - 1) / BT;
-    k_belief<<<blocks, BT, 0, (cudaStream_t)stream>>>(P);
+    k_belief<<<a->n_humans, BT, 0, (cudaStream_t)stream>>>(P);
     count_launch();
     return cuda_check(cudaGetLastError(), "k_belief launch");
 }
