@@ -103,3 +103,35 @@ def test_stationary_human_uses_masked_table_and_ragged_n():
     cx, cy = start[1] / 0.1
     reach = np.hypot(xs + x0 + 0.5 - cx, ys + y0 + 0.5 - cy).max() * 0.1
     assert reach < 0.467 * eng.cfg.steps * eng.cfg.dt + 0.3
+
+
+def test_cfg3_production_tv_within_reference_seed_spread():
+    """The north star's production-mode criterion at the headline size: per (human, step)
+    layers of the production sampler vs the bit-exact reference mode on the same inputs,
+    TV bounded by the reference's own seed-to-seed TV (1.5x + 0.005), all 8 x 250 layers."""
+    sc = make_scene("cfg3", cycles=2, humans=8)
+    layers = {}
+    for tag, seed, mode in (("a", 1, "reference"), ("b", 2, "reference"), ("p", 3, "production")):
+        cfg = EngineConfig(n=sc.n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, seed=seed, mode=mode,
+                           per_human_layers=True)
+        eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
+        eng.prime(sc.prev_xy)
+        eng.stage(sc.track[0], buf=0)
+        eng.run_cycle(buf=0)
+        torch.cuda.synchronize()
+        eng.check_errors()
+        layers[tag] = eng.layers.clone()
+        del eng
+        torch.cuda.empty_cache()
+
+    def tv(u, v):  # (humans, steps) total variation
+        return 0.5 * (u - v).abs().sum(dim=(2, 3))
+
+    spread = tv(layers["a"], layers["b"])
+    got = torch.maximum(tv(layers["p"], layers["a"]), tv(layers["p"], layers["b"]))
+    print(f"cfg3 per-layer TV: production vs reference max {float(got.max()):.4f} mean {float(got.mean()):.4f}; "
+          f"reference seed spread max {float(spread.max()):.4f} mean {float(spread.mean()):.4f}")
+    assert bool((got <= 1.5 * spread + 0.005).all()), (float(got.max()), float(spread.max()))
+    # and every layer is a probability distribution
+    mass = layers["p"].sum(dim=(2, 3))
+    assert float((mass - 1).abs().max()) < 1e-9
