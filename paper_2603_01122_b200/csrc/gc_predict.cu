@@ -112,15 +112,16 @@ struct alignas(16) SmemAct {
 };
 
 struct SmemTabs {
-    // production: (goal x, goal y, k log2e, c log2e) per hypothesis -- one LDS.128
+    // production: (goal x, goal y, k log2e, c log2e) per hypothesis -- one LDS.128;
+    // MODE_FACTS: (goal x, goal y, k log2e, Ka) and hq = (Kb, Kc, c log2e, sum_b H_b)
     float4 hp[MAXH];
+    float4 hq[MAXH];
     // production: displacement of (a, b) and heading (cos, sin) -- one LDS.64 each
     float2 fd[NAF * NBF];
     float2 hcs[NBF];
     // hypotheses of this CTA's human
     double cdf[MAXH];
     float hb[MAXH], hgx[MAXH], hgy[MAXH];
-    float hsumH[MAXH];
     int list_n[2];
     int n_hyp, m_keep, q_kind, n_speeds;
     float wth;
@@ -364,7 +365,7 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
         else C = fmaf(e, poly, C);
         cum[b] = C;
     }
-    const float Z0 = G0 * S.hsumH[h];
+    const float Z0 = G0 * S.hq[h].w;
     const float rr = u1 * (Z0 + C);
     const float t = rr - Z0;
     // heading = #{b : cum_b <= t}: cum is monotone, so halve the candidate set with one
@@ -414,6 +415,117 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     y += d.y;
 }
 
+// MODE_FACTS (standard heading set, n_speeds <= 4, w_th = 0): the factorised sampler with
+//  (1) speed weights normalised at the TOP speed instead of by a max shift: with
+//      Q = 2^-kr, G_a / G_top = Q^(top-a) 2^(c (top^2 - a^2)), so one ex2 (Q) and a few
+//      products replace 4 ex2; the per-hypothesis powers of 2^c (Ka, Kb, Kc) are staged
+//      in the prologue, and a CTA whose constants would overflow (c > ~11 at 4 speeds,
+//      i.e. beta > ~140 with the default tables) keeps the max-shift form (qg = false);
+//  (2) opposite headings b and b + 12 (theta + pi) in one go: x_{b+12} = -x_b - 2kr, so
+//      heading pair (b, b+1) costs two FFMA2 and the opposite pair one.  The cumulative
+//      sum runs in the order (0, 1, 12, 13, 2, 3, 14, 15, ...): index i <-> heading
+//      2(i>>2) + (i&1) + 12((i>>1)&1); the prologue stores the chosen-heading (cos, sin) and
+//      the displacements in that order, so the search result indexes them directly.
+__device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &P, float &x, float &y,
+                                              int h, float u1, bool qg) {
+    const float4 hp = S.hp[h];
+    const float4 hq = S.hq[h];
+    const float rx = x - hp.x, ry = y - hp.y;
+    const float r2 = fmaf(rx, rx, ry * ry);
+    float rs;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(r2, 1e-30f)));
+    const float r = r2 * rs;
+    const float kk = hp.z;
+    const float kr = kk * r;
+    const float A = -kk * rx, B = -kk * ry, nkr = -kr;
+    const int na = S.n_speeds;
+    float G1, G2, G3, Z0;
+    if (qg) {
+        const float Q = ex2_approx(nkr), Q2 = Q * Q;
+        if (na == 4) {
+            G3 = 1.f; G2 = Q * hp.w; G1 = Q2 * hq.x; Z0 = Q2 * Q * hq.y;
+        } else if (na == 3) {
+            G3 = 0.f; G2 = 1.f; G1 = Q * hp.w; Z0 = Q2 * hq.x;
+        } else {
+            G3 = 0.f; G2 = 0.f; G1 = 1.f; Z0 = Q * hp.w;
+        }
+    } else {
+        const float c2 = hq.z;
+        const float s1 = kr - c2, s2 = fmaf(2.f, kr, -4.f * c2), s3 = fmaf(3.f, kr, -9.f * c2);
+        float Smax = fmaxf(0.f, s1);
+        if (na > 2) Smax = fmaxf(Smax, s2);
+        if (na > 3) Smax = fmaxf(Smax, s3);
+        Z0 = ex2_approx(-Smax) * hq.w;
+        G1 = ex2_approx(s1 - Smax);
+        G2 = na > 2 ? ex2_approx(s2 - Smax) : 0.f;
+        G3 = na > 3 ? ex2_approx(s3 - Smax) : 0.f;
+    }
+    float cum[NBF];
+    float C = 0.f;
+    {
+        const float2 AA = make_float2(A, A), BB = make_float2(B, B), NK = make_float2(nkr, nkr);
+        const float2 NK2 = make_float2(2.f * nkr, 2.f * nkr), M1 = make_float2(-1.f, -1.f);
+        const float2 g3 = make_float2(G3, G3), g2 = make_float2(G2, G2), g1 = make_float2(G1, G1);
+#pragma unroll
+        for (int j = 0; j < NBF / 4; ++j) {
+            const float2 cs = make_float2(P.hcos[2 * j], P.hcos[2 * j + 1]);
+            const float2 sn = make_float2(P.hsin[2 * j], P.hsin[2 * j + 1]);
+            const float2 xe = __ffma2_rn(AA, cs, __ffma2_rn(BB, sn, NK));
+            const float2 xo = __ffma2_rn(xe, M1, NK2);  // headings 2j + 12, 2j + 13
+            const float2 e = make_float2(ex2_approx(xe.x), ex2_approx(xe.y));
+            const float2 eo = make_float2(ex2_approx(xo.x), ex2_approx(xo.y));
+            const float2 poly = __ffma2_rn(e, __ffma2_rn(e, g3, g2), g1);
+            const float2 polyo = __ffma2_rn(eo, __ffma2_rn(eo, g3, g2), g1);
+            C = fmaf(e.x, poly.x, C);
+            cum[4 * j] = C;
+            C = fmaf(e.y, poly.y, C);
+            cum[4 * j + 1] = C;
+            C = fmaf(eo.x, polyo.x, C);
+            cum[4 * j + 2] = C;
+            C = fmaf(eo.y, polyo.y, C);
+            cum[4 * j + 3] = C;
+        }
+    }
+    const float rr = u1 * (Z0 + C);
+    const float t = rr - Z0;
+    int b = 0;
+    float lo = 0.f;
+    {
+        bool p = cum[11] <= t;
+        b += p ? 12 : 0;
+        lo = p ? cum[11] : lo;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) cum[i] = p ? cum[i + 12] : cum[i];
+        p = cum[5] <= t;
+        b += p ? 6 : 0;
+        lo = p ? cum[5] : lo;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) cum[i] = p ? cum[i + 6] : cum[i];
+        p = cum[2] <= t;
+        b += p ? 3 : 0;
+        lo = p ? cum[2] : lo;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) cum[i] = p ? cum[i + 3] : cum[i];
+        const bool p0 = cum[0] <= t, p1 = cum[1] <= t, p2 = cum[2] <= t;
+        b += (p0 ? 1 : 0) + (p1 ? 1 : 0) + (p2 ? 1 : 0);
+        lo = p2 ? cum[2] : (p1 ? cum[1] : (p0 ? cum[0] : lo));
+    }
+    b = b < NBF - 1 ? b : NBF - 1;  // b is the cumulative-order index i
+    // the chosen heading's e exactly as the loop computed it (same FMAs, same lanes)
+    const float2 cs = S.hcs[b];  // forward (cos, sin) of heading 2(i>>2) + (i&1)
+    float xb = fmaf(A, cs.x, fmaf(B, cs.y, nkr));
+    if (b & 2) xb = fmaf(xb, -1.f, 2.f * nkr);
+    const float e = ex2_approx(xb);
+    const float w1 = G1 * e, w2 = G2 * e * e;
+    const float res = t - lo;
+    int a = 1 + ((w1 <= res) ? 1 : 0) + ((w1 + w2 <= res) ? 1 : 0);
+    a = a < na - 1 ? a : na - 1;
+    a = (rr < Z0) ? 0 : a;  // stay: row 0 of fd is (0, 0)
+    const float2 d = S.fd[a * NBF + b];
+    x += d.x;
+    y += d.y;
+}
+
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
 // particles, so a per-CTA cell count cannot overflow its half-word)
 template <int MODE, int K, bool WTH>
@@ -447,14 +559,22 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             A.ady[k] = __ldg(&T.dispy[j]);
         }
     } else {
-        for (int i = tid; i < NBF; i += NT) S.hcs[i] = make_float2(P.hcos[i], P.hsin[i]);
+        // MODE_FACTS stores headings in the cumulative order of fact_step_sym (slot i holds
+        // heading 2(i>>2) + (i&1) + 12((i>>1)&1); its (cos, sin) slot the forward heading's)
+        auto hslot = [](int i) { return MODE == MODE_FACTS ? 2 * (i >> 2) + (i & 1) + 12 * ((i >> 1) & 1) : i; };
+        for (int i = tid; i < NBF; i += NT) {
+            const int f = MODE == MODE_FACTS ? 2 * (i >> 2) + (i & 1) : i;
+            S.hcs[i] = make_float2(P.hcos[f], P.hsin[f]);
+        }
         for (int i = tid; i < NAF * NBF; i += NT) {
             const int a = i / NBF;
-            const int j = (a > 0 && a < T.n_speeds) ? __ldg(&T.a_index[i]) : -1;  // a = 0: stay
+            const int ib = a * NBF + hslot(i - a * NBF);
+            const int j = (a > 0 && a < T.n_speeds) ? __ldg(&T.a_index[ib]) : -1;  // a = 0: stay
             S.fd[i] = j >= 0 ? make_float2(__fdiv_rn(__ldg(&T.dispx[j]), P.res), __fdiv_rn(__ldg(&T.dispy[j]), P.res))
                              : make_float2(0.f, 0.f);
         }
     }
+    bool qg_ok = true;  // MODE_FACTS: top-speed normalisation representable for every hypothesis
     for (int i = tid; i < nh; i += NT) {
         const float b = __ldg(&P.beta32[h0 + i]);
         S.hb[i] = b;
@@ -468,7 +588,19 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             float sh = 0.f;
             for (int q = 0; q < T.n_headings; ++q)
                 sh += (T.w_th != 0.f) ? exp2f(-T.w_th * b * P.hth2[q] * L2E) : 1.f;
-            S.hsumH[i] = sh;
+            S.hq[i] = make_float4(0.f, 0.f, S.hp[i].w, sh);
+            if (MODE == MODE_FACTS) {
+                // speed weights relative to the top speed (fact_step_sym): powers of 2^c
+                const double c = S.hp[i].w;
+                const int top = T.n_speeds - 1;
+                const double ka = top == 3 ? exp2(5.0 * c) : (top == 2 ? exp2(3.0 * c) : sh * exp2(c));
+                const double kb = top == 3 ? exp2(8.0 * c) : (top == 2 ? sh * exp2(4.0 * c) : 0.0);
+                const double kc = top == 3 ? sh * exp2(9.0 * c) : 0.0;
+                qg_ok = qg_ok && ka < 0x1p100 && kb < 0x1p100 && kc < 0x1p100;
+                S.hp[i].w = (float)ka;
+                S.hq[i].x = (float)kb;
+                S.hq[i].y = (float)kc;
+            }
         }
     }
     if (tid == 0) {
@@ -489,7 +621,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         list = reinterpret_cast<int *>(win + ((words + 3) & ~3));
         if (tid == 0) { S.list_n[0] = 0; S.list_n[1] = 0; }
     }
-    __syncthreads();
+    const bool qg = __syncthreads_and(qg_ok) != 0;
 
     // ---- particles: hypothesis draw + start state ----
     const float sx0 = __ldg(&P.start_xy[2 * h]), sy0 = __ldg(&P.start_xy[2 * h + 1]);
@@ -584,8 +716,10 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 } else {
                     ua = r1[k]; r1[k] = r2[k]; r2[k] = r3[k];
                 }
-                if (MODE == MODE_FACT || MODE == MODE_FACTS) {
-                    fact_step<MODE == MODE_FACTS, WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
+                if (MODE == MODE_FACTS) {
+                    fact_step_sym(S, P, x, y, S.phyp[k * NT + tid], u24(ua), qg);
+                } else if (MODE == MODE_FACT) {
+                    fact_step<false, WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
                     const int a = gen_pick(S, A, x, y, S.phyp[k * NT + tid], u24(ua));
                     x += A.adx[a];
@@ -898,7 +1032,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     for (int i = 0; i < a->n_tables; ++i) wth = wth || a->h_tables[i].w_th != 0.f;
     if (mode == MODE_REF) return dispatch_k<MODE_REF, false>(P, K, (int)grid, smem, st);
     if (mode == MODE_FACTS)
-        return wth ? dispatch_k<MODE_FACTS, true>(P, K, (int)grid, smem, st)
+        return wth ? dispatch_k<MODE_FACT, true>(P, K, (int)grid, smem, st)  // w_th != 0: per-heading H_b
                    : dispatch_k<MODE_FACTS, false>(P, K, (int)grid, smem, st);
     if (mode == MODE_FACT)
         return wth ? dispatch_k<MODE_FACT, true>(P, K, (int)grid, smem, st)
