@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -200,8 +201,15 @@ def run_ours(args):
     scene = make_scene(args.config, cycles=W + K + 4, humans=8, human_offset=8 * rank)
     cfg = EngineConfig(n=scene.n, steps=scene.steps, dt=scene.dt, smoothing_sigma=0.1, seed=0,
                        mode=args.mode, time_union=False, chunk_taper=args.chunk_taper)
+    fused = distributed and not args.no_fused
+    # fused grid: NCCL max-reduce of the per-rank unions (engine.fused_reduce), or every
+    # rank's K3 writing rank 0's grid over NVLink peer memory (peer.PeerUnion)
+    peer = None
+    if fused and args.fused_path == "peer":
+        from paper_2603_01122_b200.peer import PeerUnion
+        peer = PeerUnion((scene.steps, scene.spec.height, scene.spec.width), torch.float32)
     eng = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec, cfg,
-                      human_ids=list(range(8 * rank, 8 * rank + len(scene.spaces))))
+                      human_ids=list(range(8 * rank, 8 * rank + len(scene.spaces))), peer=peer)
     # posterior after 10 observations (also warms every kernel)
     eng.prime(scene.warmup_track[0])
     for k in range(1, 11):
@@ -209,7 +217,18 @@ def run_ours(args):
         eng.run_cycle(buf=k % 2)
     torch.cuda.synchronize()
     eng.check_errors()
-    fused = distributed and not args.no_fused
+
+    def device_cycle(g, b=0):
+        """One graph-replayed cycle plus the fused-grid merge (on the current stream)."""
+        if peer is not None:
+            peer.zero(b)
+            peer.barrier()
+            g.replay()
+            peer.barrier()
+        else:
+            g.replay()
+            if fused:
+                fused_reduce(eng.unions[b], dst=0)
 
     def barrier():
         if distributed:
@@ -230,6 +249,7 @@ def run_ours(args):
     for i in range(n_k):
         eng.run_cycle(buf=0, with_h2d=False, stream=stream, events=ev[i])
     stream.synchronize()
+    barrier()
     k2_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     k3_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
 
@@ -238,9 +258,7 @@ def run_ours(args):
     cyc_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     with torch.cuda.stream(stream):
         for _ in range(W):
-            g.replay()
-            if fused:
-                fused_reduce(eng.unions[0], dst=0)
+            device_cycle(g)
     launches0 = _lib.lib().gc_launch_count()
     barrier()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -250,9 +268,7 @@ def run_ours(args):
             t_start.record(stream)
             for i in range(K):
                 cyc_ev[i][0].record(stream)
-                g.replay()
-                if fused:
-                    fused_reduce(eng.unions[0], dst=0)
+                device_cycle(g)
                 cyc_ev[i][1].record(stream)
             t_end.record(stream)
         barrier()
@@ -265,9 +281,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         for a_, b_ in extra:
             a_.record(stream)
-            g.replay()
-            if fused:
-                fused_reduce(eng.unions[0], dst=0)
+            device_cycle(g)
             b_.record(stream)
     barrier()
     per_cycle += [a.elapsed_time(b) for a, b in extra]
@@ -279,11 +293,11 @@ def run_ours(args):
     assert _lib.lib().gc_launch_count() == launches0  # nothing eager snuck in
 
     # ---- e2e: pinned H2D of observations + D2H of the fused union every cycle ----
-    u0 = eng.unions[0]
+    ushape = (scene.steps, scene.spec.height, scene.spec.width)  # float32 fused union
     h2d = eng._nb
-    d2h = u0.numel() * u0.element_size()
+    d2h = math.prod(ushape) * 4
     tr = scene.track
-    h_out = [torch.empty(u0.shape, dtype=u0.dtype).pin_memory() for _ in range(2)]
+    h_out = [torch.empty(ushape, dtype=torch.float32).pin_memory() for _ in range(2)]
     if not fused:
         # one CUDA graph per cycle: H2D of the observations, update, predict in
         # args.chunks horizon chunks whose layers stream to pinned host memory on a
@@ -321,8 +335,10 @@ def run_ours(args):
                     f"chunk's f32 union layers D2H on a copy stream while the next computes; cycles strictly "
                     f"sequential (latency = cycle time), one CUDA graph")
     else:
-        # N > 1: the fused grid needs the NCCL max-reduce; rank 0 reads it back, D2H of
-        # cycle k overlapped with cycle k+1 (double-buffered unions)
+        # N > 1: the fused grid is merged by the NCCL max-reduce (or written in place over
+        # peer memory); rank 0 reads it back, D2H of cycle k overlapped with cycle k+1
+        # (double-buffered unions; with peer memory rank 0 re-zeroes buffer b after its
+        # D2H, and every rank's next write of b follows the barrier that waits for that)
         ga = [eng.capture(buf=b, with_h2d=True) for b in (0, 1)]
         copy = torch.cuda.Stream()
         done = [torch.cuda.Event() for _ in range(2)]
@@ -339,14 +355,22 @@ def run_ours(args):
                     stream.wait_event(copied[b])
                     s_ev = torch.cuda.Event(enable_timing=True)
                     s_ev.record(stream)
+                    if peer is not None:
+                        peer.barrier()      # rank 0's zero of b precedes every rank's writes
                     ga[b].replay()
                     staged_ok[b].record(stream)
-                    fused_reduce(eng.unions[b], dst=0)
+                    if peer is not None:
+                        peer.barrier()      # every rank's K3 writes precede rank 0's read
+                    else:
+                        fused_reduce(eng.unions[b], dst=0)
                     done[b].record(stream)
                 with torch.cuda.stream(copy):
                     copy.wait_event(done[b])
                     if rank == 0:
-                        h_out[b].copy_(eng.unions[b], non_blocking=True)
+                        src = peer.tensor(b) if peer is not None else eng.unions[b]
+                        h_out[b].copy_(src, non_blocking=True)
+                        if peer is not None:
+                            src.zero_()
                     e_ev = torch.cuda.Event(enable_timing=True)
                     e_ev.record(copy)
                     copied[b].record(copy)
@@ -365,7 +389,9 @@ def run_ours(args):
         evs += e2e_loop(n_lat - K, W + K)  # latency samples only
         stream.wait_stream(copy)
         barrier()
-        e2e_note = "pinned obs H2D + NCCL fused union + rank-0 f32 D2H each cycle, D2H overlapped with the next cycle"
+        e2e_note = ("pinned obs H2D + " + ("peer-memory fused union (K3 atomicMax into rank 0's grid over "
+                    "NVLink)" if peer is not None else "NCCL fused union") +
+                    " + rank-0 f32 D2H each cycle, D2H overlapped with the next cycle")
     clocks.__exit__(None, None, None)
     e2e_ms = max_over_ranks(e_start.elapsed_time(e_end) / K)
     lat = [a_.elapsed_time(b_) for a_, b_ in evs]
@@ -429,7 +455,7 @@ def run_ours(args):
                          f"update+predict per cycle"),
             "mode": args.mode, "humans": len(scene.spaces) * world, "particles": scene.n,
             "horizon": scene.steps, "grid": [scene.spec.width, scene.spec.height],
-            "fused_grid_nccl": fused, "parallelism": f"humans sharded over {world} GPU(s)",
+            "fused_grid": (args.fused_path if fused else None), "parallelism": f"humans sharded over {world} GPU(s)",
             "l2": "per-cycle working set > L2: 160 MB union + counts rewritten each cycle (no explicit flush)",
         },
         "e2e": {"value": psteps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -466,6 +492,8 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_sample(scene, t_steps=args.cpu_t, reps=3)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     if distributed:
         dist.destroy_process_group()
     return 0
@@ -483,6 +511,8 @@ def main():
     ap.add_argument("--no-fused", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="take the multi-GPU path (NCCL group, fused reduce) even with one rank")
+    ap.add_argument("--fused-path", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1 fused grid: NCCL max-reduce, or K3 writes over NVLink peer memory")
     ap.add_argument("--no-ref-mode", action="store_true")
     ap.add_argument("--lat-cycles", type=int, default=LAT_CYCLES,
                     help="cycles the p50/p99 latencies are taken over (at least --steps)")

@@ -307,6 +307,20 @@ gc_status gc_collision_field(const void *d_layers, int32_t dtype_bytes, int32_t 
                              int32_t n_offsets, double threshold, double *d_field,
                              uint8_t *d_blocked, void *stream);
 
+/* Peer-memory fused union (multi-GPU form of the union in sim.py:500-502 /
+ * occupancy.py:162-192): the owning rank allocates the (T, H, W) union as a whole device
+ * allocation (gc_peer_alloc) and exports a CUDA IPC handle; every other rank of the node
+ * imports it (NVLink peer mapping) and passes the mapped pointer as the epilogue's
+ * d_union32 / d_union64, so its K3 atomicMax-es into the owner's grid directly (exact,
+ * order-independent).  Replaces the per-cycle NCCL max-reduce of dense grids
+ * (engine.fused_reduce) by the sparse K3 writes themselves. */
+#define GC_PEER_HANDLE_BYTES 64
+gc_status gc_peer_alloc(int64_t bytes, void **d_out);
+gc_status gc_peer_free(void *d);
+gc_status gc_peer_export(const void *d, uint8_t *h_handle);      /* h_handle: 64 bytes */
+gc_status gc_peer_import(const uint8_t *h_handle, void **d_out);
+gc_status gc_peer_close(void *d);
+
 /* rng.derive_seed (rng.py:34-39): SeedSequence(seed, path).generate_state(2,u64) xor-folded. */
 uint64_t gc_derive_seed(uint64_t seed, const uint32_t *h_path, int32_t path_len);
 

@@ -15,8 +15,9 @@ restructured for the B200:
   * optionally the union is read back to pinned host memory on a copy stream,
     double-buffered so the D2H of cycle k overlaps the compute of cycle k+1.
 
-Multi-GPU: one engine per rank over that rank's humans; ``fused_reduce`` merges the
-per-rank unions with NCCL (max) only when a single fused grid is requested.
+Multi-GPU: one engine per rank over that rank's humans; when a single fused grid is
+requested either ``fused_reduce`` merges the per-rank unions with NCCL (max), or every
+rank's K3 writes the owner's grid directly over NVLink peer memory (``peer.PeerUnion``).
 """
 
 from __future__ import annotations
@@ -73,10 +74,22 @@ class EngineConfig:
 class CycleEngine:
     def __init__(self, control_set, q_model, spaces: Sequence, grid_spec, cfg: EngineConfig,
                  initial_log_weights: Optional[Sequence[np.ndarray]] = None,
-                 human_ids: Optional[Sequence[int]] = None, counts_reduce=None):
+                 human_ids: Optional[Sequence[int]] = None, counts_reduce=None, peer=None):
         self.dev = device()
         self.cfg = cfg
         self.counts_reduce = counts_reduce
+        # peer: a peer.PeerUnion -- K3 atomicMax-es this engine's humans into the fused grid
+        # of the owning rank (NVLink peer memory) instead of a local union; the owner zeroes
+        # and reads it between PeerUnion.barrier() calls
+        self.peer = peer
+        if peer is not None:
+            if cfg.union_mode != "max" or cfg.per_human_layers or cfg.robot_radius is not None:
+                raise ValueError("a peer union takes the max union only (no per-human layers / blocked mask)")
+            if cfg.time_union:
+                raise ValueError("with a peer union the owner applies the time union (PeerUnion.finish)")
+            want = torch.float32 if cfg.union_dtype == "float32" else torch.float64
+            if peer.dtype != want or peer.shape != (cfg.steps, grid_spec.height, grid_spec.width):
+                raise ValueError("PeerUnion shape/dtype must match (steps, H, W) and union_dtype")
         if cfg.particle_shard is not None:
             i, k = cfg.particle_shard
             if not (0 <= i < k) or cfg.n % k:
@@ -145,7 +158,10 @@ class CycleEngine:
         self.counts = torch.zeros(H * self.geo.human_stride, dtype=torch.int32, device=dev)
         udt = torch.float32 if cfg.union_dtype == "float32" else torch.float64
         T, Hh, W = cfg.steps, grid_spec.height, grid_spec.width
-        self.unions = [torch.zeros((T, Hh, W), dtype=udt, device=dev) for _ in range(2)]
+        if peer is None:
+            self.unions = [torch.zeros((T, Hh, W), dtype=udt, device=dev) for _ in range(2)]
+        else:  # the owner's fused grids (None on the other ranks)
+            self.unions = [peer.tensor(b) if peer.is_owner else None for b in range(2)]
         if cfg.union_mode not in ("max", "independent"):
             raise ValueError(f"unknown union mode {cfg.union_mode!r}")
         if cfg.union_partial and cfg.union_mode != "independent":
@@ -242,7 +258,8 @@ class CycleEngine:
         fill.wait_event(fork)
         with torch.cuda.stream(fill):
             self.counts.zero_()
-            u.zero_()
+            if self.peer is None:
+                u.zero_()
             if self.layers is not None:
                 self.layers.zero_()
         join = torch.cuda.Event()
@@ -286,7 +303,14 @@ class CycleEngine:
         if self.layers is not None:
             e.d_layers64 = self.layers.data_ptr()
         ordered = cfg.union_mode == "independent"
-        if not ordered:  # max union by atomicMax inside K3
+        if self.peer is not None:  # K3 writes the owner's fused grid over peer memory
+            if d2h is not None:
+                raise ValueError("with a peer union the owner copies the fused grid after PeerUnion.barrier()")
+            if self.peer.dtype == torch.float32:
+                e.d_union32 = self.peer.ptr(buf)
+            else:
+                e.d_union64 = self.peer.ptr(buf)
+        elif not ordered:  # max union by atomicMax inside K3
             if u.dtype == torch.float32:
                 e.d_union32 = u.data_ptr()
             else:

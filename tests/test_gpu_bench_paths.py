@@ -2,7 +2,8 @@
 
 * the single-GPU path (device cycle, chunked e2e, roofline, clocks, CPU baseline);
 * the multi-GPU path (NCCL process group, fused max-reduce, overlapped rank-0 D2H) through
-  torchrun with one rank (--force-dist): the branch the driver's scaling run takes.
+  torchrun with one rank (--force-dist): the branch the driver's scaling run takes; and
+  the same branch with the peer-memory fused grid (--fused-path peer).
 """
 
 import json
@@ -54,4 +55,13 @@ def test_bench_distributed_path_one_rank():
                "--master-addr", "127.0.0.1", "--master-port", "29541", "bench.py", "--gpus", "1", "--force-dist",
                "--steps", "5", "--warmup", "3", "--lat-cycles", "10", "--no-cpu-baseline", "--no-ref-mode"])
     _check(d)
-    assert d["config"]["fused_grid_nccl"] is True
+    assert d["config"]["fused_grid"] == "nccl"
+
+
+def test_bench_distributed_path_one_rank_peer_union():
+    d = _line([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+               "--master-addr", "127.0.0.1", "--master-port", "29543", "bench.py", "--gpus", "1", "--force-dist",
+               "--fused-path", "peer", "--steps", "5", "--warmup", "3", "--lat-cycles", "10", "--no-cpu-baseline",
+               "--no-ref-mode"])
+    _check(d)
+    assert d["config"]["fused_grid"] == "peer"
