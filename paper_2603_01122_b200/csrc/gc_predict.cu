@@ -3,10 +3,10 @@
 //
 // One CTA = one contiguous block of one human's particles.  Each thread keeps K
 // particles' (x, y, hypothesis) in registers for the WHOLE horizon; per step it samples
-// an action per particle, Euler-steps, maps the particle to its cell and adds it, with
-// warp aggregation (__match_any_sync), into a shared-memory privatised window covering
-// the cells the human can reach by that step.  After a CTA barrier the touched cells
-// (kept in a shared list) are flushed with one global reduction each into the human's
+// an action per particle, Euler-steps, maps the particle to its cell and adds it (shared
+// atomic on a u16 half-word) into a shared-memory privatised window covering the cells
+// the human can reach by that step.  After a CTA barrier the touched cells
+// (kept in per-warp lists) are flushed with one global reduction each into the human's
 // windowed count buffer, and zeroed.  HBM sees only those reductions.
 //
 // Two arithmetic families:
@@ -122,7 +122,6 @@ struct SmemTabs {
     // hypotheses of this CTA's human
     double cdf[MAXH];
     float hb[MAXH], hgx[MAXH], hgy[MAXH];
-    int list_n[2];
     int n_hyp, m_keep, q_kind, n_speeds;
     float wth;
     unsigned char phyp[4 * 256];  // hypothesis index of particle slot k*NT+tid (frees registers)
@@ -536,6 +535,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     // cell is floor(u), and the utility is rescaled (k -> k res) so the weights are unchanged
     constexpr bool GRIDU = MODE == MODE_FACT || MODE == MODE_FACTS;
     const int tid = threadIdx.x, lane = tid & 31;
+    const unsigned lane_lt = (1u << lane) - 1u;  // lanes below this one
     const int h = blockIdx.x / P.ctas_per_human;
     const int blk = blockIdx.x - h * P.ctas_per_human;
     const int tsel = __ldg(&P.table_id[h]);
@@ -613,13 +613,12 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         }
     }
     unsigned *win = reinterpret_cast<unsigned *>(smem_dyn);
-    int *list = nullptr;  // packed-word indices touched this step (<= one per particle)
+    int *wlist = nullptr;  // this warp's packed-word indices touched this step (<= 32 K)
     if (P.smem_window) {
         const int R = __ldg(&P.step_r[P.steps - 1]);
         const int words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
         for (int i = tid; i < words; i += NT) win[i] = 0u;
-        list = reinterpret_cast<int *>(win + ((words + 3) & ~3));
-        if (tid == 0) { S.list_n[0] = 0; S.list_n[1] = 0; }
+        wlist = reinterpret_cast<int *>(win + ((words + 3) & ~3)) + (tid >> 5) * (32 * K);
     }
     const bool qg = __syncthreads_and(qg_ok) != 0;
 
@@ -699,6 +698,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         unsigned *gcount = P.counts + hbase + __ldg(&P.step_off[t - 1]);
         uint64_t sk0 = 0, sk1 = 0;
         int key_chunk = -1;
+        int nlist = 0;  // entries of this warp's touched list this step (warp-uniform)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
@@ -764,9 +764,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) overflow = true;
                 else local = ly * ww + lx;
             }
-            // whole warp on one cell (early steps): one aggregated add; else per lane.
-            // A word seen zero by its first add is appended to the touched list
-            // (warp-aggregated: one shared atomic per warp).
+            // A word seen zero by its first add is appended to the touched list of this
+            // warp (its own slice of the list: a ballot and a popcount, no shared atomic)
             if (P.smem_window) {
                 bool first = false;
                 if (local >= 0) {
@@ -776,24 +775,18 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                                       (off & 2u) ? 0x10000u : 1u) == 0u;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, first);
-                if (m) {
-                    const int leader = __ffs(m) - 1;
-                    int base = 0;
-                    if (lane == leader) base = atomicAdd(&S.list_n[t & 1], __popc(m));
-                    base = __shfl_sync(0xffffffffu, base, leader);
-                    if (first) list[base + __popc(m & ((1u << lane) - 1u))] = local >> 1;
-                }
+                if (first) wlist[nlist + __popc(m & lane_lt)] = local >> 1;
+                nlist += __popc(m);
             } else if (local >= 0) {
                 atomicAdd(&gcount[local], 1u);
             }
         }
         if (P.smem_window) {
             __syncthreads();
-            // flush only the touched words: one global reduction per nonzero cell
-            const int nl = S.list_n[t & 1];
-            if (tid == 0) S.list_n[(t + 1) & 1] = 0;
-            for (int i = tid; i < nl; i += NT) {
-                const int wi = list[i];
+            // flush only the touched words: each warp its own list, one global reduction
+            // per nonzero cell (a word touched by several warps is listed once, by the first)
+            for (int i = lane; i < nlist; i += 32) {
+                const int wi = wlist[i];
                 const unsigned w = win[wi];
                 win[wi] = 0u;
                 const unsigned lo = w & 0xFFFFu, hi = w >> 16;
@@ -1015,7 +1008,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.ppc = ppc;
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
-    const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4 + (size_t)ppc * 4;
+    const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4 + (size_t)NT * K * 4;
     // shared-memory windows whenever they fit (robust to coherent particle clouds);
     // GC_PREDICT_GLOBAL_HIST=1 forces direct global reductions (tuning knob)
     static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();
