@@ -5,8 +5,8 @@
 // particles' (x, y, hypothesis) in registers for the WHOLE horizon; per step it samples
 // an action per particle, Euler-steps, maps the particle to its cell and adds it (shared
 // atomic on a u16 half-word) into a shared-memory privatised window covering the cells
-// the human can reach by that step.  After a CTA barrier the touched cells
-// (kept in per-warp lists) are flushed with one global reduction each into the human's
+// the human can reach by that step.  After a CTA barrier the touched cells (each
+// remembered by the thread whose add found its word zero) are flushed with one global reduction each into the human's
 // windowed count buffer, and zeroed.  HBM sees only those reductions.
 //
 // Two arithmetic families:
@@ -535,7 +535,6 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     // cell is floor(u), and the utility is rescaled (k -> k res) so the weights are unchanged
     constexpr bool GRIDU = MODE == MODE_FACT || MODE == MODE_FACTS;
     const int tid = threadIdx.x, lane = tid & 31;
-    const unsigned lane_lt = (1u << lane) - 1u;  // lanes below this one
     const int h = blockIdx.x / P.ctas_per_human;
     const int blk = blockIdx.x - h * P.ctas_per_human;
     const int tsel = __ldg(&P.table_id[h]);
@@ -613,12 +612,14 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         }
     }
     unsigned *win = reinterpret_cast<unsigned *>(smem_dyn);
-    int *wlist = nullptr;  // this warp's packed-word indices touched this step (<= 32 K)
+    // fw[k NT]: the window word this thread's particle slot k added to first this step, or
+    // -1 (that thread owns the word's flush)
+    int *fw = nullptr;
     if (P.smem_window) {
         const int R = __ldg(&P.step_r[P.steps - 1]);
         const int words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
         for (int i = tid; i < words; i += NT) win[i] = 0u;
-        wlist = reinterpret_cast<int *>(win + ((words + 3) & ~3)) + (tid >> 5) * (32 * K);
+        fw = reinterpret_cast<int *>(win + ((words + 3) & ~3)) + tid;
     }
     const bool qg = __syncthreads_and(qg_ok) != 0;
 
@@ -698,7 +699,6 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         unsigned *gcount = P.counts + hbase + __ldg(&P.step_off[t - 1]);
         uint64_t sk0 = 0, sk1 = 0;
         int key_chunk = -1;
-        int nlist = 0;  // entries of this warp's touched list this step (warp-uniform)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + k * NT + tid;
@@ -764,29 +764,30 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) overflow = true;
                 else local = ly * ww + lx;
             }
-            // A word seen zero by its first add is appended to the touched list of this
-            // warp (its own slice of the list: a ballot and a popcount, no shared atomic)
+            // the thread whose add finds a window word zero owns that word's flush this
+            // step: it remembers the word in its own shared slot (no list, no ballot)
             if (P.smem_window) {
-                bool first = false;
+                int f = -1;
                 if (local >= 0) {
                     // u16 counter `local`: byte offset 2 local, in word (2 local) & ~3
                     const unsigned off = 2u * (unsigned)local;
-                    first = atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
-                                      (off & 2u) ? 0x10000u : 1u) == 0u;
+                    if (atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
+                                  (off & 2u) ? 0x10000u : 1u) == 0u)
+                        f = local >> 1;
                 }
-                const unsigned m = __ballot_sync(0xffffffffu, first);
-                if (first) wlist[nlist + __popc(m & lane_lt)] = local >> 1;
-                nlist += __popc(m);
+                fw[k * NT] = f;  // this thread's slot k (conflict-free)
             } else if (local >= 0) {
                 atomicAdd(&gcount[local], 1u);
             }
         }
         if (P.smem_window) {
             __syncthreads();
-            // flush only the touched words: each warp its own list, one global reduction
-            // per nonzero cell (a word touched by several warps is listed once, by the first)
-            for (int i = lane; i < nlist; i += 32) {
-                const int wi = wlist[i];
+            // flush only the touched words, each by its first toucher: one global
+            // reduction per nonzero cell, then the word is zeroed for the next step
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int wi = fw[k * NT];
+                if (wi < 0) continue;
                 const unsigned w = win[wi];
                 win[wi] = 0u;
                 const unsigned lo = w & 0xFFFFu, hi = w >> 16;
