@@ -433,7 +433,7 @@ def run_ours(args):
         xa = psteps_rank * mpp / k2_s / 1e12
         roof["xu"] = {"achieved": xa, "peak": xu_peak, "unit": "T MUFU lane-ops/s", "frac": xa / xu_peak,
                       "mufu_per_particle_step": mpp,
-                      "note": "second bound: 24 heading + 4 speed + 1 chosen-heading ex2 and 1 rsqrt per particle-step"}
+                      "note": "second bound: 24 heading + 1 speed-weight (2^-kr) + 1 chosen-heading ex2 and 1 rsqrt per particle-step"}
     if traffic:
         ga = traffic / k2_s / 1e9
         roof["hbm"] = {"achieved": ga, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ga / pk["hbm_gbs"],
