@@ -33,12 +33,13 @@ def exact_action_probs(z, belief, cs, q, space):
     return p
 
 
-def one_step_tv(q_factory, n=1 << 22, weights=None, mask_v=None, goals=((0.5, 0.3), (0.1, 0.15))):
-    cs = G.ControlSet.grid(4, 24, 1.4)
+def one_step_tv(q_factory, n=1 << 22, weights=None, mask_v=None, goals=((0.5, 0.3), (0.1, 0.15)),
+                speeds=4, betas=(0.3, 2.0, 9.0)):
+    cs = G.ControlSet.grid(speeds, 24, 1.4)
     q = q_factory()
     if mask_v is not None:
         q = G.mask_stationary(q, cs, mask_v)
-    space = G.HypothesisSpace(G.RationalitySet((0.3, 2.0, 9.0)), G.GoalSet(np.array(goals)))
+    space = G.HypothesisSpace(G.RationalitySet(betas), G.GoalSet(np.array(goals)))
     b = G.JointBelief.from_probs(weights if weights is not None else np.full(space.size, 1.0 / space.size))
     spec = G.GridSpec(400, 400, 0.001)
     z = G.HumanState(0.2005, 0.2005)
@@ -70,6 +71,21 @@ def test_factorised_masked_and_weighted():
     tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5), mask_v=0.5)
     assert fact and tv < 0.006, tv
     tv, fact = one_step_tv(lambda: G.q_goal_progress(0.4, (0.3, 0.2)), weights=[0.1, 0.2, 0.05, 0.3, 0.05, 0.3])
+    assert fact and tv < 0.006, tv
+
+
+@pytest.mark.parametrize("speeds", [2, 3, 4])
+def test_factorised_speed_counts(speeds):
+    """Top-speed normalisation of the speed weights for 2, 3 and 4 speeds (n_speeds - 1
+    moving speeds + stay), including a distant goal (small Q = 2^-kr)."""
+    tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5), speeds=speeds, goals=((0.5, 0.3), (40.0, 30.0)))
+    assert fact and tv < 0.006, tv
+
+
+def test_factorised_large_beta_fallback():
+    """beta = 300 overflows the top-speed constants 2^(c top^2): the CTA keeps the
+    max-shift speed weights (and the other hypotheses of that human with it)."""
+    tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5), betas=(0.3, 2.0, 300.0))
     assert fact and tv < 0.006, tv
 
 
