@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     // the factorised sampler keeps particles in grid units u = (x - origin) / res: the
     // cell is floor(u), and the utility is rescaled (k -> k res) so the weights are unchanged
     constexpr bool GRIDU = MODE == MODE_FACT || MODE == MODE_FACTS;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const int h = blockIdx.x / P.ctas_per_human;
     const int blk = blockIdx.x - h * P.ctas_per_human;
     const int tsel = __ldg(&P.table_id[h]);
