@@ -1,6 +1,9 @@
 """Build libgridcast_b200.so in-tree for sm_100a (explicit nvcc; no JIT cache).
 
-    python -m paper_2603_01122_b200.build
+    python -m paper_2603_01122_b200.build [--force] [--checked]
+
+``--checked`` builds _lib/checked/libgridcast_b200.so with device asserts on the hot
+kernels' indices (run anything against it with GC_LIB_PATH=<that path>).
 """
 
 from __future__ import annotations
@@ -40,18 +43,24 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+# bounds-checked variant (every hot-kernel index a device assert; GC_LIB_PATH selects it)
+CHECKED_OUT = os.path.join(HERE, "_lib", "checked", "libgridcast_b200.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    out = CHECKED_OUT if checked else OUT
+    if not checked and not force and not needs_build():
         return OUT
     from concurrent.futures import ThreadPoolExecutor
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    objdir = os.path.join(HERE, "_lib", "obj")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    objdir = os.path.join(HERE, "_lib", "obj_checked" if checked else "obj")
     os.makedirs(objdir, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
+    extra = ["-DGC_CHECKED"] if checked else []
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, *FILE_FLAGS.get(os.path.basename(src), []), "-c", "-o", obj, src]
+        cmd = [nvcc, *NVCC_FLAGS, *extra, *FILE_FLAGS.get(os.path.basename(src), []), "-c", "-o", obj, src]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd))
@@ -60,10 +69,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(compile_one, sources()))
-    subprocess.run([nvcc, *LINK_FLAGS, "-o", OUT + ".tmp", *objs], check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    subprocess.run([nvcc, *LINK_FLAGS, "-o", out + ".tmp", *objs], check=True)
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

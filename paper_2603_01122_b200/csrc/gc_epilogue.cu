@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
         const int X = X0 - rad + lx, Y = Y0 - rad + ly;
         double v = 0.0;
         if (X >= x0 && X <= x1 && Y >= y0 && Y <= y1) {
+            GC_DCHECK(__ldg(&P.step_off[t]) + (long long)(Y - y0) * ww + (X - x0) < P.human_stride);
             const unsigned c = __ldg(&cnt[(Y - y0) * ww + (X - x0)]);
             if (c) {
                 v = (double)c / (double)P.n;  // exactly the reference's counts / n
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
         } else {
             v = vin[(yy + rad) * E + (xx + rad)];
         }
+        GC_DCHECK(yy * E + xx + 2 * rad < E * E && (rad == 0 || yy * E + xx + 2 * rad < ET * E));
         const long long cell = (long long)Y * P.grid_w + X;
         if (P.layers64) P.layers64[((long long)h * P.steps + t) * P.grid_h * P.grid_w + cell] = v;
         if (v > 0.0) {

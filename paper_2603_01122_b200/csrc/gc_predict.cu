@@ -409,6 +409,7 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     // stay (rr < Z0): every zero-speed action has displacement 0 -- row a = 0 of fd is
     // (0, 0) for every heading, so staying is just a = 0
     a = (rr < Z0) ? 0 : a;
+    GC_DCHECK(a >= 0 && a < NAF && b >= 0 && b < NBF);
     const float2 d = S.fd[a * NBF + b];
     x += d.x;
     y += d.y;
@@ -427,6 +428,7 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
 //      the displacements in that order, so the search result indexes them directly.
 __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &P, float &x, float &y,
                                               int h, float u1, bool qg) {
+    GC_DCHECK(h >= 0 && h < S.n_hyp);
     const float4 hp = S.hp[h];
     const float4 hq = S.hq[h];
     const float rx = x - hp.x, ry = y - hp.y;
@@ -520,6 +522,7 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     int a = 1 + ((w1 <= res) ? 1 : 0) + ((w1 + w2 <= res) ? 1 : 0);
     a = a < na - 1 ? a : na - 1;
     a = (rr < Z0) ? 0 : a;  // stay: row 0 of fd is (0, 0)
+    GC_DCHECK(a >= 0 && a < NAF && b >= 0 && b < NBF);
     const float2 d = S.fd[a * NBF + b];
     x += d.x;
     y += d.y;
@@ -615,9 +618,10 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     // fw[k NT]: the window word this thread's particle slot k added to first this step, or
     // -1 (that thread owns the word's flush)
     int *fw = nullptr;
+    int words = 0;  // window capacity (u32 words)
     if (P.smem_window) {
         const int R = __ldg(&P.step_r[P.steps - 1]);
-        const int words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
+        words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
         for (int i = tid; i < words; i += NT) win[i] = 0u;
         fw = reinterpret_cast<int *>(win + ((words + 3) & ~3)) + tid;
     }
@@ -657,7 +661,12 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             px[k] = GRIDU ? __fdiv_rn(sx0 - P.ox, P.res) : sx0;
             py[k] = GRIDU ? __fdiv_rn(sy0 - P.oy, P.res) : sy0;
             ph[k] = 0; r1[k] = r2[k] = r3[k] = 0u;
-            if (p >= P.n || k * NT + tid >= P.ppc) continue;
+            if (p >= P.n || k * NT + tid >= P.ppc) {
+                // padded slot: it steps (no divergence) but never counts; give it a valid
+                // hypothesis so it reads defined tables (found by the GC_CHECKED build)
+                S.phyp[k * NT + tid] = 0;
+                continue;
+            }
             if (P.t_begin > 1) {  // resume a chunked horizon
                 const long long g = (long long)h * P.n + p;
                 const float2 st = P.state_xy[g];
@@ -697,6 +706,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         const int y0 = max(0, cy - R), y1 = min(P.grid_h - 1, cy + R);
         const int ww = x1 - x0 + 1, wh = y1 - y0 + 1;
         unsigned *gcount = P.counts + hbase + __ldg(&P.step_off[t - 1]);
+        GC_DCHECK(__ldg(&P.step_off[t - 1]) + (long long)ww * wh <= P.human_stride);
         uint64_t sk0 = 0, sk1 = 0;
         int key_chunk = -1;
 #pragma unroll
@@ -771,12 +781,14 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 if (local >= 0) {
                     // u16 counter `local`: byte offset 2 local, in word (2 local) & ~3
                     const unsigned off = 2u * (unsigned)local;
+                    GC_DCHECK(local < ww * wh && (int)(off >> 2) < words);
                     if (atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
                                   (off & 2u) ? 0x10000u : 1u) == 0u)
                         f = local >> 1;
                 }
                 fw[k * NT] = f;  // this thread's slot k (conflict-free)
             } else if (local >= 0) {
+                GC_DCHECK(local < ww * wh);
                 atomicAdd(&gcount[local], 1u);
             }
         }
@@ -788,9 +800,11 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             for (int k = 0; k < K; ++k) {
                 const int wi = fw[k * NT];
                 if (wi < 0) continue;
+                GC_DCHECK(wi < words);
                 const unsigned w = win[wi];
                 win[wi] = 0u;
                 const unsigned lo = w & 0xFFFFu, hi = w >> 16;
+                GC_DCHECK(2 * wi + (hi ? 1 : 0) < ww * wh);
                 if (lo) atomicAdd(&gcount[2 * wi], lo);
                 if (hi) atomicAdd(&gcount[2 * wi + 1], hi);
             }
