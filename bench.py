@@ -118,6 +118,7 @@ def cpu_sample(scene, t_steps=10, reps=3, workers=None):
     from oracle import model, port
     from oracle.predict import Grid, belief_update
     workers = workers or (os.cpu_count() or 1)
+    t_steps = min(t_steps, scene.steps)
     cs = scene.control_set
     tb = model.make_tables(cs.v, cs.theta, scene.dt, model.QSpec("goal_progress", 0.5))
     sp = scene.spaces[0]
@@ -144,7 +145,7 @@ def cpu_sample(scene, t_steps=10, reps=3, workers=None):
         "value": psteps / cycle_s, "unit": UNIT, "cores": workers, "kind": "port",
         "hz": 1.0 / cycle_s, "cycle_s": cycle_s,
         "sample": (f"1 human x {scene.n} particles x {t_steps} steps + 1 belief update, median of {reps}; "
-                   f"extrapolated x{H} humans x{scene.steps // t_steps} in T (reference CPU path restated "
+                   f"extrapolated x{H} humans x{scene.steps / t_steps:g} in T (reference CPU path restated "
                    f"in oracle/port.py, ThreadPool {workers} workers, OPENBLAS_NUM_THREADS=1)"),
     }
 
@@ -167,7 +168,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": cycle_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "hz": 1.0 / cycle_s,
-        "config": {"workload": f"{args.config}: 8 humans x 262144 particles x 250 steps dt 0.02, 400x400 union",
+        "config": {"workload": (f"{args.config}: {len(scene.spaces)} humans x {scene.n} particles x {scene.steps} "
+                                f"steps dt {scene.dt}, {scene.spec.width}x{scene.spec.height} union"),
                    "parallelism": "host threads"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "port",
                          "sample": vals[0]["sample"]},
@@ -198,7 +200,9 @@ def run_ours(args):
     from paper_2603_01122_b200.scenario import make_scene
 
     K, W = args.steps, args.warmup
-    scene = make_scene(args.config, cycles=W + K + 4, humans=8, human_offset=8 * rank)
+    from paper_2603_01122_b200.scenario import CONFIGS
+    hpg = CONFIGS[args.config]["humans"]  # humans per GPU (weak scaling): cfg3 8, cfg1/cfg2 1
+    scene = make_scene(args.config, cycles=W + K + 4, humans=hpg, human_offset=hpg * rank)
     cfg = EngineConfig(n=scene.n, steps=scene.steps, dt=scene.dt, smoothing_sigma=0.1, seed=0,
                        mode=args.mode, time_union=False, chunk_taper=args.chunk_taper)
     fused = distributed and not args.no_fused
@@ -209,7 +213,7 @@ def run_ours(args):
         from paper_2603_01122_b200.peer import PeerUnion
         peer = PeerUnion((scene.steps, scene.spec.height, scene.spec.width), torch.float32)
     eng = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec, cfg,
-                      human_ids=list(range(8 * rank, 8 * rank + len(scene.spaces))), peer=peer)
+                      human_ids=list(range(hpg * rank, hpg * rank + len(scene.spaces))), peer=peer)
     # posterior after 10 observations (also warms every kernel)
     eng.prime(scene.warmup_track[0])
     for k in range(1, 11):
@@ -451,12 +455,14 @@ def run_ours(args):
         "hz": 1000.0 / ms, "p50_ms": p50, "p99_ms": p99, "latency_cycles": n_lat,
         "config": {
             "workload": (f"{args.config}: {len(scene.spaces)} humans/GPU x {scene.n} particles x {scene.steps} "
-                         f"steps dt {scene.dt}, |H|=20, |U|=96, 400x400 @0.1 m union, sigma 0.1 m, "
+                         f"steps dt {scene.dt}, |H|={scene.spaces[0].size}, |U|={len(scene.control_set)}, "
+                         f"{scene.spec.width}x{scene.spec.height} @{scene.spec.resolution} m union, sigma 0.1 m, "
                          f"update+predict per cycle"),
             "mode": args.mode, "humans": len(scene.spaces) * world, "particles": scene.n,
             "horizon": scene.steps, "grid": [scene.spec.width, scene.spec.height],
             "fused_grid": (args.fused_path if fused else None), "parallelism": f"humans sharded over {world} GPU(s)",
-            "l2": "per-cycle working set > L2: 160 MB union + counts rewritten each cycle (no explicit flush)",
+            "l2": (f"per-cycle working set: {d2h / 1e6:.0f} MB f32 union + counts rewritten each cycle, "
+                   f"{'above' if d2h > 126e6 else 'below'} the 126 MB L2 (no explicit flush)"),
         },
         "e2e": {"value": psteps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h if (rank == 0 or not fused) else 0,
@@ -472,7 +478,7 @@ def run_ours(args):
         import dataclasses
         eng_r = CycleEngine(scene.control_set, scene.q, scene.spaces, scene.spec,
                             dataclasses.replace(cfg, mode="reference"),
-                            human_ids=list(range(8 * rank, 8 * rank + len(scene.spaces))))
+                            human_ids=list(range(hpg * rank, hpg * rank + len(scene.spaces))))
         eng_r.prime(scene.warmup_track[0])
         eng_r.stage(scene.warmup_track[1], buf=0)
         eng_r.run_cycle(buf=0)
