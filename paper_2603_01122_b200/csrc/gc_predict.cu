@@ -290,9 +290,10 @@ __device__ __forceinline__ int gen_pick(const SmemTabs &H, const SmemAct &S, flo
 //   G_a = exp(a k r - c a^2 - S),     S = max_a (a k r - c a^2),  H_b = exp(-beta w_th th_b^2)
 // -> per step: NB ex2 (e_b), 4 ex2 (G_a), Horner in e_b, inverse CDF over headings then
 //    over speeds.  Zero-speed actions share displacement 0 and merge into one "stay".
+//    (fact_step_sym below: the standard heading set, one ex2 for all G_a.)
 // the standard ControlSet.grid heading set theta_b = -pi + b*pi/12 (agents.py:79-87),
-// float32 cos/sin as the host computes them; compiled in so the heading loop uses
-// immediate operands instead of constant-bank loads
+// float32 cos/sin as the host computes them: a launch whose tables hold exactly these
+// values takes MODE_FACTS (symmetric heading pairs, fact_step_sym)
 #define GC_STD_COS                                                                                  \
     {-1.f, -0.965925813f, -0.866025388f, -0.707106769f, -0.5f, -0.258819044f, 6.12323426e-17f,     \
      0.258819044f, 0.5f, 0.707106769f, 0.866025388f, 0.965925813f, 1.f, 0.965925813f, 0.866025388f, \
@@ -303,12 +304,10 @@ __device__ __forceinline__ int gen_pick(const SmemTabs &H, const SmemAct &S, flo
      -0.965925813f, -0.866025388f, -0.707106769f, -0.5f, -0.258819044f, 0.f, 0.258819044f, 0.5f,   \
      0.707106769f, 0.866025388f, 0.965925813f, 1.f, 0.965925813f, 0.866025388f, 0.707106769f, 0.5f, \
      0.258819044f}
-__device__ constexpr float kStdCos[NBF] = GC_STD_COS;
-__device__ constexpr float kStdSin[NBF] = GC_STD_SIN;
 static const float hStdCos[NBF] = GC_STD_COS;
 static const float hStdSin[NBF] = GC_STD_SIN;
 
-template <bool STDH, bool WTH>
+template <bool WTH>
 __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, float &x, float &y,
                                           int h, float u1) {
     const float4 hp = S.hp[h];
@@ -354,8 +353,8 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
 #endif
 #pragma unroll
     for (int b = 0; b < NBF; ++b) {
-        const float cb = STDH ? kStdCos[b] : P.hcos[b];
-        const float sb = STDH ? kStdSin[b] : P.hsin[b];
+        const float cb = P.hcos[b];
+        const float sb = P.hsin[b];
         // e_b = exp(-k (d_b + r)), d_b = rel . (cos th_b, sin th_b): 2 FFMA + 1 MUFU
         const float e = ex2_approx(fmaf(A, cb, fmaf(B, sb, nkr)));
         // cumulative moving weight: C += H_b e (G1 + e (G2 + e G3)), 3 FFMA
@@ -729,7 +728,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 if (MODE == MODE_FACTS) {
                     fact_step_sym(S, P, x, y, S.phyp[k * NT + tid], u24(ua), qg);
                 } else if (MODE == MODE_FACT) {
-                    fact_step<false, WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
+                    fact_step<WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
                     const int a = gen_pick(S, A, x, y, S.phyp[k * NT + tid], u24(ua));
                     x += A.adx[a];
