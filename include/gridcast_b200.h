@@ -114,7 +114,7 @@ typedef struct {
     const int32_t *d_step_r;   /* (steps,) */
     const int64_t *d_step_off; /* (steps,) */
     int64_t human_stride;
-    int32_t max_win_cells;     /* max_t (2 r_t + 1)^2 */
+    int32_t max_win_cells;     /* max (2 r_t + 1)^2 over the steps of this launch [t_begin, t_end) */
     int32_t _pad2;
     uint32_t *d_counts;
     /* optional outputs */

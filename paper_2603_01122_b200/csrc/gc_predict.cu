@@ -619,7 +619,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     int *fw = nullptr;
     int words = 0;  // window capacity (u32 words)
     if (P.smem_window) {
-        const int R = __ldg(&P.step_r[P.steps - 1]);
+        // the largest window of THIS launch's steps (a horizon chunk may fit in shared
+        // memory when the whole horizon does not): the host sized it from max_win_cells
+        const int R = __ldg(&P.step_r[P.t_end - 2]);
         words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
         for (int i = tid; i < words; i += NT) win[i] = 0u;
         fw = reinterpret_cast<int *>(win + ((words + 3) & ~3)) + tid;

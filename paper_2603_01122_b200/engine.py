@@ -69,6 +69,11 @@ class EngineConfig:
     # horizon chunking (chunks > 1): chunk c spans ~ chunk_taper^c of the horizon, so the
     # last chunks -- whose D2H cannot overlap later compute -- are short; 1.0 = uniform
     chunk_taper: float = 0.5
+    # shared-memory budget (KB) of K2's count window + first-touch slots: a one-chunk
+    # horizon whose last windows exceed it is split so its first part still runs on
+    # shared-memory windows.  Off by default: at the cfg4 shard (T = 500, 2^20 particles
+    # per human) the split measured 42.8 ms per cycle against 40.4 ms on the global path
+    window_budget_kb: float = 0.0
 
 
 class CycleEngine:
@@ -234,6 +239,24 @@ class CycleEngine:
                 starts.append(s)
         return [(t0, t1) for t0, t1 in zip(starts, starts[1:] + [T + 1])]
 
+    def window_bounds(self):
+        """1-based [t0, t1) ranges of a one-chunk cycle: the whole horizon, or -- when its
+        reachable-cell windows outgrow ``cfg.window_budget_kb`` of shared memory -- the
+        longest prefix (ending on a Philox block boundary) whose windows fit, then the rest
+        (K2 adds those steps straight to global memory).  Bit-identical either way."""
+        T, cells = self.cfg.steps, self.geo.win_cells
+        budget = self.cfg.window_budget_kb * 1024
+
+        def fits(c):  # u16 counters two per word (rounded to 4 words) + 4 KB first-touch slots
+            return ((int(c) + 1) // 2 + 3) // 4 * 16 + 4096 <= budget
+
+        if budget <= 0 or fits(cells[T - 1]) or self.counts_reduce is not None:
+            return [(1, T + 1)]
+        t = 1
+        while t + 4 <= T and fits(cells[t + 4 - 2]):
+            t += 4
+        return [(1, T + 1)] if t <= 1 else [(1, t), (t, T + 1)]
+
     def _ensure_state(self):
         if getattr(self, "state_xy", None) is None:
             N = self.n_humans * self.n_local
@@ -269,7 +292,7 @@ class CycleEngine:
                                  self.d_fallback, self.d_logw, self.d_logw, self.d_status, cfg.obs_dt,
                                  math.inf, 1, H, stream=stream)
         stream.wait_event(join)
-        bounds = self.chunk_bounds(chunks) if chunks > 1 else [(1, cfg.steps + 1)]
+        bounds = self.chunk_bounds(chunks) if chunks > 1 else self.window_bounds()
         if self.counts_reduce is not None and len(bounds) > 1:
             raise NotImplementedError("particle sharding runs the horizon in one chunk")
         if len(bounds) > 1:
@@ -318,6 +341,7 @@ class CycleEngine:
             e.time_union = int(cfg.time_union)
         for ci, (t0, t1) in enumerate(bounds):
             a.t_begin, a.t_end = (t0, t1) if len(bounds) > 1 else (0, 0)
+            a.max_win_cells = int(geo.win_cells[t1 - 2])  # this launch's largest window
             if events is not None and ci == 0:
                 events[0].record(stream)
             _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")

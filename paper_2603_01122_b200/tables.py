@@ -220,6 +220,7 @@ class Geometry:
         self.step_off = np.concatenate([[0], np.cumsum(cells)[:-1]]).astype(np.int64)
         self.human_stride = int(cells.sum())
         self.max_win_cells = int(cells.max())
+        self.win_cells = cells.astype(np.int64)  # (2 r_t + 1)^2 per step (non-decreasing)
         sc = sigma_m / self.res if sigma_m > 0 else 0.0
         if sc < 1e-12:
             self.radius = 0

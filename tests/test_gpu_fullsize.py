@@ -32,10 +32,11 @@ def window_sums(eng):
     return out
 
 
-def run(name, mode="production", chunks=0, humans=8, n=None, stationary=()):
+def run(name, mode="production", chunks=0, humans=8, n=None, stationary=(), budget_kb=0.0):
     sc = make_scene(name, cycles=2, humans=humans)
     n = n or sc.n
-    cfg = EngineConfig(n=n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, seed=3, mode=mode)
+    cfg = EngineConfig(n=n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, seed=3, mode=mode,
+                       window_budget_kb=budget_kb)
     eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
     eng.prime(sc.prev_xy)
     obs = sc.track[0].copy()
@@ -77,12 +78,28 @@ def test_cfg3_chunked_equals_single_launch(mode):
 
 
 def test_cfg4_shard_global_histogram_path_conserves_particles():
-    """cfg4's per-GPU shard (8 humans x 1,048,576 particles x 500 steps): the reachable
-    windows exceed shared memory, so K2 adds straight into the L2 count windows."""
+    """cfg4's per-GPU shard (8 humans x 1,048,576 particles x 500 steps): the late reachable
+    windows exceed shared memory, so K2 adds those steps straight into the L2 count windows."""
     eng = run("cfg4_rank")
     np.testing.assert_array_equal(window_sums(eng), eng.cfg.n)
     u = eng.unions[0]
     assert torch.isfinite(u).all() and float(u.max()) <= 1.0
+
+
+@pytest.mark.parametrize("mode", ["production", "reference"])
+def test_long_horizon_window_split_equals_global_path(mode):
+    """T = 500 (cfg4 shape): the engine runs steps 1..248 on shared-memory windows and the
+    rest on global atomics (two launches, particle state handed over); bit-identical to
+    the whole horizon on the global path (window_budget_kb=0)."""
+    n = 65536 if mode == "production" else 4096
+    a = run("cfg4_rank", mode=mode, humans=2, n=n, budget_kb=46.0)
+    assert a.window_bounds() == [(1, 249), (249, 501)]
+    np.testing.assert_array_equal(window_sums(a), n)
+    ua = a.unions[0].cpu().numpy()
+    del a
+    b = run("cfg4_rank", mode=mode, humans=2, n=n, budget_kb=0)
+    assert b.window_bounds() == [(1, 501)]
+    np.testing.assert_array_equal(b.unions[0].cpu().numpy(), ua)
 
 
 def test_stationary_human_uses_masked_table_and_ragged_n():

@@ -11,10 +11,11 @@ from paper_2603_01122_b200.engine import CycleEngine, EngineConfig  # noqa: E402
 from paper_2603_01122_b200.scenario import make_scene  # noqa: E402
 
 
-def main():
+def main(budget_kb=0.0):
     sc = make_scene("cfg4_rank", cycles=4, humans=8)
     eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec,
-                      EngineConfig(n=sc.n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, mode="production"))
+                      EngineConfig(n=sc.n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, mode="production",
+                                   window_budget_kb=budget_kb))
     eng.prime(sc.warmup_track[0])
     for k in range(1, 11):
         eng.stage(sc.warmup_track[k], buf=0)
@@ -36,10 +37,10 @@ def main():
     eng.check_errors()
     cyc = a.elapsed_time(b) / 5
     ps = 8 * sc.n * sc.steps
-    print(f"cfg4_rank: K2 {sum(e[0].elapsed_time(e[1]) for e in ev) / 3:.2f} ms, "
+    print(f"cfg4_rank (window budget {budget_kb} KB, launches {eng.window_bounds()}): K2 {sum(e[0].elapsed_time(e[1]) for e in ev) / 3:.2f} ms, "
           f"K3 {sum(e[1].elapsed_time(e[2]) for e in ev) / 3:.3f} ms, cycle {cyc:.2f} ms "
           f"({1000 / cyc:.1f} Hz, {ps / cyc / 1e6:.1f} G particle-steps/s)")
 
 
 if __name__ == "__main__":
-    main()
+    main(float(sys.argv[1]) if len(sys.argv) > 1 else 0.0)
