@@ -279,14 +279,18 @@ class CycleEngine:
         fork = torch.cuda.Event()
         fork.record(stream)
         fill.wait_event(fork)
+        # K2 waits only for the counts; the union / layer fills (160 MB at cfg3) keep
+        # running under K2 and are joined before the first epilogue
         with torch.cuda.stream(fill):
             self.counts.zero_()
+            join = torch.cuda.Event()
+            join.record(fill)
             if self.peer is None:
                 u.zero_()
             if self.layers is not None:
                 self.layers.zero_()
-        join = torch.cuda.Event()
-        join.record(fill)
+            join_out = torch.cuda.Event()
+            join_out.record(fill)
         if with_update:
             launch_belief_update(self.btab, self.d_hyp_off, self.d_beta64, self.d_goal64, self.d_obs,
                                  self.d_fallback, self.d_logw, self.d_logw, self.d_status, cfg.obs_dt,
@@ -349,6 +353,8 @@ class CycleEngine:
                 events[1].record(stream)
             if self.counts_reduce is not None:
                 self.counts_reduce(self.counts)  # e.g. NCCL all-reduce(sum) over the shards
+            if ci == 0:
+                stream.wait_event(join_out)  # output grids zeroed before K3 writes them
             if len(bounds) > 1:
                 e.tile_begin, e.tile_end = int(geo.tile_start[t0 - 1]), int(geo.tile_start[t1 - 1])
                 e.t_begin, e.t_end = t0 - 1, t1 - 1
