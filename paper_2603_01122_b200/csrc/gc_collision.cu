@@ -44,21 +44,32 @@ __global__ void __launch_bounds__(CNT) k_collision(const Tin *in, int W, int H, 
         }
     }
     __syncthreads();
-    const int xx = threadIdx.x % CT;
+    // each thread sums CY = 4 cells of one column (rows yy0, yy0 + 8, ...) together: one
+    // offset load and address per offset for all four, four independent float64 chains
+    // (each still the reference's sequential order)
+    constexpr int CY = CT / (CNT / CT);
+    const int xx = threadIdx.x % CT, yy0 = threadIdx.x / CT;
     const int X = X0 + xx;
-    for (int yy = threadIdx.x / CT; yy < CT; yy += CNT / CT) {
-        const int Y = Y0 + yy;
-        if (X >= W || Y >= H) continue;
-        const double *base = tile + (yy + rc) * E + (xx + rc);
-        double s = 0.0;
-        for (int k = 0; k < n_off; ++k) {
-            const int2 o = D.o[k];
-            s += base[o.y * E + o.x];
-        }
-        s = s < 1.0 ? s : 1.0;  // np.minimum(out, 1.0)
+    const double *base = tile + (yy0 + rc) * E + (xx + rc);
+    double s[CY];
+#pragma unroll
+    for (int c = 0; c < CY; ++c) s[c] = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < n_off; ++k) {
+        const int2 o = D.o[k];
+        const double *b = base + o.y * E + o.x;
+#pragma unroll
+        for (int c = 0; c < CY; ++c) s[c] += b[c * (CNT / CT) * E];
+    }
+    if (X >= W) return;
+#pragma unroll
+    for (int c = 0; c < CY; ++c) {
+        const int Y = Y0 + yy0 + c * (CNT / CT);
+        if (Y >= H) break;
+        const double v = s[c] < 1.0 ? s[c] : 1.0;  // np.minimum(out, 1.0)
         const long long oi = (long long)L * W * H + (long long)Y * W + X;
-        if (field) field[oi] = s;
-        if (blocked) blocked[oi] = s >= threshold ? 1 : 0;
+        if (field) field[oi] = v;
+        if (blocked) blocked[oi] = v >= threshold ? 1 : 0;
     }
 }
 
