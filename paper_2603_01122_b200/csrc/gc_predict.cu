@@ -71,6 +71,7 @@ struct KParams {
     unsigned *counts;
     int smem_window;
     int act_off;  // byte offset of SmemAct in dynamic shared memory (REF/GEN modes)
+    int dyn_smem; // dynamic shared memory bytes of the launch (bounds checks)
     int t_begin, t_end;          // steps [t_begin, t_end) of this launch (1-based)
     int p_offset;                // global index of this launch's first particle (particle sharding)
     float2 *state_xy;            // particle state between horizon chunks
@@ -625,6 +626,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
         for (int i = tid; i < words; i += NT) win[i] = 0u;
         fw = reinterpret_cast<int *>(win + ((words + 3) & ~3)) + tid;
+        GC_DCHECK((((words + 3) & ~3) + NT * K) * 4 <= P.dyn_smem);
     }
     const bool qg = __syncthreads_and(qg_ok) != 0;
 
@@ -1032,6 +1034,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.act_off = P.smem_window ? (int)((win_bytes + 15) & ~(size_t)15) : 0;  // 16-byte aligned rows
     const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;
     const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : 0);
+    P.dyn_smem = (int)smem;
     cudaStream_t st = (cudaStream_t)stream;
     bool stdh = fact;
     for (int b = 0; stdh && b < NBF; ++b) stdh = P.hcos[b] == hStdCos[b] && P.hsin[b] == hStdSin[b];
