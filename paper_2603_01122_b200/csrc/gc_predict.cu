@@ -649,7 +649,6 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
 
     float px[K], py[K];
     int ph[K];
-    unsigned r1[K], r2[K], r3[K];  // unused words of the particle's current Philox4x32 block
     const int pbase = blk * P.ppc;
     {
         uint64_t hk0 = 0, hk1 = 0;
@@ -660,11 +659,11 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int p = pbase + k * NT + tid;
+            const int p = pbase + tid * K + k;
             px[k] = GRIDU ? __fdiv_rn(sx0 - P.ox, P.res) : sx0;
             py[k] = GRIDU ? __fdiv_rn(sy0 - P.oy, P.res) : sy0;
-            ph[k] = 0; r1[k] = r2[k] = r3[k] = 0u;
-            if (p >= P.n || k * NT + tid >= P.ppc) {
+            ph[k] = 0;
+            if (p >= P.n || tid * K + k >= P.ppc) {
                 // padded slot: it steps (no divergence) but never counts; give it a valid
                 // hypothesis so it reads defined tables (found by the GC_CHECKED build)
                 S.phyp[k * NT + tid] = 0;
@@ -712,23 +711,25 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         GC_DCHECK(__ldg(&P.step_off[t - 1]) + (long long)ww * wh <= P.human_stride);
         uint64_t sk0 = 0, sk1 = 0;
         int key_chunk = -1;
+        // production streams: one Philox4x32-10 block per step for every 4 consecutive
+        // particles (block counter: global particle index / 4, step, human stream, tag);
+        // particle p takes word p % 4.  A thread's K = 4 particles are consecutive and
+        // aligned, so each thread draws exactly one block per step and keeps no state.
+        U4 rb = U4{0u, 0u, 0u, 0u};
+        if (MODE != MODE_REF)
+            rb = philox4x32(U4{(unsigned)((pbase + tid * K + P.p_offset) >> 2), (unsigned)(t - 1), sc2, sk_hi ^ 0xA11CEu},
+                            PHK0, PHK1);
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int p = pbase + k * NT + tid;
-            const bool valid = p < P.n && k * NT + tid < P.ppc;
+            const int p = pbase + tid * K + k;
+            const bool valid = p < P.n && tid * K + k < P.ppc;
             int local = -1;
             if (MODE != MODE_REF) {
                 // production: padded lanes compute too (no divergence), they just do not count
                 float x = px[k], y = py[k];
-                // one Philox4x32-10 block per particle per four steps (one 24-bit uniform
-                // per step); the block counter is (particle, step/4, human stream, tag)
-                unsigned ua;
-                if (((t - 1) & 3) == 0) {
-                    const U4 o = philox4x32(U4{(unsigned)(p + P.p_offset), (unsigned)((t - 1) >> 2), sc2, sk_hi ^ 0xA11CEu}, PHK0, PHK1);
-                    ua = o.x; r1[k] = o.y; r2[k] = o.z; r3[k] = o.w;
-                } else {
-                    ua = r1[k]; r1[k] = r2[k]; r2[k] = r3[k];
-                }
+                // word (p % 4) of this step's block (K = 4: word k; K < 4: the thread's slice)
+                const int wsel = K == 4 ? k : ((p + P.p_offset) & 3);
+                const unsigned ua = wsel == 0 ? rb.x : (wsel == 1 ? rb.y : (wsel == 2 ? rb.z : rb.w));
                 if (MODE == MODE_FACTS) {
                     fact_step_sym(S, P, x, y, S.phyp[k * NT + tid], u24(ua), qg);
                 } else if (MODE == MODE_FACT) {
@@ -818,8 +819,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     if (P.t_end <= P.steps && P.state_xy) {  // hand the particles to the next chunk
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int p = pbase + k * NT + tid;
-            if (p < P.n && k * NT + tid < P.ppc) {
+            const int p = pbase + tid * K + k;
+            if (p < P.n && tid * K + k < P.ppc) {
                 const long long g = (long long)h * P.n + p;
                 P.state_xy[g] = make_float2(px[k], py[k]);
                 P.state_hyp[g] = (unsigned char)ph[k];
@@ -829,8 +830,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     if (P.xy_out) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int p = pbase + k * NT + tid;
-            if (p < P.n && k * NT + tid < P.ppc) {
+            const int p = pbase + tid * K + k;
+            if (p < P.n && tid * K + k < P.ppc) {
                 P.xy_out[((long long)h * P.n + p) * 2] = GRIDU ? fmaf(px[k], P.res, P.ox) : px[k];
                 P.xy_out[((long long)h * P.n + p) * 2 + 1] = GRIDU ? fmaf(py[k], P.res, P.oy) : py[k];
             }
@@ -1008,6 +1009,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
                  "gc_predict: a chunked horizon needs particle state buffers");
     P.state_xy = (float2 *)a->d_state_xy; P.state_hyp = a->d_state_hyp;
     GC_CHECK_ARG(a->p_offset >= 0 && (long long)a->p_offset + a->n < (1ll << 31), "gc_predict: bad particle offset");
+    GC_CHECK_ARG(a->p_offset % 4 == 0, "gc_predict: particle shards must start at a multiple of 4");
     P.p_offset = a->p_offset;
 
     // particles per thread K and particles per CTA: enough CTAs to fill 148 SMs x 3
@@ -1023,6 +1025,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     int ppc = NT * K;
     P.ctas_per_human = (a->n + ppc - 1) / ppc;
     ppc = (a->n + P.ctas_per_human - 1) / P.ctas_per_human;  // balance the last CTA
+    ppc = (ppc + 3) & ~3;  // 4-aligned: a thread's particles share one production Philox block
     P.ppc = ppc;
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");

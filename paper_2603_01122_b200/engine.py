@@ -97,8 +97,8 @@ class CycleEngine:
                 raise ValueError("PeerUnion shape/dtype must match (steps, H, W) and union_dtype")
         if cfg.particle_shard is not None:
             i, k = cfg.particle_shard
-            if not (0 <= i < k) or cfg.n % k:
-                raise ValueError("particle_shard (i, k) needs 0 <= i < k and k | n")
+            if not (0 <= i < k) or cfg.n % k or (cfg.n // k) % 4:
+                raise ValueError("particle_shard (i, k) needs 0 <= i < k, k | n and n / k a multiple of 4")
             self.n_local, self.p_offset = cfg.n // k, i * (cfg.n // k)
         else:
             self.n_local, self.p_offset = cfg.n, 0
