@@ -6,7 +6,9 @@ Reads gpurun_out/launches.csv (launch list of a bench run), gpurun_out/cycle_cfg
 (--set full of K1/K2/K3 of one cfg3 cycle) and gpurun_out/k2_cfg3.ncu-rep (--set full of
 K2 alone, source-level) and writes:
   profiles/<tag>_launches_cfg3.csv, <tag>_launch_shares.txt, <tag>_ncu_cycle_cfg3.txt,
-  profiles/ncu_summary.json (the K2 figures bench.py quotes in its roofline block).
+  profiles/ncu_summary.json (the K2 figures bench.py quotes in its roofline block),
+  <tag>_ncu_k2_reference_mode.txt, <tag>_ncu_frows.txt and the SASS listings / summary of
+  the in-tree library (cuobjdump, here).
 """
 import argparse
 import collections
@@ -115,6 +117,29 @@ def main():
     }}
     json.dump(summary, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=2)
     print(json.dumps(summary, indent=1))
+
+    # reference-arithmetic K2 and the f-row kernels
+    ref = os.path.join(src, "k2_refmode.ncu-rep")
+    if os.path.exists(ref):
+        open(os.path.join(prof, f"{a.tag}_ncu_k2_reference_mode.txt"), "w").write(
+            "# ncu --set full of the REFERENCE-arithmetic kernel k_predict<0,1,0> (1 human x 65536 particles x 20 "
+            "steps)\n" + capture(ncu_summary.main, ref) + "\n# dynamic SASS opcode mix (lane-instructions per "
+            "particle-step)\n" + capture(ncu_opmix.main, ref, 65536 * 20))
+    ext = os.path.join(src, "extras.ncu-rep")
+    if os.path.exists(ext):
+        open(os.path.join(prof, f"{a.tag}_ncu_frows.txt"), "w").write(
+            "# ncu --set full of the f-row kernels (tools/profile_extras.py): collision field of a 250x400x400 f32 "
+            "union,\n# MPPI 4096 rollouts x 40 steps against that mask, exact enumeration 100x100 cells x 96 actions "
+            "x 10 hyps\n# (tools/capture_profiles.sh; per-launch values)\n" + capture(ncu_summary.main, ext))
+    # SASS of the cycle kernels and the static summary of every kernel in the library
+    import sass_extract
+    import sass_summary
+    so = os.path.join(ROOT, "paper_2603_01122_b200", "_lib", "libgridcast_b200.so")
+    for name, fn in (("k_predict_production", "_ZN2gc9k_predictILi3ELi4ELb0EEEvNS_7KParamsE"),
+                     ("k_epilogue", "_ZN2gc10k_epilogueILi3EEEvNS_7EParamsE"),
+                     ("k_belief", "_ZN2gc8k_beliefENS_7BParamsE")):
+        open(os.path.join(prof, f"{a.tag}_sass_{name}.txt"), "w").write(sass_extract.extract(so, fn) + "\n")
+    open(os.path.join(prof, f"{a.tag}_sass_summary_all_kernels.txt"), "w").write(capture(sass_summary.main, so))
 
 
 if __name__ == "__main__":
