@@ -20,4 +20,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pr
 python tools/profile_extras.py > gpurun_out/plain_extras.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collision|k_mppi|k_exact" -s 2 -c 6 \
     -o gpurun_out/extras python tools/profile_extras.py > gpurun_out/ncu_extras.log 2>&1
+# every other kernel of the library (unions, time union, naive, emplace, smooth, sampling,
+# propagate_step) at the small sizes of tools/sanitize_run.py
+python tools/sanitize_run.py > gpurun_out/plain_aux.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none -k regex:"k_(union|time_union|naive|emplace|smooth|sample_hyp|propagate_step)" -c 12 \
+    -o gpurun_out/aux python tools/sanitize_run.py > gpurun_out/ncu_aux.log 2>&1
 tail -n 2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_k2.log gpurun_out/ncu_ref.log gpurun_out/ncu_extras.log

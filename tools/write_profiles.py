@@ -131,6 +131,13 @@ def main():
             "# ncu --set full of the f-row kernels (tools/profile_extras.py): collision field of a 250x400x400 f32 "
             "union,\n# MPPI 4096 rollouts x 40 steps against that mask, exact enumeration 100x100 cells x 96 actions "
             "x 10 hyps\n# (tools/capture_profiles.sh; per-launch values)\n" + capture(ncu_summary.main, ext))
+    aux = os.path.join(src, "aux.ncu-rep")
+    if os.path.exists(aux):
+        open(os.path.join(prof, f"{a.tag}_ncu_aux_kernels.txt"), "w").write(
+            "# ncu --set full of the remaining kernels (ordered unions, time union, predict_naive, emplace, "
+            "smooth,\n# sample_hypotheses, propagate_step) at tools/sanitize_run.py's small sizes: latency-bound "
+            "utility launches,\n# listed for completeness (tools/capture_profiles.sh; per-launch values)\n"
+            + capture(ncu_summary.main, aux))
     # SASS of the cycle kernels and the static summary of every kernel in the library
     import sass_extract
     import sass_summary
