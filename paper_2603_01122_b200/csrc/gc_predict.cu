@@ -426,8 +426,9 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
 //      sum runs in the order (0, 1, 12, 13, 2, 3, 14, 15, ...): index i <-> heading
 //      2(i>>2) + (i&1) + 12((i>>1)&1); the prologue stores the chosen-heading (cos, sin) and
 //      the displacements in that order, so the search result indexes them directly.
-__device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &P, float &x, float &y,
-                                              int h, float u1, bool qg) {
+template <bool WTH>
+__device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &P, const float *Htab, float &x,
+                                              float &y, int h, float u1, bool qg) {
     GC_DCHECK(h >= 0 && h < S.n_hyp);
     const float4 hp = S.hp[h];
     const float4 hq = S.hq[h];
@@ -477,13 +478,19 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
             const float2 eo = make_float2(ex2_approx(xo.x), ex2_approx(xo.y));
             const float2 poly = __ffma2_rn(e, __ffma2_rn(e, g3, g2), g1);
             const float2 polyo = __ffma2_rn(eo, __ffma2_rn(eo, g3, g2), g1);
-            C = fmaf(e.x, poly.x, C);
+            float2 w = e, wo = eo;
+            if (WTH) {  // heading weights H_b of this hypothesis, slots 4j..4j+3 (one LDS.128)
+                const float4 H4 = *reinterpret_cast<const float4 *>(Htab + h * NBF + 4 * j);
+                w = __fmul2_rn(e, make_float2(H4.x, H4.y));
+                wo = __fmul2_rn(eo, make_float2(H4.z, H4.w));
+            }
+            C = fmaf(w.x, poly.x, C);
             cum[4 * j] = C;
-            C = fmaf(e.y, poly.y, C);
+            C = fmaf(w.y, poly.y, C);
             cum[4 * j + 1] = C;
-            C = fmaf(eo.x, polyo.x, C);
+            C = fmaf(wo.x, polyo.x, C);
             cum[4 * j + 2] = C;
-            C = fmaf(eo.y, polyo.y, C);
+            C = fmaf(wo.y, polyo.y, C);
             cum[4 * j + 3] = C;
         }
     }
@@ -517,7 +524,8 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     float xb = fmaf(A, cs.x, fmaf(B, cs.y, nkr));
     if (b & 2) xb = fmaf(xb, -1.f, 2.f * nkr);
     const float e = ex2_approx(xb);
-    const float w1 = G1 * e, w2 = G2 * e * e;
+    const float eh = WTH ? e * Htab[h * NBF + b] : e;
+    const float w1 = G1 * eh, w2 = G2 * e * eh;
     const float res = t - lo;
     int a = 1 + ((w1 <= res) ? 1 : 0) + ((w1 + w2 <= res) ? 1 : 0);
     a = a < na - 1 ? a : na - 1;
@@ -551,6 +559,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         S.wth = T.w_th * 1.4426950408889634f;
     }
     SmemAct &A = *reinterpret_cast<SmemAct *>(smem_dyn + P.act_off);
+    // MODE_FACTS with w_th != 0: per-hypothesis heading weights H_b = exp(-beta w_th th_b^2)
+    // in CDF slot order (MAXH x NBF floats, in place of the unused SmemAct rows)
+    float *Htab = reinterpret_cast<float *>(smem_dyn + P.act_off);
     if (MODE != MODE_FACT && MODE != MODE_FACTS) {
         for (int k = tid; k < T.m_keep; k += NT) {
             const int j = __ldg(&T.keep[k]);
@@ -575,6 +586,13 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             S.fd[i] = j >= 0 ? make_float2(__fdiv_rn(__ldg(&T.dispx[j]), P.res), __fdiv_rn(__ldg(&T.dispy[j]), P.res))
                              : make_float2(0.f, 0.f);
         }
+        if (MODE == MODE_FACTS && WTH) {
+            // same expression as the stay mass sum_b H_b below, so the CDF and Z0 agree
+            for (int i = tid; i < nh * NBF; i += NT) {
+                const int hh = i / NBF, q = hslot(i - hh * NBF);
+                Htab[i] = exp2f(-T.w_th * __ldg(&P.beta32[h0 + hh]) * P.hth2[q] * 1.4426950408889634f);
+            }
+        }
     }
     bool qg_ok = true;  // MODE_FACTS: top-speed normalisation representable for every hypothesis
     for (int i = tid; i < nh; i += NT) {
@@ -589,7 +607,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                                   b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E);
             float sh = 0.f;
             for (int q = 0; q < T.n_headings; ++q)
-                sh += (T.w_th != 0.f) ? exp2f(-T.w_th * b * P.hth2[q] * L2E) : 1.f;
+                sh += (T.w_th != 0.f) ? exp2f(-T.w_th * b * P.hth2[q] * 1.4426950408889634f) : 1.f;
             S.hq[i] = make_float4(0.f, 0.f, S.hp[i].w, sh);
             if (MODE == MODE_FACTS) {
                 // speed weights relative to the top speed (fact_step_sym): powers of 2^c
@@ -731,7 +749,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 const int wsel = K == 4 ? k : ((p + P.p_offset) & 3);
                 const unsigned ua = wsel == 0 ? rb.x : (wsel == 1 ? rb.y : (wsel == 2 ? rb.z : rb.w));
                 if (MODE == MODE_FACTS) {
-                    fact_step_sym(S, P, x, y, S.phyp[k * NT + tid], u24(ua), qg);
+                    fact_step_sym<WTH>(S, P, Htab, x, y, S.phyp[k * NT + tid], u24(ua), qg);
                 } else if (MODE == MODE_FACT) {
                     fact_step<WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
@@ -911,7 +929,8 @@ gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t s
     auto fn = k_predict<MODE, K, WTH>;
     static bool configured = false;  // per instantiation: raise the dynamic limit once
     if (!configured) {
-        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 + (int)sizeof(SmemAct)));
+        const int extra = (int)(sizeof(SmemAct) > (size_t)MAXH * NBF * 4 ? sizeof(SmemAct) : (size_t)MAXH * NBF * 4);
+        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 + extra));
         configured = true;
     }
     fn<<<grid, NT, smem, st>>>(P);
@@ -1036,18 +1055,19 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.smem_window = (win_bytes <= 64 * 1024 && !force_global) ? 1 : 0;
     P.act_off = P.smem_window ? (int)((win_bytes + 15) & ~(size_t)15) : 0;  // 16-byte aligned rows
     const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;
-    const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : 0);
-    P.dyn_smem = (int)smem;
-    cudaStream_t st = (cudaStream_t)stream;
-    bool stdh = fact;
-    for (int b = 0; stdh && b < NBF; ++b) stdh = P.hcos[b] == hStdCos[b] && P.hsin[b] == hStdSin[b];
-    const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? (stdh ? MODE_FACTS : MODE_FACT) : MODE_GEN)
-                                                      : MODE_REF;
     bool wth = false;
     for (int i = 0; i < a->n_tables; ++i) wth = wth || a->h_tables[i].w_th != 0.f;
+    bool stdh = fact;
+    for (int b = 0; stdh && b < NBF; ++b) stdh = P.hcos[b] == hStdCos[b] && P.hsin[b] == hStdSin[b];
+    const size_t htab = (a->rng_mode == GC_RNG_PRODUCTION && stdh && wth) ? (size_t)MAXH * NBF * 4 : 0;
+    const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : htab);
+    P.dyn_smem = (int)smem;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? (stdh ? MODE_FACTS : MODE_FACT) : MODE_GEN)
+                                                      : MODE_REF;
     if (mode == MODE_REF) return dispatch_k<MODE_REF, false>(P, K, (int)grid, smem, st);
     if (mode == MODE_FACTS)
-        return wth ? dispatch_k<MODE_FACT, true>(P, K, (int)grid, smem, st)  // w_th != 0: per-heading H_b
+        return wth ? dispatch_k<MODE_FACTS, true>(P, K, (int)grid, smem, st)  // H_b table in shared memory
                    : dispatch_k<MODE_FACTS, false>(P, K, (int)grid, smem, st);
     if (mode == MODE_FACT)
         return wth ? dispatch_k<MODE_FACT, true>(P, K, (int)grid, smem, st)

@@ -1,6 +1,6 @@
 """K2 time of the production samplers at the cfg3 shape (8 humans x 262,144 x 250): the
-factorised grid sampler vs the generic per-action softmax (a 96-action control set that is
-not a speed x heading grid)."""
+factorised grid sampler (plain and with a heading penalty w_theta) vs the generic
+per-action softmax (a 96-action control set that is not a speed x heading grid)."""
 import math
 import os
 import sys
@@ -40,6 +40,7 @@ def time_k2(cs, q, label, n=262144, steps=250, humans=8):
 def main():
     q = G.q_goal_progress(0.5)
     time_k2(G.ControlSet.grid(4, 24, 1.4), q, "grid(4, 24, 1.4)")
+    time_k2(G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5, (0.0, 0.2)), "grid(4, 24, 1.4), w_theta 0.2")
     r = np.random.default_rng(0)
     acts = [G.ControlAction(float(v), float(t)) for v, t in zip(r.uniform(0, 1.4, 96), r.uniform(-math.pi, math.pi, 96))]
     time_k2(G.ControlSet(acts), q, "96 random actions")
