@@ -719,6 +719,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     if (MODE == MODE_REF) { pool_step = pool_pre; ss_absorb(pool_step, 1u); }  // STEP_DRAWS
 
     const long long hbase = (long long)h * P.human_stride;
+    U4 rbk = U4{0u, 0u, 0u, 0u};  // K < 4: the block this lane drew for its turn (see below)
     bool overflow = false;  // a particle outside its reachable window (reported once at exit)
     for (int t = P.t_begin; t < P.t_end; ++t) {
         const int R = __ldg(&P.step_r[t - 1]);
@@ -733,10 +734,27 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         // particles (block counter: global particle index / 4, step, human stream, tag);
         // particle p takes word p % 4.  A thread's K = 4 particles are consecutive and
         // aligned, so each thread draws exactly one block per step and keeps no state.
+        // With K < 4 the G = 4 / K lanes of a particle group take turns: every G steps
+        // lane j of the group draws the block of step t + j, and each step the group reads
+        // that step's words from the lane holding them (shuffles) -- one block per lane
+        // per G steps instead of G lanes drawing the same block every step.
         U4 rb = U4{0u, 0u, 0u, 0u};
-        if (MODE != MODE_REF)
-            rb = philox4x32(U4{(unsigned)((pbase + tid * K + P.p_offset) >> 2), (unsigned)(t - 1), sc2, sk_hi ^ 0xA11CEu},
-                            PHK0, PHK1);
+        if (MODE != MODE_REF) {
+            const unsigned g4 = (unsigned)((pbase + tid * K + P.p_offset) >> 2);
+            if (K == 4) {
+                rb = philox4x32(U4{g4, (unsigned)(t - 1), sc2, sk_hi ^ 0xA11CEu}, PHK0, PHK1);
+            } else {
+                constexpr int G = 4 / K;
+                const int sgrp = (t - 1) % G;  // this step's offset in the group's turn
+                if (sgrp == 0)
+                    rbk = philox4x32(U4{g4, (unsigned)(t - 1 + (tid % G)), sc2, sk_hi ^ 0xA11CEu}, PHK0, PHK1);
+                const int src = (tid & 31) - (tid % G) + sgrp;  // lane holding step t's block
+                rb.x = __shfl_sync(0xffffffffu, rbk.x, src);
+                rb.y = __shfl_sync(0xffffffffu, rbk.y, src);
+                rb.z = __shfl_sync(0xffffffffu, rbk.z, src);
+                rb.w = __shfl_sync(0xffffffffu, rbk.w, src);
+            }
+        }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + tid * K + k;

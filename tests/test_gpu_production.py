@@ -150,3 +150,25 @@ def test_production_hypothesis_frequencies():
                          want_hyp=True)
     freq = np.bincount(out["hyp"][0].cpu().numpy(), minlength=4) / 200_000
     np.testing.assert_allclose(freq, probs, atol=0.01)
+
+
+def test_production_streams_independent_of_launch_shape():
+    """A human's production draws depend only on (seed, stream, particle, step): alone
+    (small launch: K = 1 particle per thread, lanes take turns drawing Philox blocks) and as
+    the first of 160 humans (K = 4, one block per thread per step) its layers are identical."""
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    space = G.HypothesisSpace(G.RationalitySet.log_spaced(5), G.GoalSet(np.array([[8.5, 5.0], [1.5, 7.0]])))
+    spec = G.GridSpec(100, 100, 0.1)
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, 0.1, dev)
+    lw = np.log(np.random.default_rng(4).dirichlet(np.ones(space.size)))
+    lw -= np.log(np.exp(lw).sum())
+    job = PR.HumanJob(G.HumanState(5.0, 5.0), lw, space.beta_of, space.goal_xy_of, 99, (), 0)
+    others = [PR.HumanJob(G.HumanState(2.0 + 0.03 * i, 3.0), lw, space.beta_of, space.goal_xy_of, 99, (), 0)
+              for i in range(159)]
+    n, T = 4096, 9  # 9 steps: K = 1 takes turns over 4 steps, a partial last turn included
+    alone = PR.run_predict([job], [tab], n, T, 0.1, 0.0, spec, "production")["layers"][0].cpu().numpy()
+    multi = PR.run_predict([job] + others, [tab], n, T, 0.1, 0.0, spec, "production")["layers"][0].cpu().numpy()
+    assert alone.sum() > 0
+    np.testing.assert_array_equal(alone, multi)
