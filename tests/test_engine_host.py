@@ -18,9 +18,39 @@ def test_chunk_bounds_partition_the_horizon_on_philox_phase(steps, chunks, taper
     assert b[0][0] == 1 and b[-1][1] == steps + 1
     assert all(t0 < t1 for t0, t1 in b)
     assert all(b[i][1] == b[i + 1][0] for i in range(len(b) - 1))
-    # production streams draw one Philox block per 4 steps: every chunk starts on a block
+    # chunks start on 4-step boundaries (the K < 4 production path takes turns over up to
+    # 4 steps; the engine keeps this phase for every launch shape)
     assert all((t0 - 1) % 4 == 0 for t0, _ in b)
     assert len(b) <= max(1, chunks)
+
+
+class _Geo:
+    def __init__(self, steps, budget_kb, cells=400, res=0.1, dt=0.02, reduce=None):
+        from paper_2603_01122_b200.occupancy import GridSpec
+        from paper_2603_01122_b200.tables import Geometry
+        self.cfg = EngineConfig(steps=steps, window_budget_kb=budget_kb)
+        self.geo = Geometry(GridSpec(cells, cells, res), steps, 1.4 * dt, 0.1, "cpu")
+        self.counts_reduce = reduce
+
+
+@pytest.mark.parametrize("steps", [1, 4, 100, 248, 250, 500, 1000])
+@pytest.mark.parametrize("budget", [0.0, 46.0, 64.0])
+def test_window_bounds_split_long_horizons_on_4_step_boundaries(steps, budget):
+    e = _Geo(steps, budget)
+    b = CycleEngine.window_bounds(e)
+    assert b[0][0] == 1 and b[-1][1] == steps + 1 and len(b) <= 2
+    if len(b) == 2:
+        t = b[0][1]
+        assert (t - 1) % 4 == 0 and budget > 0
+        cells = e.geo.win_cells
+
+        def kb(c):
+            return (((int(c) + 1) // 2 + 3) // 4 * 16 + 4096) / 1024
+        assert kb(cells[t - 2]) <= budget < kb(cells[steps - 1])   # the prefix fits, the whole does not
+    if budget == 0.0 or steps <= 248:
+        assert b == [(1, steps + 1)]
+    # particle sharding keeps one launch (its counts are reduced across GPUs before K3)
+    assert CycleEngine.window_bounds(_Geo(steps, budget, reduce=lambda c: c)) == [(1, steps + 1)]
 
 
 def test_tapered_chunks_shrink_toward_the_end():
