@@ -34,15 +34,17 @@ def exact_action_probs(z, belief, cs, q, space):
 
 
 def one_step_tv(q_factory, n=1 << 22, weights=None, mask_v=None, goals=((0.5, 0.3), (0.1, 0.15)),
-                speeds=4, betas=(0.3, 2.0, 9.0)):
+                speeds=4, betas=(0.3, 2.0, 9.0), origin=(0.0, 0.0), shape=(400, 400)):
     cs = G.ControlSet.grid(speeds, 24, 1.4)
     q = q_factory()
     if mask_v is not None:
         q = G.mask_stationary(q, cs, mask_v)
     space = G.HypothesisSpace(G.RationalitySet(betas), G.GoalSet(np.array(goals)))
     b = G.JointBelief.from_probs(weights if weights is not None else np.full(space.size, 1.0 / space.size))
-    spec = G.GridSpec(400, 400, 0.001)
-    z = G.HumanState(0.2005, 0.2005)
+    W, H = shape
+    spec = G.GridSpec(W, H, 0.001, origin)
+    z = G.HumanState(origin[0] + 0.2005, origin[1] + 0.2005)
+    goals = tuple((gx + origin[0], gy + origin[1]) for gx, gy in goals)
     dev = torch.device("cuda")
     tab = PR.action_tables(cs, q, 0.1, dev)
     job = PR.HumanJob(z, b.log_weights, space.beta_of, space.goal_xy_of, 12345, (), 0)
@@ -54,9 +56,9 @@ def one_step_tv(q_factory, n=1 << 22, weights=None, mask_v=None, goals=((0.5, 0.
     x = np.float32(z.x) + disp[:, 0]
     y = np.float32(z.y) + disp[:, 1]
     inv = np.float32(1.0) / np.float32(0.001)
-    ix = np.clip(np.floor((x - np.float32(0)) * inv).astype(int), 0, 399)
-    iy = np.clip(np.floor((y - np.float32(0)) * inv).astype(int), 0, 399)
-    exact = np.zeros((400, 400))
+    ix = np.clip(np.floor((x - np.float32(origin[0])) * inv).astype(int), 0, W - 1)
+    iy = np.clip(np.floor((y - np.float32(origin[1])) * inv).astype(int), 0, H - 1)
+    exact = np.zeros((H, W))
     np.add.at(exact, (iy, ix), p)
     return 0.5 * np.abs(layer - exact).sum(), tab.factorised
 
@@ -79,6 +81,12 @@ def test_factorised_speed_counts(speeds):
     """Top-speed normalisation of the speed weights for 2, 3 and 4 speeds (n_speeds - 1
     moving speeds + stay), including a distant goal (small Q = 2^-kr)."""
     tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5), speeds=speeds, goals=((0.5, 0.3), (40.0, 30.0)))
+    assert fact and tv < 0.006, tv
+
+
+def test_factorised_offset_origin_and_rectangular_grid():
+    """Grid units u = (x - origin) / res with a negative origin and a 420 x 380 grid."""
+    tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5), origin=(-1.5, 2.25), shape=(420, 380))
     assert fact and tv < 0.006, tv
 
 
