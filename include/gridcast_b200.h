@@ -124,7 +124,7 @@ typedef struct {
     /* horizon chunking: run steps [t_begin, t_end) (1-based; 0, 0 = the whole horizon).
      * A chunk starting after step 1 resumes the particles saved by the previous chunk in
      * d_state_xy (float2 per particle) / d_state_hyp (uint8 hypothesis index); chunk
-     * starts must satisfy (t_begin - 1) % 4 == 0 (Philox block phase). */
+     * starts must satisfy (t_begin - 1) % 4 == 0 (the production streams' lane-turn phase). */
     int32_t t_begin, t_end;
     float *d_state_xy;
     uint8_t *d_state_hyp;

@@ -107,7 +107,7 @@ __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, in
 }
 
 // MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
-// after the window and the touched list; absent from the production kernel)
+// after the window and the first-touch slots; absent from the production kernel)
 struct alignas(16) SmemAct {
     float ax[MAXM], ay[MAXM], aat[MAXM], adx[MAXM], ady[MAXM];
 };

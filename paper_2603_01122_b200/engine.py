@@ -226,7 +226,7 @@ class CycleEngine:
     # ---- the device cycle ---------------------------------------------------------------
     def chunk_bounds(self, chunks: int):
         """1-based [t0, t1) step ranges of ``chunks`` horizon chunks; every chunk start is
-        1 + a multiple of 4 (Philox phase of the production streams).  Chunk sizes shrink
+        1 + a multiple of 4 (the turn phase of the production streams' small-launch path).  Chunk sizes shrink
         geometrically (``cfg.chunk_taper``) toward the end of the horizon."""
         T = self.cfg.steps
         chunks = max(1, min(chunks, (T + 3) // 4))
@@ -242,7 +242,7 @@ class CycleEngine:
     def window_bounds(self):
         """1-based [t0, t1) ranges of a one-chunk cycle: the whole horizon, or -- when its
         reachable-cell windows outgrow ``cfg.window_budget_kb`` of shared memory -- the
-        longest prefix (ending on a Philox block boundary) whose windows fit, then the rest
+        longest prefix (ending on a 4-step boundary) whose windows fit, then the rest
         (K2 adds those steps straight to global memory).  Bit-identical either way."""
         T, cells = self.cfg.steps, self.geo.win_cells
         budget = self.cfg.window_budget_kb * 1024
