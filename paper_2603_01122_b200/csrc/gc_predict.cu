@@ -107,7 +107,7 @@ __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, in
 }
 
 // MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
-// after the window and the first-touch slots; absent from the production kernel)
+// after the window; absent from the production kernel)
 struct alignas(16) SmemAct {
     float ax[MAXM], ay[MAXM], aat[MAXM], adx[MAXM], ady[MAXM];
 };
@@ -633,9 +633,6 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         }
     }
     unsigned *win = reinterpret_cast<unsigned *>(smem_dyn);
-    // fw[k NT]: the window word this thread's particle slot k added to first this step, or
-    // -1 (that thread owns the word's flush)
-    int *fw = nullptr;
     int words = 0;  // window capacity (u32 words)
     if (P.smem_window) {
         // the largest window of THIS launch's steps (a horizon chunk may fit in shared
@@ -643,8 +640,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         const int R = __ldg(&P.step_r[P.t_end - 2]);
         words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
         for (int i = tid; i < words; i += NT) win[i] = 0u;
-        fw = reinterpret_cast<int *>(win + ((words + 3) & ~3)) + tid;
-        GC_DCHECK((((words + 3) & ~3) + NT * K) * 4 <= P.dyn_smem);
+        GC_DCHECK(((words + 3) & ~3) * 4 <= P.dyn_smem);
     }
     const bool qg = __syncthreads_and(qg_ok) != 0;
 
@@ -730,6 +726,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         GC_DCHECK(__ldg(&P.step_off[t - 1]) + (long long)ww * wh <= P.human_stride);
         uint64_t sk0 = 0, sk1 = 0;
         int key_chunk = -1;
+        // fwr[k]: the window word particle slot k added to first this step, or -1 (this
+        // thread then owns that word's flush)
+        int fwr[K];
         // production streams: one Philox4x32-10 block per step for every 4 consecutive
         // particles (block counter: global particle index / 4, step, human stream, tag);
         // particle p takes word p % 4.  A thread's K = 4 particles are consecutive and
@@ -815,7 +814,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 else local = ly * ww + lx;
             }
             // the thread whose add finds a window word zero owns that word's flush this
-            // step: it remembers the word in its own shared slot (no list, no ballot)
+            // step: it remembers the word in a register (no list, no ballot)
             if (P.smem_window) {
                 int f = -1;
                 if (local >= 0) {
@@ -826,7 +825,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                                   (off & 2u) ? 0x10000u : 1u) == 0u)
                         f = local >> 1;
                 }
-                fw[k * NT] = f;  // this thread's slot k (conflict-free)
+                fwr[k] = f;
             } else if (local >= 0) {
                 GC_DCHECK(local < ww * wh);
                 atomicAdd(&gcount[local], 1u);
@@ -838,7 +837,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             // reduction per nonzero cell, then the word is zeroed for the next step
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const int wi = fw[k * NT];
+                const int wi = fwr[k];
                 if (wi < 0) continue;
                 GC_DCHECK(wi < words);
                 const unsigned w = win[wi];
@@ -1066,7 +1065,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.ppc = ppc;
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
-    const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4 + (size_t)NT * K * 4;
+    const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4;
     // shared-memory windows whenever they fit (robust to coherent particle clouds);
     // GC_PREDICT_GLOBAL_HIST=1 forces direct global reductions (tuning knob)
     static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();

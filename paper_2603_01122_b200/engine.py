@@ -69,7 +69,7 @@ class EngineConfig:
     # horizon chunking (chunks > 1): chunk c spans ~ chunk_taper^c of the horizon, so the
     # last chunks -- whose D2H cannot overlap later compute -- are short; 1.0 = uniform
     chunk_taper: float = 0.5
-    # shared-memory budget (KB) of K2's count window + first-touch slots: a one-chunk
+    # shared-memory budget (KB) of K2's count window: a one-chunk
     # horizon whose last windows exceed it is split so its first part still runs on
     # shared-memory windows.  Off by default: at the cfg4 shard (T = 500, 2^20 particles
     # per human) the split measured 42.8 ms per cycle against 40.4 ms on the global path
@@ -247,8 +247,8 @@ class CycleEngine:
         T, cells = self.cfg.steps, self.geo.win_cells
         budget = self.cfg.window_budget_kb * 1024
 
-        def fits(c):  # u16 counters two per word (rounded to 4 words) + 4 KB first-touch slots
-            return ((int(c) + 1) // 2 + 3) // 4 * 16 + 4096 <= budget
+        def fits(c):  # u16 counters two per word (rounded to 4 words)
+            return ((int(c) + 1) // 2 + 3) // 4 * 16 <= budget
 
         if budget <= 0 or fits(cells[T - 1]) or self.counts_reduce is not None:
             return [(1, T + 1)]

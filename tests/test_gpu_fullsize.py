@@ -88,12 +88,12 @@ def test_cfg4_shard_global_histogram_path_conserves_particles():
 
 @pytest.mark.parametrize("mode", ["production", "reference"])
 def test_long_horizon_window_split_equals_global_path(mode):
-    """T = 500 (cfg4 shape): the engine runs steps 1..248 on shared-memory windows and the
+    """T = 500 (cfg4 shape): the engine runs steps 1..264 on shared-memory windows and the
     rest on global atomics (two launches, particle state handed over); bit-identical to
     the whole horizon on the global path (window_budget_kb=0)."""
     n = 65536 if mode == "production" else 4096
     a = run("cfg4_rank", mode=mode, humans=2, n=n, budget_kb=46.0)
-    assert a.window_bounds() == [(1, 249), (249, 501)]
+    assert a.window_bounds() == [(1, 265), (265, 501)]
     np.testing.assert_array_equal(window_sums(a), n)
     ua = a.unions[0].cpu().numpy()
     del a
