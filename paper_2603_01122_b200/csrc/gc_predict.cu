@@ -6,8 +6,9 @@
 // an action per particle, Euler-steps, maps the particle to its cell and adds it (shared
 // atomic on a u16 half-word) into a shared-memory privatised window covering the cells
 // the human can reach by that step.  After a CTA barrier the touched cells (each
-// remembered by the thread whose add found its word zero) are flushed with one global reduction each into the human's
-// windowed count buffer, and zeroed.  HBM sees only those reductions.
+// remembered by the thread whose add found its word zero) are flushed with one global
+// reduction each into the human's windowed count buffer, and zeroed.  HBM sees only those
+// reductions.
 //
 // Two arithmetic families:
 //   MODE_REF  : the reference float32 step op for op: per-action
@@ -415,7 +416,7 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     y += d.y;
 }
 
-// MODE_FACTS (standard heading set, n_speeds <= 4, w_th = 0): the factorised sampler with
+// MODE_FACTS (standard heading set, n_speeds <= 4): the factorised sampler with
 //  (1) speed weights normalised at the TOP speed instead of by a max shift: with
 //      Q = 2^-kr, G_a / G_top = Q^(top-a) 2^(c (top^2 - a^2)), so one ex2 (Q) and a few
 //      products replace 4 ex2; the per-hypothesis powers of 2^c (Ka, Kb, Kc) are staged
@@ -426,6 +427,8 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
 //      sum runs in the order (0, 1, 12, 13, 2, 3, 14, 15, ...): index i <-> heading
 //      2(i>>2) + (i&1) + 12((i>>1)&1); the prologue stores the chosen-heading (cos, sin) and
 //      the displacements in that order, so the search result indexes them directly.
+//  (3) WTH (w_th != 0): heading weights H_b = exp(-beta w_th theta_b^2) per hypothesis from a
+//      shared-memory table in the same order (Htab), one LDS.128 per four headings.
 template <bool WTH>
 __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &P, const float *Htab, float &x,
                                               float &y, int h, float u1, bool qg) {
