@@ -522,7 +522,7 @@ def main():
     ap.add_argument("--no-ref-mode", action="store_true")
     ap.add_argument("--lat-cycles", type=int, default=LAT_CYCLES,
                     help="cycles the p50/p99 latencies are taken over (at least --steps)")
-    ap.add_argument("--chunks", type=int, default=6, help="horizon chunks of the e2e cycle (D2H overlap)")
+    ap.add_argument("--chunks", type=int, default=7, help="horizon chunks of the e2e cycle (D2H overlap)")
     ap.add_argument("--chunk-taper", type=float, default=0.5, help="chunk size ratio (1.0 = uniform chunks)")
     ap.add_argument("--cpu-t", type=int, default=25)
     ap.add_argument("--ref-t", type=int, default=10)
