@@ -102,9 +102,12 @@ def test_predict_delta_mass_and_smoothing(mode):
             assert (st.layers[k] >= 0).all()
 
 
-def test_deterministic_for_any_worker_count():
+@pytest.mark.parametrize("mode", MODES)
+def test_deterministic_for_any_worker_count(mode):
+    """test_prediction.py:128-136: bitwise identical for any worker count -- and, on the GPU,
+    for repeated launches (integer count atomics, order-independent max)."""
     z0, cs, q, space, spec = lattice()
-    cfg = G.PredictionConfig(n=8192, steps=3, dt=1.0, smoothing_sigma=0.1, seed=11)
+    cfg = G.PredictionConfig(n=8192, steps=3, dt=1.0, smoothing_sigma=0.1, seed=11, mode=mode)
     stacks = [G.predict(z0, G.init_belief(space), cfg, cs, q, space, spec, workers=w) for w in (None, 1, 2, 5)]
     for s in stacks[1:]:
         np.testing.assert_array_equal(s.layers, stacks[0].layers)

@@ -152,3 +152,22 @@ def test_cfg3_production_tv_within_reference_seed_spread():
     # and every layer is a probability distribution
     mass = layers["p"].sum(dim=(2, 3))
     assert float((mass - 1).abs().max()) < 1e-9
+
+
+def test_cfg3_graph_replays_are_bitwise_reproducible():
+    """The captured cycle replayed twice on the same inputs (same cycle seed) gives the same
+    fused union bit for bit: production streams are counter-based, counts are integer
+    atomics, the union is an order-independent max."""
+    sc = make_scene("cfg3", cycles=2, humans=8)
+    cfg = EngineConfig(n=sc.n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, seed=3, mode="production")
+    eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
+    eng.prime(sc.prev_xy)
+    eng.stage(sc.track[0], buf=0)
+    g = eng.capture(buf=0, with_h2d=True, with_update=False)
+    g.replay()
+    torch.cuda.synchronize()
+    first = eng.unions[0].cpu().numpy()
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(eng.unions[0].cpu().numpy(), first)
+    assert first.max() > 0
