@@ -447,12 +447,11 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     float G1, G2, G3, Z0;
     if (qg) {
         const float Q = ex2_approx(nkr), Q2 = Q * Q;
-        if (na == 4) {
+        if (na == 4) {  // the standard grid: straight-line code on the common path
             G3 = 1.f; G2 = Q * hp.w; G1 = Q2 * hq.x; Z0 = Q2 * Q * hq.y;
-        } else if (na == 3) {
-            G3 = 0.f; G2 = 1.f; G1 = Q * hp.w; Z0 = Q2 * hq.x;
         } else {
-            G3 = 0.f; G2 = 0.f; G1 = 1.f; Z0 = Q * hp.w;
+            const bool p3 = na == 3;
+            G3 = 0.f; G2 = p3 ? 1.f : 0.f; G1 = p3 ? Q * hp.w : 1.f; Z0 = p3 ? Q2 * hq.x : Q * hp.w;
         }
     } else {
         const float c2 = hq.z;
