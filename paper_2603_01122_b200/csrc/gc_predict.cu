@@ -641,8 +641,9 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         // memory when the whole horizon does not): the host sized it from max_win_cells
         const int R = __ldg(&P.step_r[P.t_end - 2]);
         words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
-        for (int i = tid; i < words; i += NT) win[i] = 0u;
-        GC_DCHECK(((words + 3) & ~3) * 4 <= P.dyn_smem);
+        // + one sink word that lanes without a cell add to (branch-free add; never flushed)
+        for (int i = tid; i <= words; i += NT) win[i] = 0u;
+        GC_DCHECK(((words + 1 + 3) & ~3) * 4 <= P.dyn_smem);
     }
     const bool qg = __syncthreads_and(qg_ok) != 0;
 
@@ -818,16 +819,14 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             // the thread whose add finds a window word zero owns that word's flush this
             // step: it remembers the word in a register (no list, no ballot)
             if (P.smem_window) {
-                int f = -1;
-                if (local >= 0) {
-                    // u16 counter `local`: byte offset 2 local, in word (2 local) & ~3
-                    const unsigned off = 2u * (unsigned)local;
-                    GC_DCHECK(local < ww * wh && (int)(off >> 2) < words);
-                    if (atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
-                                  (off & 2u) ? 0x10000u : 1u) == 0u)
-                        f = local >> 1;
-                }
-                fwr[k] = f;
+                // u16 counter `local`: byte offset 2 local, in word (2 local) & ~3; a lane
+                // without a cell (padding) adds to the sink word instead -- no branch
+                const bool has = local >= 0;
+                const unsigned off = has ? 2u * (unsigned)local : 4u * (unsigned)words;
+                GC_DCHECK(!has || (local < ww * wh && (int)(off >> 2) < words));
+                const unsigned old = atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
+                                               (off & 2u) ? 0x10000u : 1u);
+                fwr[k] = (has && old == 0u) ? (local >> 1) : -1;
             } else if (local >= 0) {
                 GC_DCHECK(local < ww * wh);
                 atomicAdd(&gcount[local], 1u);
@@ -1067,7 +1066,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.ppc = ppc;
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
-    const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 3) & ~3) * 4;
+    const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 1 + 3) & ~3) * 4;  // + sink word
     // shared-memory windows whenever they fit (robust to coherent particle clouds);
     // GC_PREDICT_GLOBAL_HIST=1 forces direct global reductions (tuning knob)
     static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();
