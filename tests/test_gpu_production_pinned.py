@@ -1,0 +1,42 @@
+"""GPU: production-mode outputs pinned to digests (a kernel-change regression guard).
+
+Production mode is not compared with the reference bit for bit (its streams are the B200
+Philox4x32 streams, checked in distribution by test_gpu_production.py), but for a fixed
+seed it is deterministic.  These digests pin its counts and layers for the standard
+symmetric sampler (4 / 3 / 2 speeds, with and without a heading penalty) and the generic
+factorised sampler (16 headings), so an optimisation of K2 that is meant to be
+bit-identical (e.g. a different search or flush) is checked as such.  An intended change
+of the production streams or arithmetic updates the digests here, with `python
+tools/hash_production.py` as the generator.
+"""
+
+import importlib.util
+import os
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+PINNED = {
+    "grid(4,24)": "b47985fd57c60da3",
+    "grid(4,24) w_theta": "f9633af7f1ddb8da",
+    "grid(3,24)": "8bd6e4cb9f228571",
+    "grid(2,24)": "9f97898cdc7472c8",
+    "grid(4,16)": "1363a77b2fdb4405",
+}
+
+
+def _tool():
+    spec = importlib.util.spec_from_file_location("hash_production", os.path.join(ROOT, "tools", "hash_production.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_production_outputs_match_pinned_digests():
+    got = {label: d for label, _f, d in _tool().cases()}
+    assert got == PINNED

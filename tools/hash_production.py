@@ -37,8 +37,10 @@ def digest(cs, q, n=65536, steps=60, humans=4):
     return tab.factorised, m.hexdigest()[:16]
 
 
-def main():
+def cases():
+    """(label, factorised, digest) of each pinned case (tests/test_gpu_production_pinned.py)."""
     q = G.q_goal_progress(0.5)
+    out = []
     for label, cs, qq in [
         ("grid(4,24)", G.ControlSet.grid(4, 24, 1.4), q),
         ("grid(4,24) w_theta", G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5, (0.0, 0.2))),
@@ -47,6 +49,12 @@ def main():
         ("grid(4,16)", G.ControlSet.grid(4, 16, 1.4), q),
     ]:
         f, d = digest(cs, qq)
+        out.append((label, f, d))
+    return out
+
+
+def main():
+    for label, f, d in cases():
         print(f"{label:22s} factorised={f} {d}")
 
 
