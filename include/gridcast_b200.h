@@ -36,6 +36,23 @@ typedef enum {
     GC_WINDOW_OVERFLOW = 6     /* a particle left its reachable-cell window (internal bug) */
 } gc_status;
 
+/* Bits of gc_predict's device status word d_error (raised by the kernel, stream-ordered;
+ * the Python mirror reads it after the launch and raises RuntimeError / ValueError):
+ *   WINDOW_OVERFLOW  a particle left its reachable-cell window (internal bug);
+ *   HYPOTHESES       a human with d_hyp_off[h+1] - d_hyp_off[h] outside 1..GC_MAX_HYPOTHESES
+ *                    (its CTAs return without counting anything);
+ *   WINDOW_CAPACITY  max_win_cells under-reports the windows of the launch's steps (the
+ *                    shared-memory window would not fit; the launch counts nothing). */
+#define GC_ERRBIT_WINDOW_OVERFLOW (1u << 6)
+#define GC_ERRBIT_HYPOTHESES (1u << 8)
+#define GC_ERRBIT_WINDOW_CAPACITY (1u << 9)
+
+/* Size limits of the kernels (shared-memory tables): hypotheses per human (|B| x |G|)
+ * and actions per control set.  gc_belief_update marks a human outside 1..GC_MAX_HYPOTHESES
+ * with GC_BAD_ARG in d_status; gc_predict raises GC_ERRBIT_HYPOTHESES. */
+#define GC_MAX_HYPOTHESES 128
+#define GC_MAX_ACTIONS 256
+
 /* Utility families (agents.py:245-296).  *_FULL = the reference's `base` (with the
  * row-constant -|rel|^2), used when a stationary mask dropped base_policy (belief.py:222). */
 enum { GC_Q_GOAL_PROGRESS = 0, GC_Q_GOAL_PROGRESS_FULL = 1, GC_Q_DEFAULT = 2, GC_Q_TABLE = 3 };
@@ -114,13 +131,14 @@ typedef struct {
     const int32_t *d_step_r;   /* (steps,) */
     const int64_t *d_step_off; /* (steps,) */
     int64_t human_stride;
-    int32_t max_win_cells;     /* max (2 r_t + 1)^2 over the steps of this launch [t_begin, t_end) */
+    int32_t max_win_cells;     /* max (2 r_t + 1)^2 over the steps of this launch [t_begin, t_end):
+                                  sizes the shared-memory window (too small -> GC_ERRBIT_WINDOW_CAPACITY) */
     int32_t _pad2;
     uint32_t *d_counts;
     /* optional outputs */
     int32_t *d_hyp_out;        /* (n_humans, n) sampled hypothesis indices or NULL */
     float *d_xy_out;           /* (n_humans, n, 2) final positions or NULL */
-    uint32_t *d_error;         /* device status word (GC_WINDOW_OVERFLOW bit) or NULL */
+    uint32_t *d_error;         /* device status word (GC_ERRBIT_* bits, OR-ed) or NULL */
     /* horizon chunking: run steps [t_begin, t_end) (1-based; 0, 0 = the whole horizon).
      * A chunk starting after step 1 resumes the particles saved by the previous chunk in
      * d_state_xy (float2 per particle) / d_state_hyp (uint8 hypothesis index); chunk
@@ -185,7 +203,8 @@ typedef struct {
     int32_t clamp_on_mismatch;        /* 1: update with the nearest action anyway (sim.py:469-478) */
     const double *d_prior;            /* (sum |H|,) log weights */
     double *d_post;                   /* (sum |H|,) log weights (may alias d_prior) */
-    int32_t *d_status;                /* (n_humans,) GC_OK / GC_SNAP_MISMATCH */
+    int32_t *d_status;                /* (n_humans,) GC_OK / GC_SNAP_MISMATCH / GC_EMPTY_CONTROL_SET /
+                                         GC_BAD_ARG (0 or > GC_MAX_HYPOTHESES hypotheses) */
     int32_t *d_action;                /* (n_humans,) snapped action index or NULL */
 } gc_belief_args;
 

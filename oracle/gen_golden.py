@@ -17,6 +17,17 @@ not exist on the GPU box).  Cases (reference file:line they exercise):
                                                                 sim.py:489-504
   exact.npz     exact_predict() on the lattice instance         prediction.py:303-377
   naive_*.npz   predict_naive() float64 per-particle loop        prediction.py:258-300
+  cfg3_cycle.npz  the headline shape: 8 humans x 262,144 particles of the cfg3 scene after
+                10 belief updates, 25 steps, sim-style seed/prefix/masked Q, sigma 0.1,
+                per-human counts, max union and time union       sim.py:455-505
+  long_cfg4.npz   a cfg4 human (T = 500: windows beyond shared memory -> K2's global-
+                histogram path), 4096 particles                 prediction.py:223-255
+  uniforms_cfg1.npz the reference's own pre-drawn uniforms of the cfg1_s0 case (hypothesis
+                and step draws) for GC_RNG_UNIFORMS            prediction.py:128-131, :186-192
+
+    PYTHONPATH=/root/reference/pkg/src python -m oracle.gen_golden [case ...]
+regenerates only the named cases (philox exp predict belief smooth multi exact collision
+gcst mppi naive cfg3_cycle long_cfg4 uniforms).
 """
 
 from __future__ import annotations
@@ -460,20 +471,176 @@ def gen_mppi(G):
     np.savez_compressed(os.path.join(OUT, "mppi.npz"), layers=layers, **out)
 
 
+def _sparse_counts(counts_list):
+    """(T, H, W) per-step counts -> (idx (nnz, 3) int32 [t, iy, ix], val int32)."""
+    idx, val = [], []
+    for t, c in enumerate(counts_list):
+        iy, ix = np.nonzero(c)
+        idx.append(np.stack([np.full(len(iy), t), iy, ix], 1))
+        val.append(c[iy, ix])
+    return np.concatenate(idx).astype(np.int32), np.concatenate(val).astype(np.int32)
+
+
+def _sparse_layers(layers):
+    nz = np.nonzero(layers)
+    return np.stack(nz, 1).astype(np.int32), layers[nz]
+
+
+def _digest(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _scene_beliefs(G, sc, n_updates=10):
+    """sim.py:455-485 over the scene's warm-up track: per human the posterior after
+    n_updates observations (ControlSnapMismatch -> retry with snap_tol=inf), the last
+    heading and the stationary flag."""
+    from gridcast.belief import ControlSnapMismatch, update_belief
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    out = []
+    for i, sp in enumerate(sc.spaces):
+        space = G.HypothesisSpace(G.RationalitySet.log_spaced(5), G.GoalSet(np.array(sp.goals.positions)))
+        b = G.init_belief(space)
+        heading, stationary = 0.0, False
+        for k in range(1, n_updates + 1):
+            prev = G.HumanState(*sc.warmup_track[k - 1][i])
+            obs = G.HumanState(*sc.warmup_track[k][i])
+            try:
+                b = update_belief(b, prev, obs, 0.1, cs, q, space, fallback_theta=heading)
+            except ControlSnapMismatch:
+                b = update_belief(b, prev, obs, 0.1, cs, q, space, fallback_theta=heading, snap_tol=math.inf)
+            moved = math.hypot(obs.x - prev.x, obs.y - prev.y)
+            stationary = moved / 0.1 < 0.05
+            if moved > 1e-9:
+                heading = math.atan2(obs.y - prev.y, obs.x - prev.x)
+        out.append((space, b, heading, stationary))
+    return cs, q, out
+
+
+def gen_cfg3_cycle(G, steps=25):
+    """The headline launch shape from the live reference: the bench's cfg3 scene (8 humans,
+    each its own 4-goal HypothesisSpace, 262,144 particles, 400x400 @ 0.1 m, dt 0.02), the
+    10th cycle of sim.run_episode's pattern (belief after 10 updates, seed
+    derive_seed(0, 7, 9), prefix (2, i), masked Q when stationary), sigma 0.1, truncated to
+    ``steps`` steps; per-human counts, hypothesis/position digests, the max union and its
+    time union (sim.py:489-505)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from gridcast import rng
+    from gridcast.belief import mask_stationary
+    from gridcast.occupancy import emplace_counts, smooth_values, union_max
+    from gridcast.prediction import (ParticleBatch, PredictionConfig, predict, propagate_step,
+                                     sample_hypotheses)
+    from paper_2603_01122_b200.scenario import make_scene
+    sc = make_scene("cfg3", cycles=2)
+    cs, q, beliefs = _scene_beliefs(G, sc)
+    qm = mask_stationary(q, cs, 0.5)
+    spec = G.GridSpec(400, 400, 0.1)
+    n, dt, sigma = sc.n, sc.dt, 0.1
+    seed = rng.derive_seed(0, 7, 9)
+    humans, per_layers, payload = [], [], {}
+    for i, (space, b, heading, stationary) in enumerate(beliefs):
+        z0 = G.HumanState(*sc.warmup_track[10][i])
+        qi = qm if stationary else q
+        pre = (rng.HUMAN_PREFIX, i)
+        hyp = sample_hypotheses(b, n, seed, prefix=pre)
+        batch = ParticleBatch.duplicated(z0, hyp)
+        counts, layers = [], np.empty((steps, spec.height, spec.width))
+        for t in range(1, steps + 1):
+            batch = propagate_step(batch, cs, qi, space, dt, seed, step=t, workers=8, prefix=pre)
+            c = emplace_counts(batch.xy, spec)
+            counts.append(c.astype(np.int64))
+            layers[t - 1] = smooth_values(c / n, spec, sigma)
+        if i == 0:  # the loop above is predict() (prediction.py:243-255) verbatim: check it
+            cfg = PredictionConfig(n=n, steps=steps, dt=dt, smoothing_sigma=sigma, seed=seed)
+            st = predict(z0, b, cfg, cs, qi, space, spec, workers=8, prefix=pre)
+            assert np.array_equal(st.layers, layers)
+        per_layers.append(layers)
+        ci, cv = _sparse_counts(counts)
+        payload[f"count_idx_{i}"], payload[f"count_val_{i}"] = ci, cv
+        li, lv = _sparse_layers(layers)
+        payload[f"layer_idx_{i}"], payload[f"layer_val_{i}"] = li, lv
+        humans.append(dict(start=[z0.x, z0.y], goals=np.asarray(space.goals.positions).tolist(),
+                           log_w=b.log_weights.tolist(), stationary=bool(stationary), heading=heading,
+                           hyp_sha256=_digest(hyp.astype(np.int32)),
+                           xy_sha256=_digest(batch.xy.astype(np.float32))))
+        print("cfg3_cycle human", i, "nnz", len(cv), "stationary", stationary)
+    u = np.stack([union_max([G.OccupancyGrid(spec, L[k]) for L in per_layers]).values for k in range(steps)])
+    tu = np.maximum.accumulate(u, axis=0)
+    payload["union_idx"], payload["union_val"] = _sparse_layers(u)
+    payload["tunion_idx"], payload["tunion_val"] = _sparse_layers(tu)
+    meta = dict(n=n, steps=steps, dt=dt, sigma=sigma, seed=str(seed), cycle=9, grid=[400, 400, 0.1, [0.0, 0.0]],
+                warmup_track=np.asarray(sc.warmup_track).tolist(), humans=humans,
+                betas=list(G.RationalitySet.log_spaced(5).betas))
+    np.savez_compressed(os.path.join(OUT, "cfg3_cycle.npz"), meta=json.dumps(meta), **payload)
+
+
+def gen_long_cfg4(G, n=4096, steps=500):
+    """A cfg4 human (T = 500, dt 0.02, 400x400): its reachable windows (285 x 285 cells at the
+    last step) exceed shared memory, so K2 takes the global-histogram path."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from gridcast.occupancy import emplace_counts, smooth_values
+    from gridcast.prediction import ParticleBatch, propagate_step, sample_hypotheses
+    from oracle import model
+    from paper_2603_01122_b200.scenario import make_scene
+    sc = make_scene("cfg4_rank", cycles=2, humans=1)
+    cs, q, beliefs = _scene_beliefs(G, sc)
+    space, b, _, _ = beliefs[0]
+    spec = G.GridSpec(400, 400, 0.1)
+    dt, sigma, seed, pre = sc.dt, 0.1, 5, (2, 0)
+    z0 = G.HumanState(*sc.warmup_track[10][0])
+    hyp = sample_hypotheses(b, n, seed, prefix=pre)
+    batch = ParticleBatch.duplicated(z0, hyp)
+    counts = []
+    keep_steps = [0, 249, steps - 1]
+    layers = []
+    for t in range(1, steps + 1):
+        batch = propagate_step(batch, cs, q, space, dt, seed, step=t, workers=8, prefix=pre)
+        c = emplace_counts(batch.xy, spec)
+        counts.append(c.astype(np.int64))
+        if t - 1 in keep_steps:
+            layers.append(smooth_values(c / n, spec, sigma))
+    ci, cv = _sparse_counts(counts)
+    tb = model.make_tables(cs.v, cs.theta, dt, model.QSpec("goal_progress", 0.5))
+    meta = dict(n=n, steps=steps, dt=dt, sigma=sigma, seed=seed, prefix=list(pre), grid=[400, 400, 0.1, [0.0, 0.0]],
+                z0=[z0.x, z0.y], goals=np.asarray(space.goals.positions).tolist(),
+                betas=list(G.RationalitySet.log_spaced(5).betas))
+    li, lv = _sparse_layers(np.stack(layers))
+    np.savez_compressed(os.path.join(OUT, "long_cfg4.npz"), meta=json.dumps(meta), log_w=b.log_weights,
+                        hyp=hyp.astype(np.int32), xy_last=batch.xy.astype(np.float32), count_idx=ci, count_val=cv,
+                        layer_steps=np.array(keep_steps), layer_idx=li, layer_val=lv,
+                        sx=tb.sx, sy=tb.sy, at=tb.at, pen=tb.pen, dispx=tb.dispx, dispy=tb.dispy, keep=tb.keep,
+                        q_kind=np.int32(tb.q_kind))
+    print("long_cfg4 nnz", len(cv))
+
+
+def gen_uniforms(G):
+    """The reference's own random draws of the cfg1_s0 case, drawn by its rng module exactly
+    as sample_hypotheses (prediction.py:128-131) and propagate_step (prediction.py:186-192)
+    draw them: hypothesis u (n,) float64 and per-step chunk uniforms (T, n) float32."""
+    from gridcast import rng
+    case = predict_cases()["cfg1_s0"]
+    n, steps, seed, pre = case["n"], case["steps"], case["seed"], tuple(case["prefix"])
+    hyp_u = rng.stream(seed, *pre, rng.HYPOTHESIS_DRAWS).random(n)
+    u = np.empty((steps, n), dtype=np.float32)
+    for t in range(1, steps + 1):
+        for a, b, c in rng.chunk_ranges(n, 1024):
+            u[t - 1, a:b] = rng.stream(seed, *pre, rng.STEP_DRAWS, t, c).random(b - a, dtype=np.float32)
+    np.savez_compressed(os.path.join(OUT, "uniforms_cfg1.npz"), hyp_u=hyp_u, step_u=u)
+
+
+GENERATORS = dict(philox=lambda G: gen_philox(G), exp=lambda G: gen_exp(), predict=gen_predict, belief=gen_belief,
+                  smooth=gen_smooth, multi=gen_multi, exact=gen_exact, collision=gen_collision, gcst=gen_gcst,
+                  mppi=gen_mppi, naive=gen_naive, cfg3_cycle=gen_cfg3_cycle, long_cfg4=gen_long_cfg4,
+                  uniforms=gen_uniforms)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     G = _ref()
-    gen_philox(G)
-    gen_exp()
-    gen_predict(G)
-    gen_belief(G)
-    gen_smooth(G)
-    gen_multi(G)
-    gen_exact(G)
-    gen_collision(G)
-    gen_gcst(G)
-    gen_mppi(G)
-    gen_naive(G)
+    names = sys.argv[1:] or list(GENERATORS)
+    for name in names:
+        GENERATORS[name](G)
     import platform
     with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
         f.write(f"generated by oracle/gen_golden.py from {REF}\n")

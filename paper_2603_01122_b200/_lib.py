@@ -22,6 +22,11 @@ GC_SNAP_MISMATCH = 3
 GC_UNSUPPORTED_Q = 4
 GC_CUDA_ERROR = 5
 GC_WINDOW_OVERFLOW = 6
+# bits of gc_predict's d_error word (include/gridcast_b200.h)
+GC_ERRBIT_WINDOW_OVERFLOW = 1 << 6
+GC_ERRBIT_HYPOTHESES = 1 << 8
+GC_ERRBIT_WINDOW_CAPACITY = 1 << 9
+GC_MAX_HYPOTHESES = 128
 
 GC_Q_GOAL_PROGRESS = 0
 GC_Q_GOAL_PROGRESS_FULL = 1
@@ -197,6 +202,20 @@ def lib():
 
 def last_error() -> str:
     return lib().gc_last_error().decode(errors="replace")
+
+
+def check_error_word(word: int, what: str = "gc_predict"):
+    """Raise for the GC_ERRBIT_* bits of a gc_predict device status word."""
+    word = int(word) & 0xFFFFFFFF
+    if word == 0:
+        return
+    if word & GC_ERRBIT_HYPOTHESES:
+        raise ValueError(f"{what}: every human needs 1..{GC_MAX_HYPOTHESES} hypotheses")
+    if word & GC_ERRBIT_WINDOW_CAPACITY:
+        raise ValueError(f"{what}: max_win_cells is smaller than the launch's reachable-cell windows")
+    if word & GC_ERRBIT_WINDOW_OVERFLOW:
+        raise RuntimeError(f"{what}: a particle left its reachable-cell window (internal error)")
+    raise RuntimeError(f"{what}: device status word {word:#x}")
 
 
 def check(status: int, what: str = ""):

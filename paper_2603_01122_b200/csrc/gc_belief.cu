@@ -90,6 +90,10 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
     }
     const int idx = bidx;
     const int h0 = P.hyp_off[h], nh = P.hyp_off[h + 1] - h0;
+    if (nh < 1 || nh > BMAXH) {  // shared tables hold BMAXH hypotheses (uniform over the CTA)
+        if (threadIdx.x == 0) P.status[h] = GC_BAD_ARG;
+        return;
+    }
     // per-action tables of this lane's actions, loaded once (<= 8 per lane)
     double ax[8], ay[8], aat[8];
     bool amask[8];

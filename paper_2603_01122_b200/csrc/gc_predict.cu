@@ -18,6 +18,7 @@
 //   MODE_FACT : production, exact in distribution for grid control sets with
 //               goal-progress utility: weight(a,b) = H_b G_a e_b^a, one ex2 per heading.
 //   MODE_GEN  : production generic per-action softmax (fast ex2) for any control set.
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -34,6 +35,9 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 
 #ifndef GC_FFMA2
 #define GC_FFMA2 1  // packed FP32x2 heading loop (sm_100 FFMA2)
+#endif
+#ifndef GC_WORLD_CELLS
+#define GC_WORLD_CELLS 1  // production particles in float32 world coordinates, exact cells
 #endif
 
 constexpr unsigned PHK0 = 0xA4093822u, PHK1 = 0x299F31D0u;  // production Philox key
@@ -71,6 +75,7 @@ struct KParams {
     long long human_stride;
     unsigned *counts;
     int smem_window;
+    int win_cap_words;  // u32 words the host allocated for the window (incl. the sink word)
     int act_off;  // byte offset of SmemAct in dynamic shared memory (REF/GEN modes)
     int dyn_smem; // dynamic shared memory bytes of the launch (bounds checks)
     int t_begin, t_end;          // steps [t_begin, t_end) of this launch (1-based)
@@ -102,9 +107,26 @@ __device__ __forceinline__ int floor_clamp(float f, float nm1) {
     return __float_as_int(__fadd_rd(f, 8388608.f)) - 0x4B000000;
 }
 
+// the reference's cell of a float32 world position, floor(fl(fl(x - ox) / res)) clamped
+// (occupancy.py:43-51), without the IEEE division's slow path: q0 = fl(t * fl(1/res)) is
+// within an ulp of t / res, and one fma-exact residual correction, q = fl(q0 + fl(t - q0 res)
+// * fl(1/res)), is the correctly rounded quotient (Markstein; checked exhaustively against
+// __fdiv_rn for the grid resolutions in tests/test_gpu_cell_exact.py).  Production
+// particles keep the reference's float32 world coordinates (x += dispx[a]), so particles
+// that follow the same actions land in the same cells as the reference's -- clusters that
+// sit exactly on a cell edge included.
+__device__ __forceinline__ int cell_exact1(float x, float o, float res, float inv, float nm1) {
+    return floor_clamp(div_rn_recip(__fsub_rn(x, o), res, inv), nm1);
+}
+
 __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, int &ix, int &iy) {
+#if GC_WORLD_CELLS
+    ix = cell_exact1(x, P.ox, P.res, P.inv_res, P.wm1f);
+    iy = cell_exact1(y, P.oy, P.res, P.inv_res, P.hm1f);
+#else
     ix = floor_clamp((x - P.ox) * P.inv_res, P.wm1f);
     iy = floor_clamp((y - P.oy) * P.inv_res, P.hm1f);
+#endif
 }
 
 // MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
@@ -412,8 +434,8 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
     a = (rr < Z0) ? 0 : a;
     GC_DCHECK(a >= 0 && a < NAF && b >= 0 && b < NBF);
     const float2 d = S.fd[a * NBF + b];
-    x += d.x;
-    y += d.y;
+    x = __fadd_rn(x, d.x);  // the reference's float32 position update (prediction.py:161-162)
+    y = __fadd_rn(y, d.y);
 }
 
 // MODE_FACTS (standard heading set, n_speeds <= 4): the factorised sampler with
@@ -534,8 +556,8 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     a = (rr < Z0) ? 0 : a;  // stay: row 0 of fd is (0, 0)
     GC_DCHECK(a >= 0 && a < NAF && b >= 0 && b < NBF);
     const float2 d = S.fd[a * NBF + b];
-    x += d.x;
-    y += d.y;
+    x = __fadd_rn(x, d.x);  // the reference's float32 position update (prediction.py:161-162)
+    y = __fadd_rn(y, d.y);
 }
 
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
@@ -546,7 +568,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     __shared__ SmemTabs S;
     // the factorised sampler keeps particles in grid units u = (x - origin) / res: the
     // cell is floor(u), and the utility is rescaled (k -> k res) so the weights are unchanged
-    constexpr bool GRIDU = MODE == MODE_FACT || MODE == MODE_FACTS;
+    constexpr bool GRIDU = !GC_WORLD_CELLS && (MODE == MODE_FACT || MODE == MODE_FACTS);
     const int tid = threadIdx.x;
     const int h = blockIdx.x / P.ctas_per_human;
     const int blk = blockIdx.x - h * P.ctas_per_human;
@@ -554,6 +576,12 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
     const KTable &T = P.tab[tsel];
     const int h0 = __ldg(&P.hyp_off[h]);
     const int nh = __ldg(&P.hyp_off[h + 1]) - h0;
+    // 1..MAXH hypotheses per human (the shared tables' size): a human outside that range
+    // is not predicted and the launch reports it (uniform over the CTA, before any write)
+    if (nh < 1 || nh > MAXH) {
+        if (tid == 0 && P.error) atomicOr(P.error, GC_ERRBIT_HYPOTHESES);
+        return;
+    }
 
     // ---- stage tables in shared memory ----
     if (tid == 0) {
@@ -585,8 +613,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             const int a = i / NBF;
             const int ib = a * NBF + hslot(i - a * NBF);
             const int j = (a > 0 && a < T.n_speeds) ? __ldg(&T.a_index[ib]) : -1;  // a = 0: stay
-            S.fd[i] = j >= 0 ? make_float2(__fdiv_rn(__ldg(&T.dispx[j]), P.res), __fdiv_rn(__ldg(&T.dispy[j]), P.res))
-                             : make_float2(0.f, 0.f);
+            const float2 d = j >= 0 ? make_float2(__ldg(&T.dispx[j]), __ldg(&T.dispy[j])) : make_float2(0.f, 0.f);
+            S.fd[i] = GRIDU ? make_float2(__fdiv_rn(d.x, P.res), __fdiv_rn(d.y, P.res)) : d;
         }
         if (MODE == MODE_FACTS && WTH) {
             // same expression as the stay mass sum_b H_b below, so the CDF and Z0 agree
@@ -604,9 +632,12 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         S.hgy[i] = __ldg(&P.goal32[2 * (h0 + i) + 1]);
         if (MODE == MODE_FACT || MODE == MODE_FACTS) {
             const float L2E = 1.4426950408889634f;
-            S.hp[i] = make_float4(__fdiv_rn(S.hgx[i] - P.ox, P.res), __fdiv_rn(S.hgy[i] - P.oy, P.res),
-                                  2.f * b * T.tau * T.dv * L2E * P.res,
-                                  b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E);
+            // goal and utility slope in the particles' units (world, or grid units when GRIDU)
+            S.hp[i] = GRIDU ? make_float4(__fdiv_rn(S.hgx[i] - P.ox, P.res), __fdiv_rn(S.hgy[i] - P.oy, P.res),
+                                          2.f * b * T.tau * T.dv * L2E * P.res,
+                                          b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E)
+                            : make_float4(S.hgx[i], S.hgy[i], 2.f * b * T.tau * T.dv * L2E,
+                                          b * (T.tau * T.tau + T.w_v) * T.dv * T.dv * L2E);
             float sh = 0.f;
             for (int q = 0; q < T.n_headings; ++q)
                 sh += (T.w_th != 0.f) ? exp2f(-T.w_th * b * P.hth2[q] * 1.4426950408889634f) : 1.f;
@@ -641,6 +672,12 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
         // memory when the whole horizon does not): the host sized it from max_win_cells
         const int R = __ldg(&P.step_r[P.t_end - 2]);
         words = ((2 * R + 1) * (2 * R + 1) + 1) >> 1;
+        // the window is sized here from step_r and on the host from max_win_cells: a
+        // caller that under-reported max_win_cells gets an error bit, never an overrun
+        if (words + 1 > P.win_cap_words) {
+            if (tid == 0 && P.error) atomicOr(P.error, GC_ERRBIT_WINDOW_CAPACITY);
+            return;
+        }
         // + one sink word that lanes without a cell add to (branch-free add; never flushed)
         for (int i = tid; i <= words; i += NT) win[i] = 0u;
         GC_DCHECK(((words + 1 + 3) & ~3) * 4 <= P.dyn_smem);
@@ -774,8 +811,8 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                     fact_step<WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
                     const int a = gen_pick(S, A, x, y, S.phyp[k * NT + tid], u24(ua));
-                    x += A.adx[a];
-                    y += A.ady[a];
+                    x = __fadd_rn(x, A.adx[a]);
+                    y = __fadd_rn(y, A.ady[a]);
                 }
                 px[k] = x; py[k] = y;
                 int ix, iy;
@@ -851,7 +888,7 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
             __syncthreads();
         }
     }
-    if (overflow && P.error) atomicOr(P.error, 1u << GC_WINDOW_OVERFLOW);
+    if (overflow && P.error) atomicOr(P.error, GC_ERRBIT_WINDOW_OVERFLOW);
     if (P.t_end <= P.steps && P.state_xy) {  // hand the particles to the next chunk
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -945,11 +982,16 @@ static KTable to_ktable(const gc_action_table &a) {
 template <int MODE, int K, bool WTH>
 gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t st) {
     auto fn = k_predict<MODE, K, WTH>;
-    static bool configured = false;  // per instantiation: raise the dynamic limit once
-    if (!configured) {
+    // function attributes are per device context: raise the dynamic limit once per device
+    // (bit d of the mask; concurrent first calls may both set it, which is harmless)
+    static std::atomic<unsigned long long> configured{0ull};
+    int dev = 0;
+    GC_CUDA(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
         const int extra = (int)(sizeof(SmemAct) > (size_t)MAXH * NBF * 4 ? sizeof(SmemAct) : (size_t)MAXH * NBF * 4);
         GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 + extra));
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     fn<<<grid, NT, smem, st>>>(P);
     count_launch();
@@ -1071,6 +1113,7 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     // GC_PREDICT_GLOBAL_HIST=1 forces direct global reductions (tuning knob)
     static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();
     P.smem_window = (win_bytes <= 64 * 1024 && !force_global) ? 1 : 0;
+    P.win_cap_words = (int)(win_bytes / 4);
     P.act_off = P.smem_window ? (int)((win_bytes + 15) & ~(size_t)15) : 0;  // 16-byte aligned rows
     const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;
     bool wth = false;

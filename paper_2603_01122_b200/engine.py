@@ -181,6 +181,13 @@ class CycleEngine:
             self.blocked = [torch.zeros((T, Hh, W), dtype=torch.uint8, device=dev) for _ in range(2)]
         self._tarr = (_lib.ActionTable * 2)(*[t.struct for t in self.tables])
         self.last_xy = None
+        # stage() of an unprimed engine: that cycle has no previous observation, so (like
+        # sim.py:462-485, which updates only when last_xy is set) it predicts without an update
+        self._skip_update = [False, False]
+        self._stream = None  # the stream of the last cycle (belief reads/writes are ordered on it)
+        # per pinned input buffer: the event after run_cycle's H2D copy out of it; stage()
+        # waits for it before overwriting the buffer (cycles are issued asynchronously)
+        self._h2d_done = [None, None]
         self.heading = np.zeros(H)
         self.cycle = 0
         self.graphs = {}
@@ -205,16 +212,26 @@ class CycleEngine:
 
     # ---- host-side packing of one observation cycle ----------------------------------
     def stage(self, obs_xy: np.ndarray, buf: int = 0):
-        """Pack the cycle's observations (H, 2) float64 into the pinned input buffer."""
+        """Pack the cycle's observations (H, 2) float64 into the pinned input buffer.
+
+        Without a previous observation (no ``prime`` and no earlier cycle) the cycle only
+        predicts from ``obs_xy``: no belief update, unmasked Q (sim.py:462-485 updates and
+        sets ``stationary`` only once ``last_xy`` exists).  ``run_cycle`` honours this;
+        a captured graph always contains the update, so replay it only on primed cycles."""
         obs_xy = np.asarray(obs_xy, dtype=float)
+        if self._h2d_done[buf] is not None:
+            self._h2d_done[buf].synchronize()  # the previous cycle's copy out of this buffer is done
+            self._h2d_done[buf] = None
         self._select(buf)
-        prev = self.last_xy if self.last_xy is not None else obs_xy
+        primed = self.last_xy is not None
+        prev = self.last_xy if primed else obs_xy
+        self._skip_update[buf] = not primed
         self.h_obs[:, 0:2] = prev
         self.h_obs[:, 2:4] = obs_xy
         self.h_fallback[:] = self.heading
         d = obs_xy - prev
         moved = np.hypot(d[:, 0], d[:, 1])
-        stationary = moved / self.cfg.obs_dt < self.cfg.stationary_speed
+        stationary = (moved / self.cfg.obs_dt < self.cfg.stationary_speed) & primed
         self.h_tid[:] = stationary.astype(np.int32)
         mv = moved > 1e-9
         self.heading = np.where(mv, np.arctan2(d[:, 1], d[:, 0]), self.heading)
@@ -270,6 +287,7 @@ class CycleEngine:
         each chunk's layers are copied to it on ``copy_stream`` while later chunks compute."""
         cfg, geo, H = self.cfg, self.geo, self.n_humans
         sh = ctypes.c_void_p(stream.cuda_stream)
+        self._stream = stream
         # the output fills run on a side stream concurrently with K1 (K1 occupies one warp
         # per human; the fills are HBM-bound): fork from, and join back into, `stream`
         u = self.unions[buf]
@@ -393,18 +411,27 @@ class CycleEngine:
         """Eager (uncaptured) cycle on ``stream``; ``events`` = 3 CUDA events recorded
         before K2, after K2 and after K3 (kernel timing on the launching stream)."""
         s = stream or torch.cuda.current_stream()
+        with_update = with_update and not self._skip_update[buf]
         with torch.cuda.stream(s):
             if with_h2d:
                 self.d_in.copy_(self.h_ins[buf], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s)
+                self._h2d_done[buf] = ev
             self._launch(buf, with_update, s, events, chunks=chunks, d2h=d2h, copy_stream=copy_stream)
         return self.unions[buf]
 
     def capture(self, buf: int = 0, with_h2d: bool = True, with_update: bool = True, chunks: int = 1,
-                d2h=None):
+                d2h=None, events=None):
         """Capture one cycle into a CUDA graph (replay with ``replay``).  With ``d2h`` (a
         pinned host tensor shaped like the union) the chunked D2H copies are part of the
-        graph, on a forked copy stream."""
-        key = (buf, with_h2d, with_update, chunks, None if d2h is None else d2h.data_ptr())
+        graph, on a forked copy stream.  ``events``: 3 CUDA events created with
+        ``external=True`` (event-record nodes) recorded before K2, after K2 and after K3
+        inside the graph, so every replay times its kernels on the graph's own clock."""
+        if with_update and self._skip_update[buf]:
+            raise RuntimeError("capture(): prime() the engine first (a graph always runs the belief update)")
+        key = (buf, with_h2d, with_update, chunks, None if d2h is None else d2h.data_ptr(),
+               None if events is None else id(events))
         if key in self.graphs:
             return self.graphs[key][0]
         s = torch.cuda.Stream()
@@ -418,22 +445,38 @@ class CycleEngine:
         with torch.cuda.graph(g, stream=s):
             if with_h2d:
                 self.d_in.copy_(self.h_ins[buf], non_blocking=True)
-            self._launch(buf, with_update, s, chunks=chunks, d2h=d2h, copy_stream=cp)
-        self.graphs[key] = (g, cp)  # keep the copy stream alive with the graph
+            self._launch(buf, with_update, s, events=events, chunks=chunks, d2h=d2h, copy_stream=cp)
+        self.graphs[key] = (g, cp, events)  # keep the copy stream / events alive with the graph
         return g
 
+    def _belief_stream(self):
+        return self._stream if self._stream is not None else torch.cuda.current_stream(self.dev)
+
     def posterior(self, i: int) -> np.ndarray:
+        """Human i's device posterior, read after the cycles already issued on the engine's stream."""
         a, b = self.hyp_off[i], self.hyp_off[i + 1]
-        return self.d_logw[a:b].cpu().numpy()
+        s = self._belief_stream()
+        with torch.cuda.stream(s):
+            out = self.d_logw[a:b].to("cpu", non_blocking=True)
+        s.synchronize()
+        return out.numpy()
 
     def reset_belief(self, i: int):
-        """Uniform belief for human i (goal departure, sim.py:563-568; belief.py:120-123)."""
+        """Uniform belief for human i (goal departure, sim.py:563-568; belief.py:120-123),
+        ordered on the engine's launch stream after the cycles already issued there."""
         a, b = int(self.hyp_off[i]), int(self.hyp_off[i + 1])
-        self.d_logw[a:b] = -math.log(b - a)
+        with torch.cuda.stream(self._belief_stream()):
+            self.d_logw[a:b] = -math.log(b - a)
 
     def check_errors(self):
-        if int(self.d_err.item()) != 0:
-            raise RuntimeError("gc_predict: a particle left its reachable-cell window")
+        """Raise for K2's sticky device status bits (and clear them)."""
+        s = self._belief_stream()
+        s.synchronize()
+        word = int(self.d_err.item())
+        if word:
+            self.d_err.zero_()
+            torch.cuda.synchronize(self.dev)
+            _lib.check_error_word(word, "gc_predict")
 
 
 def fused_reduce(union: torch.Tensor, group=None, dst: Optional[int] = None, mode: str = "max",

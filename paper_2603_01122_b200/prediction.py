@@ -201,10 +201,21 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
                 sigma: float, spec: GridSpec, mode: str, per_human_layers: bool = True,
                 union64: bool = False, union32: bool = False, time_union: bool = False,
                 uniforms: Optional[torch.Tensor] = None, hyp_in: Optional[torch.Tensor] = None,
-                want_hyp: bool = False, want_xy: bool = False, stream=None, union_mode: str = "max"):
+                hyp_u: Optional[torch.Tensor] = None, want_hyp: bool = False, want_xy: bool = False, stream=None, union_mode: str = "max"):
     """Batched K2 + K3 launch; returns a dict of device tensors.  union_mode "max" merges
     the humans by atomicMax inside K3; "independent" (1 - prod(1 - p), occupancy.py:180-184)
-    merges the per-human float64 layers afterwards in human order (gc_union_layers)."""
+    merges the per-human float64 layers afterwards in human order (gc_union_layers).
+
+    ``uniforms`` (humans, steps, n) float32 and ``hyp_u`` (humans, n) float64 select
+    GC_RNG_UNIFORMS: the reference arithmetic driven by caller-supplied draws (e.g. the
+    reference's own rng.stream draws, prediction.py:128-131, :186-192)."""
+    if hyp_u is not None and uniforms is None:
+        raise ValueError("hyp_u needs uniforms (GC_RNG_UNIFORMS)")
+    if uniforms is not None:
+        if tuple(uniforms.shape) != (len(jobs), steps, n) or uniforms.dtype != torch.float32:
+            raise ValueError("uniforms must be a (humans, steps, n) float32 device tensor")
+        if hyp_u is not None and (tuple(hyp_u.shape) != (len(jobs), n) or hyp_u.dtype != torch.float64):
+            raise ValueError("hyp_u must be a (humans, n) float64 device tensor")
     if union_mode not in ("max", "independent"):
         raise ValueError(f"unknown union mode {union_mode!r}")
     dev = device()
@@ -250,7 +261,7 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     a.d_beta32, a.d_goal32, a.d_cdf, a.d_log_w = d_beta.data_ptr(), d_goal.data_ptr(), d_cdf.data_ptr(), None
     a.d_seed, a.d_prefix, a.d_prefix_len = d_seed.data_ptr(), d_pre.data_ptr(), d_plen.data_ptr()
     a.d_uniforms = uniforms.data_ptr() if uniforms is not None else None
-    a.d_hyp_u = None
+    a.d_hyp_u = hyp_u.data_ptr() if hyp_u is not None else None
     a.d_hyp_in = hyp_in.data_ptr() if hyp_in is not None else None
     tarr = (_lib.ActionTable * len(tables))(*[t.struct for t in tables])
     a.h_tables, a.n_tables, a.d_table_id = tarr, len(tables), d_tid.data_ptr()
@@ -296,8 +307,7 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
                                                         spec.height * spec.width, sh), "gc_time_union")
         if not per_human_layers:
             del out["layers"]
-    if int(err.item()) != 0:
-        raise RuntimeError("gc_predict: a particle left its reachable-cell window (internal error)")
+    _lib.check_error_word(err.item(), "gc_predict")
     out["counts"] = counts
     out["geometry"] = geo
     return out

@@ -1,8 +1,10 @@
 """Synthetic pedestrian scenes of the benchmark shapes (BASELINE.json configs).
 
 Common inputs: res 0.1 m, origin (0, 0); ControlSet.grid(4, 24, 1.4) (m = 96);
-q_goal_progress(0.5); RationalitySet.log_spaced(5); goals on a circle of radius 3.5 m
-around each human's start (the cli.py:176-179 bench pattern); belief = posterior after
+q_goal_progress(0.5); RationalitySet.log_spaced(5); goals on a circle of radius 0.35 x room
+around each human's start (the cli.py:176-179 bench puts them 3.5 m from the
+centre of its 10 m room) -- cfg1 3.5 m, cfg2 7 m, cfg3/cfg4 14 m; ``goal_radius`` overrides
+it (e.g. 3.5 m at every config, the round-1 scene); belief = posterior after
 10 observations (dt 0.1 s) of a Boltzmann walker with beta = 10 heading to goal 0.
 Tracks are generated on the host before any timing starts.
 """
@@ -56,11 +58,12 @@ def _starts(h: int, room: float) -> np.ndarray:
 
 
 def make_scene(name: str = "cfg3", cycles: int = 64, seed: int = 0, humans: int | None = None,
-               human_offset: int = 0) -> Scene:
+               human_offset: int = 0, goal_radius: float | None = None) -> Scene:
     """Build the scene; ``humans``/``human_offset`` select a shard (multi-GPU weak scaling)."""
     c = dict(CONFIGS[name])
     H = humans if humans is not None else c["humans"]
     room = c["cells"] * 0.1
+    gr = 0.35 * room if goal_radius is None else float(goal_radius)
     spec = GridSpec(c["cells"], c["cells"], 0.1)
     cs = ControlSet.grid(4, 24, 1.4)
     q = q_goal_progress(0.5)
@@ -71,7 +74,7 @@ def make_scene(name: str = "cfg3", cycles: int = 64, seed: int = 0, humans: int 
     for i in range(H):
         s = base[(i + human_offset) % len(base)] + rng.uniform(-0.5, 0.5, 2)
         ang = 2.0 * np.pi * np.arange(c["goals"]) / c["goals"] + rng.uniform(0, np.pi / 2)
-        goals = np.stack([s[0] + 3.5 * np.cos(ang), s[1] + 3.5 * np.sin(ang)], axis=1)
+        goals = np.stack([s[0] + gr * np.cos(ang), s[1] + gr * np.sin(ang)], axis=1)
         spaces.append(HypothesisSpace(rs, GoalSet(goals)))
         starts.append(s)
         goals0.append(goals[0])
@@ -88,6 +91,7 @@ def make_scene(name: str = "cfg3", cycles: int = 64, seed: int = 0, humans: int 
             z = human_step(z, cs[j], 0.1)
             track[k, i] = (z.x, z.y)
     sc = Scene(name, cs, q, spaces, spec, track[10], c["n"], c["steps"], c["dt"])
+    sc.goal_radius = gr
     sc.warmup_track = track[:11]
     sc.prev_xy = track[10]
     sc.track = track[11:]

@@ -43,25 +43,41 @@ def _check(d):
 
 def test_bench_single_gpu_contract():
     d = _line([sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--lat-cycles", "20", "--cpu-t", "1",
-               "--no-ref-mode"])
+               "--cpu-runs", "1", "--no-ref-mode"])
     _check(d)
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("port", "reference")
+    assert cb["host"]["nproc"] >= 1 and "numpy" in cb["host"] and cb["extrapolation"]["sampled_steps"] == 1
     assert d["p99_ms"] >= d["p50_ms"] > 0 and d["latency_cycles"] >= 20
+    # the headline e2e is the reference's float64 layout, the float32 one beside it
+    assert d["e2e"]["dtype"] == "f64" and d["e2e_f32"]["dtype"] == "f32"
+    assert d["e2e"]["d2h_bytes_per_step"] == 2 * d["e2e_f32"]["d2h_bytes_per_step"]
+    # K2 timed inside the replayed graph: a share of the cycle, never more than it
+    assert 0 < d["kernels_ms"]["k_predict"] < d["ms_per_step"]
+
+
+def test_bench_gpus_beyond_the_box_fails_loudly():
+    import torch
+    n = torch.cuda.device_count() + 1
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", str(n), "--steps", "3"], capture_output=True,
+                         text=True, timeout=300, cwd=ROOT)
+    assert out.returncode != 0 and "CUDA device" in out.stderr
+    assert not [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
 
 
 def test_bench_distributed_path_one_rank():
     d = _line([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
                "--master-addr", "127.0.0.1", "--master-port", "29541", "bench.py", "--gpus", "1", "--force-dist",
-               "--steps", "5", "--warmup", "3", "--lat-cycles", "10", "--no-cpu-baseline", "--no-ref-mode"])
+               "--steps", "5", "--warmup", "3", "--lat-cycles", "10", "--no-cpu-baseline", "--no-ref-mode",
+               "--no-e2e-alt"])
     _check(d)
-    assert d["config"]["fused_grid"] == "nccl"
+    assert d["fused_grid"] == "nccl" and d["n_gpus"] == 1
 
 
 def test_bench_distributed_path_one_rank_peer_union():
     d = _line([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
                "--master-addr", "127.0.0.1", "--master-port", "29543", "bench.py", "--gpus", "1", "--force-dist",
                "--fused-path", "peer", "--steps", "5", "--warmup", "3", "--lat-cycles", "10", "--no-cpu-baseline",
-               "--no-ref-mode"])
+               "--no-ref-mode", "--no-e2e-alt"])
     _check(d)
-    assert d["config"]["fused_grid"] == "peer"
+    assert d["fused_grid"] == "peer" and d["n_gpus"] == 1

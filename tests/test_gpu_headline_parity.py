@@ -1,0 +1,306 @@
+"""GPU parity at the headline launch shapes (VERDICT r01 "pin the headline shapes").
+
+Reference mode must be bit-exact against the LIVE reference's goldens not only for small
+single-human launches (K = 1 particle per thread, tests/test_gpu_parity.py) but for the
+launch shapes the benchmark runs:
+
+  * K = 2 and K = 4 particles per thread (gc_predict picks K from the launch size:
+    K = 2 from 303,104 particles, K = 4 from 606,208) -- golden humans replicated in one
+    launch, every copy bit-identical to the golden;
+  * the cfg3 scene itself (8 humans x 262,144 particles, 400 x 400, after 10 belief
+    updates, sim.py:455-505 seed / prefix / union) -- tests/golden/cfg3_cycle.npz, through
+    run_predict and through the CycleEngine (K1 + K2 + K3);
+  * the global-histogram path (a cfg4 human, T = 500: its windows exceed shared memory) --
+    tests/golden/long_cfg4.npz;
+  * GC_RNG_UNIFORMS fed the reference's own pre-drawn uniforms (tests/golden/uniforms_cfg1.npz,
+    drawn by gridcast.rng exactly as prediction.py:128-131 / :186-192 draw them).
+
+Production mode is then checked against the live reference's own cfg3 layers (TV within
+the reference's seed-to-seed spread, the spread measured on the now-pinned reference mode).
+"""
+
+import hashlib
+import json
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_01122_b200 as G  # noqa: E402
+from paper_2603_01122_b200 import prediction as PR  # noqa: E402
+
+NT = 256
+
+
+def launch_k(total):
+    """Particles per thread gc_predict picks for a launch of `total` particles (gc_predict.cu)."""
+    k = 1
+    while k < 4 and total // (NT * k * 2) >= 4 * 148:
+        k *= 2
+    return k
+
+
+def golden_objects(name):
+    c = golden_io.PredictCase(name)
+    m = c.meta
+    cs = G.ControlSet([G.ControlAction(float(v), float(t)) for v, t in zip(m["v"], m["theta"])])
+    space = G.HypothesisSpace(G.RationalitySet(tuple(m["betas"])), G.GoalSet(np.array(m["goals"])))
+    qd = m["q"]
+    q = (G.q_goal_progress(qd["tau"], (qd["w_v"], qd["w_th"])) if qd["family"] == "goal_progress"
+         else G.q_default((qd["w_v"], qd["w_th"])))
+    if qd["v_threshold"] is not None:
+        q = G.mask_stationary(q, cs, qd["v_threshold"])
+    W, H, res, org = c.grid
+    return c, cs, space, q, G.GridSpec(W, H, res, org)
+
+
+def windowed_from_sparse(geo, start32, idx, val):
+    """Golden sparse counts (t, iy, ix) -> one human's windowed u32 count row."""
+    row = np.zeros(geo.human_stride, dtype=np.int64)
+    for t in np.unique(idx[:, 0]):
+        sel = idx[:, 0] == t
+        x0, y0, w, _ = geo.window(start32, int(t))
+        pos = geo.step_off[t] + (idx[sel, 1] - y0) * w + (idx[sel, 2] - x0)
+        row[pos] = val[sel]
+    return row
+
+
+def sparse_from_windowed(geo, start32, row, steps):
+    idx, val = [], []
+    for t in range(steps):
+        x0, y0, w, hh = geo.window(start32, t)
+        blk = row[geo.step_off[t]:geo.step_off[t] + w * hh].reshape(hh, w)
+        iy, ix = np.nonzero(blk)
+        idx.append(np.stack([np.full(len(iy), t), iy + y0, ix + x0], 1))
+        val.append(blk[iy, ix])
+    return np.concatenate(idx), np.concatenate(val)
+
+
+def sparse_dense(idx, val, shape):
+    a = np.zeros(shape)
+    a[tuple(idx.T)] = val
+    return a
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ---- K = 2 / K = 4 launches of replicated golden humans --------------------------------
+
+REPLICATED = [(name, k) for name in ("cfg2_t30", "cfg1_s0", "ragged_w", "max_sizes") for k in (2, 4)]
+
+
+@pytest.mark.parametrize("name,k", REPLICATED)
+def test_replicated_golden_humans_bit_exact_at_k(name, k):
+    c, cs, space, q, spec = golden_objects(name)
+    thr = NT * (k // 2) * 2 * 4 * 148  # smallest launch gc_predict runs with k particles per thread
+    humans = -(-thr // c.n)
+    assert launch_k(humans * c.n) == k, (humans, c.n)
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, c.dt, dev)
+    job = PR.HumanJob(G.HumanState(*c.z0), c.log_w, space.beta_of, space.goal_xy_of, c.seed, c.prefix, 0)
+    out = PR.run_predict([job] * humans, [tab], c.n, c.steps, c.dt, 0.0, spec, "reference",
+                         per_human_layers=False, want_hyp=True, want_xy=True)
+    geo = out["geometry"]
+    hyp, xy = out["hyp"], out["xy"]
+    assert bool((hyp == hyp[0]).all()) and bool((xy == xy[0]).all())
+    np.testing.assert_array_equal(hyp[0].cpu().numpy(), c.hyp)
+    np.testing.assert_array_equal(xy[0].cpu().numpy(), c.xy_last)
+    rows = out["counts"].view(humans, geo.human_stride)
+    assert bool((rows == rows[0]).all())
+    start32 = (np.float32(c.z0[0]), np.float32(c.z0[1]))
+    want = windowed_from_sparse(geo, start32, c.count_idx, c.count_val)
+    np.testing.assert_array_equal(rows[0].cpu().numpy().view(np.uint32).astype(np.int64), want)
+
+
+# ---- the cfg3 scene (8 x 262,144, 400 x 400), live-reference golden -------------------
+
+def cfg3_golden():
+    z = golden_io.load("cfg3_cycle.npz")
+    meta = json.loads(str(z["meta"]))
+    return z, meta
+
+
+def cfg3_jobs(meta, tabs):
+    jobs = []
+    for i, hm in enumerate(meta["humans"]):
+        space = G.HypothesisSpace(G.RationalitySet(tuple(meta["betas"])), G.GoalSet(np.array(hm["goals"])))
+        jobs.append(PR.HumanJob(G.HumanState(*hm["start"]), np.array(hm["log_w"]), space.beta_of,
+                                space.goal_xy_of, int(meta["seed"]), (2, i), int(hm["stationary"])))
+    return jobs
+
+
+def test_cfg3_scene_reference_mode_bit_exact():
+    """run_predict of the 8 cfg3 humans in one K = 4 launch vs the live reference: per-human
+    counts, hypothesis draws and final positions bit for bit, smoothed layers, max union and
+    time union <= 1e-15."""
+    z, meta = cfg3_golden()
+    cs, q = G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5)
+    dev = torch.device("cuda")
+    tabs = [PR.action_tables(cs, q, meta["dt"], dev), PR.action_tables(cs, G.mask_stationary(q, cs, 0.5), meta["dt"], dev)]
+    jobs = cfg3_jobs(meta, tabs)
+    n, T = meta["n"], meta["steps"]
+    assert launch_k(len(jobs) * n) == 4
+    spec = G.GridSpec(400, 400, 0.1)
+    out = PR.run_predict(jobs, tabs, n, T, meta["dt"], meta["sigma"], spec, "reference", per_human_layers=True,
+                         union64=True, want_hyp=True, want_xy=True)
+    geo = out["geometry"]
+    rows = out["counts"].view(len(jobs), geo.human_stride).cpu().numpy().view(np.uint32).astype(np.int64)
+    for i, (j, hm) in enumerate(zip(jobs, meta["humans"])):
+        assert sha(out["hyp"][i].cpu().numpy().astype(np.int32)) == hm["hyp_sha256"], i
+        assert sha(out["xy"][i].cpu().numpy().astype(np.float32)) == hm["xy_sha256"], i
+        start32 = (np.float32(j.z0.x), np.float32(j.z0.y))
+        idx, val = sparse_from_windowed(geo, start32, rows[i], T)
+        np.testing.assert_array_equal(idx, z[f"count_idx_{i}"])
+        np.testing.assert_array_equal(val, z[f"count_val_{i}"])
+        got = out["layers"][i].cpu().numpy()
+        np.testing.assert_allclose(got, sparse_dense(z[f"layer_idx_{i}"], z[f"layer_val_{i}"], got.shape),
+                                   rtol=0, atol=1e-15)
+    u = out["union64"].cpu().numpy()
+    np.testing.assert_allclose(u, sparse_dense(z["union_idx"], z["union_val"], u.shape), rtol=0, atol=1e-15)
+    out = PR.run_predict(jobs, tabs, n, T, meta["dt"], meta["sigma"], spec, "reference", per_human_layers=False,
+                         union64=True, time_union=True)
+    u = out["union64"].cpu().numpy()
+    np.testing.assert_allclose(u, sparse_dense(z["tunion_idx"], z["tunion_val"], u.shape), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("time_union", [False, True])
+def test_cfg3_engine_cycle_matches_live_reference(time_union):
+    """The CycleEngine (K1 belief update -> K2 -> K3, one process-wide cycle as the bench
+    runs it) over the cfg3 scene's 10 warm-up observations: posteriors vs the reference's
+    update chain, and the 10th cycle's fused float64 union (+ time union) vs the reference."""
+    from paper_2603_01122_b200.engine import CycleEngine, EngineConfig
+    from paper_2603_01122_b200.scenario import make_scene
+    z, meta = cfg3_golden()
+    sc = make_scene("cfg3", cycles=2)
+    np.testing.assert_allclose(sc.warmup_track, np.array(meta["warmup_track"]), rtol=0, atol=0)
+    cfg = EngineConfig(n=meta["n"], steps=meta["steps"], dt=meta["dt"], smoothing_sigma=meta["sigma"], seed=0,
+                       mode="reference", union_dtype="float64", time_union=time_union)
+    eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
+    eng.prime(sc.warmup_track[0])
+    for k in range(1, 11):
+        eng.stage(sc.warmup_track[k], buf=k % 2)
+        u = eng.run_cycle(buf=k % 2)
+    torch.cuda.synchronize()
+    eng.check_errors()
+    assert eng.cycle == 10  # the 10th cycle used derive_seed(0, 7, 9)
+    for i, hm in enumerate(meta["humans"]):
+        np.testing.assert_allclose(np.exp(eng.posterior(i)), np.exp(hm["log_w"]), rtol=1e-9, atol=1e-300)
+        assert int(eng.h_tid[i]) == int(hm["stationary"])
+    key = "tunion" if time_union else "union"
+    got = u.cpu().numpy()
+    np.testing.assert_allclose(got, sparse_dense(z[f"{key}_idx"], z[f"{key}_val"], got.shape), rtol=0, atol=1e-15)
+
+
+# ---- the global-histogram path (T = 500) -------------------------------------------------
+
+def test_long_horizon_global_histogram_path_bit_exact():
+    z = golden_io.load("long_cfg4.npz")
+    m = json.loads(str(z["meta"]))
+    cs, q = G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5)
+    space = G.HypothesisSpace(G.RationalitySet(tuple(m["betas"])), G.GoalSet(np.array(m["goals"])))
+    spec = G.GridSpec(400, 400, 0.1)
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, m["dt"], dev)
+    geo = PR.geometry(spec, m["steps"], tab.max_step, m["sigma"], dev)
+    win_bytes = (((geo.max_win_cells + 1) // 2 + 1 + 3) // 4) * 16
+    assert win_bytes > 64 * 1024  # gc_predict adds straight to global memory
+    job = PR.HumanJob(G.HumanState(*m["z0"]), z["log_w"], space.beta_of, space.goal_xy_of, m["seed"],
+                      tuple(m["prefix"]), 0)
+    out = PR.run_predict([job], [tab], m["n"], m["steps"], m["dt"], m["sigma"], spec, "reference",
+                         want_hyp=True, want_xy=True)
+    np.testing.assert_array_equal(out["hyp"][0].cpu().numpy(), z["hyp"])
+    np.testing.assert_array_equal(out["xy"][0].cpu().numpy(), z["xy_last"])
+    row = out["counts"].cpu().numpy().view(np.uint32).astype(np.int64)
+    idx, val = sparse_from_windowed(out["geometry"], (np.float32(m["z0"][0]), np.float32(m["z0"][1])), row,
+                                    m["steps"])
+    np.testing.assert_array_equal(idx, z["count_idx"])
+    np.testing.assert_array_equal(val, z["count_val"])
+    got = out["layers"][0].cpu().numpy()[z["layer_steps"]]
+    np.testing.assert_allclose(got, sparse_dense(z["layer_idx"], z["layer_val"], got.shape), rtol=0, atol=1e-15)
+
+
+# ---- GC_RNG_UNIFORMS with the reference's own draws -------------------------------------
+
+def test_uniforms_mode_with_reference_drawn_uniforms():
+    """Deterministic mode fed the uniforms gridcast.rng itself drew (north star: "a
+    deterministic mode consumes the reference's own pre-drawn uniform samples"): hypothesis
+    draws and per-step counts bit-identical to the reference's predict."""
+    c, cs, space, q, spec = golden_objects("cfg1_s0")
+    zu = golden_io.load("uniforms_cfg1.npz")
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, c.dt, dev)
+    # a seed that would draw DIFFERENT numbers: everything must come from the buffers
+    job = PR.HumanJob(G.HumanState(*c.z0), c.log_w, space.beta_of, space.goal_xy_of, c.seed + 12345, (9, 9), 0)
+    u = torch.as_tensor(zu["step_u"][None], device=dev)
+    hu = torch.as_tensor(zu["hyp_u"][None], device=dev)
+    out = PR.run_predict([job], [tab], c.n, c.steps, c.dt, c.sigma, spec, "reference", uniforms=u, hyp_u=hu,
+                         want_hyp=True, want_xy=True)
+    np.testing.assert_array_equal(out["hyp"][0].cpu().numpy(), c.hyp)
+    np.testing.assert_array_equal(out["xy"][0].cpu().numpy(), c.xy_last)
+    row = out["counts"].cpu().numpy().view(np.uint32).astype(np.int64)
+    want = windowed_from_sparse(out["geometry"], (np.float32(c.z0[0]), np.float32(c.z0[1])), c.count_idx,
+                                c.count_val)
+    np.testing.assert_array_equal(row, want)
+
+
+def test_uniforms_mode_cfg2_with_oracle_streams_and_replicas():
+    """cfg2 shape (65,536 x 30) in GC_RNG_UNIFORMS mode, uniforms from the pinned oracle
+    streams (oracle.philox == gridcast.rng on philox.npz), 5 humans (K = 2) each with its
+    own slice of the uniform buffer."""
+    from oracle import philox
+    from oracle import predict as OP
+    c, cs, space, q, spec = golden_objects("cfg2_t30")
+    step_u = np.stack([OP.step_uniforms(c.seed, c.prefix, t, c.n) for t in range(1, c.steps + 1)])
+    hyp_u = philox.stream_random_f64(c.seed, tuple(c.prefix) + (0,), c.n)
+    humans = 5
+    assert launch_k(humans * c.n) == 2
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, c.dt, dev)
+    job = PR.HumanJob(G.HumanState(*c.z0), c.log_w, space.beta_of, space.goal_xy_of, 0, (), 0)
+    u = torch.as_tensor(np.repeat(step_u[None], humans, 0), device=dev)
+    hu = torch.as_tensor(np.repeat(hyp_u[None], humans, 0), device=dev)
+    out = PR.run_predict([job] * humans, [tab], c.n, c.steps, c.dt, 0.0, spec, "reference", uniforms=u,
+                         hyp_u=hu, per_human_layers=False, want_hyp=True, want_xy=True)
+    geo = out["geometry"]
+    want = windowed_from_sparse(geo, (np.float32(c.z0[0]), np.float32(c.z0[1])), c.count_idx, c.count_val)
+    rows = out["counts"].view(humans, geo.human_stride).cpu().numpy().view(np.uint32).astype(np.int64)
+    for h in range(humans):
+        np.testing.assert_array_equal(out["hyp"][h].cpu().numpy(), c.hyp)
+        np.testing.assert_array_equal(out["xy"][h].cpu().numpy(), c.xy_last)
+        np.testing.assert_array_equal(rows[h], want)
+
+
+# ---- production mode vs the live reference at the cfg3 shape ----------------------------
+
+def test_cfg3_production_tv_vs_live_reference_layers():
+    """Production sampler on the cfg3 golden's inputs vs the LIVE reference's layers: per
+    (human, step) TV <= 1.5 x the reference's seed-to-seed TV + 0.005, where the spread is
+    measured on the reference mode that test_cfg3_scene_reference_mode_bit_exact pins."""
+    z, meta = cfg3_golden()
+    cs, q = G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5)
+    dev = torch.device("cuda")
+    tabs = [PR.action_tables(cs, q, meta["dt"], dev), PR.action_tables(cs, G.mask_stationary(q, cs, 0.5), meta["dt"], dev)]
+    jobs = cfg3_jobs(meta, tabs)
+    n, T, spec = meta["n"], meta["steps"], G.GridSpec(400, 400, 0.1)
+    ref = np.stack([sparse_dense(z[f"layer_idx_{i}"], z[f"layer_val_{i}"], (T, 400, 400)) for i in range(len(jobs))])
+    ref = torch.as_tensor(ref, device=dev)
+
+    def layers(mode, seed):
+        js = [PR.HumanJob(j.z0, j.log_weights, j.beta_of, j.goal_xy_of, seed, j.prefix, j.table) for j in jobs]
+        return PR.run_predict(js, tabs, n, T, meta["dt"], meta["sigma"], spec, mode)["layers"]
+
+    def tv(u, v):
+        return 0.5 * (u - v).abs().sum(dim=(2, 3))
+
+    spread = torch.maximum(tv(layers("reference", 101), ref), tv(layers("reference", 202), ref))
+    got = tv(layers("production", 303), ref)
+    print(f"cfg3 golden: production vs live reference TV max {float(got.max()):.4f} mean {float(got.mean()):.4f}; "
+          f"reference seed spread max {float(spread.max()):.4f} mean {float(spread.mean()):.4f}")
+    assert bool((got <= 1.5 * spread + 0.005).all()), (float(got.max()), float(spread.max()))

@@ -151,3 +151,62 @@ def test_oracle_predict_naive_matches_reference(name):
         np.testing.assert_array_equal(out["layers"], c.layers)
     else:
         np.testing.assert_allclose(out["layers"], c.layers, rtol=0, atol=1e-15)
+
+
+def _oracle_sparse_counts(z0, log_w, n, steps, seed, prefix, tables, beta_of, goal_xy_of, grid):
+    """The oracle cycle (C step + pinned streams) with sparse per-step counts (t, iy, ix)."""
+    hyp = OP.sample_hypotheses(log_w, n, seed, prefix)
+    xy = np.tile(np.array(z0, dtype=np.float32), (n, 1))
+    b32, g32 = np.asarray(beta_of, np.float32), np.asarray(goal_xy_of, np.float32)
+    idx, val = [], []
+    for t in range(1, steps + 1):
+        xy = cstep.propagate(xy, hyp, b32, g32, tables, OP.step_uniforms(seed, prefix, t, n))
+        cells, cnt = np.unique(cstep.cells(xy, grid), return_counts=True)
+        idx.append(np.stack([np.full(len(cells), t - 1), cells // grid.width, cells % grid.width], 1))
+        val.append(cnt)
+    return hyp, xy, np.concatenate(idx), np.concatenate(val)
+
+
+def test_oracle_long_horizon_cfg4_case():
+    """long_cfg4.npz (T = 500, the GPU's global-histogram path) reproduced by the oracle."""
+    z = golden_io.load("long_cfg4.npz")
+    m = json.loads(str(z["meta"]))
+    tb = model.Tables(np.asarray(model.control_grid(4, 24, 1.4)[0]), np.asarray(model.control_grid(4, 24, 1.4)[1]),
+                      z["sx"], z["sy"], z["at"], z["pen"], z["dispx"], z["dispy"], z["keep"], int(z["q_kind"]))
+    beta_of, goal_xy_of = model.hypothesis_tables(m["betas"], m["goals"])
+    hyp, xy, idx, val = _oracle_sparse_counts(m["z0"], z["log_w"], m["n"], m["steps"], m["seed"], tuple(m["prefix"]),
+                                              tb, beta_of, goal_xy_of, OP.Grid(400, 400, 0.1))
+    np.testing.assert_array_equal(hyp, z["hyp"])
+    np.testing.assert_array_equal(xy, z["xy_last"])
+    np.testing.assert_array_equal(idx, z["count_idx"])
+    np.testing.assert_array_equal(val, z["count_val"])
+
+
+def test_oracle_cfg3_scene_human0():
+    """cfg3_cycle.npz human 0 (262,144 particles of the bench scene; the first 6 of its 25
+    steps, to keep the CPU suite short -- the GPU test checks all 25) by the oracle."""
+    import hashlib
+    z = golden_io.load("cfg3_cycle.npz")
+    m = json.loads(str(z["meta"]))
+    hm = m["humans"][0]
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, m["dt"], model.QSpec("goal_progress", 0.5, 0.0, 0.0,
+                                                       0.5 if hm["stationary"] else None))
+    beta_of, goal_xy_of = model.hypothesis_tables(m["betas"], hm["goals"])
+    T = 6
+    hyp, xy, idx, val = _oracle_sparse_counts(hm["start"], np.array(hm["log_w"]), m["n"], T, int(m["seed"]),
+                                              (2, 0), tb, beta_of, goal_xy_of, OP.Grid(400, 400, 0.1))
+    assert hashlib.sha256(hyp.astype(np.int32).tobytes()).hexdigest() == hm["hyp_sha256"]
+    sel = z["count_idx_0"][:, 0] < T
+    np.testing.assert_array_equal(idx, z["count_idx_0"][sel])
+    np.testing.assert_array_equal(val, z["count_val_0"][sel])
+
+
+def test_reference_drawn_uniforms_match_oracle_streams():
+    """uniforms_cfg1.npz (drawn by gridcast.rng) == the oracle's stream restatement."""
+    zu = golden_io.load("uniforms_cfg1.npz")
+    c = golden_io.PredictCase("cfg1_s0")
+    np.testing.assert_array_equal(philox.stream_random_f64(c.seed, tuple(c.prefix) + (0,), c.n), zu["hyp_u"])
+    for t in range(1, c.steps + 1):
+        np.testing.assert_array_equal(OP.step_uniforms(c.seed, c.prefix, t, c.n), zu["step_u"][t - 1])
+    np.testing.assert_array_equal(OP.sample_hypotheses(c.log_w, c.n, c.seed, c.prefix), c.hyp)
