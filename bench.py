@@ -348,7 +348,7 @@ def run_ours(args):
     if rank == 0 and distributed:
         print(f"bench.py: {world} rank(s), fused grid: "
               f"{'none' if not fused else ('NVLink peer-memory atomicMax (peer.PeerUnion)' if fused_path == 'peer' else 'NCCL max-reduce to rank 0')}",
-              flush=True)
+              file=sys.stderr, flush=True)
 
     def make_engine(union_dtype, peer=None):
         cfg = EngineConfig(n=scene.n, steps=scene.steps, dt=scene.dt, smoothing_sigma=0.1, seed=0,
@@ -524,12 +524,17 @@ def run_ours(args):
                             e.peer.barrier()      # every rank's K3 writes precede rank 0's read
                         else:
                             fused_reduce(e.unions[b], dst=0)
+                        if e.utile is not None:   # the fused grid's nonzero tiles: OR of the ranks'
+                            dist.reduce(e.utile[b], dst=0, op=dist.ReduceOp.MAX)
                         done[b].record(stream)
                     with torch.cuda.stream(copy):
                         copy.wait_event(done[b])
                         if rank == 0:
                             src = e.peer.tensor(b) if e.peer is not None else e.unions[b]
-                            h_out[b].copy_(src, non_blocking=True)
+                            if e.utile is not None:  # tile-sparse publication of the fused grid
+                                e.publish(b, h_out[b], union=src, stream=copy)
+                            else:
+                                h_out[b].copy_(src, non_blocking=True)
                             if e.peer is not None:
                                 src.zero_()
                         e_ev = torch.cuda.Event(enable_timing=True)
@@ -552,8 +557,9 @@ def run_ours(args):
             barrier()
             note = ("pinned obs H2D + " + ("peer-memory fused union (K3 atomicMax into rank 0's grid over "
                     "NVLink)" if e.peer is not None else "NCCL fused union") +
-                    f" + rank-0 {'f64' if dtype == torch.float64 else 'f32'} D2H each cycle, D2H overlapped "
-                    f"with the next cycle")
+                    f" + rank-0 {'f64' if dtype == torch.float64 else 'f32'} "
+                    f"{'tile-sparse publication (tile flags OR-reduced over ranks)' if e.utile is not None else 'D2H'}"
+                    f" each cycle, overlapped with the next cycle")
         e_ms = max_over_ranks(e_start.elapsed_time(e_end) / K)
         lat = [a_.elapsed_time(b_) for a_, b_ in evs]
         e.check_errors()
@@ -699,7 +705,7 @@ def main():
     ap.add_argument("--no-ref-mode", action="store_true")
     ap.add_argument("--lat-cycles", type=int, default=LAT_CYCLES,
                     help="cycles the p50/p99 latencies are taken over (at least --steps)")
-    ap.add_argument("--chunks", type=int, default=7, help="horizon chunks of the e2e cycle (D2H overlap)")
+    ap.add_argument("--chunks", type=int, default=4, help="horizon chunks of the e2e cycle (D2H overlap)")
     ap.add_argument("--chunk-taper", type=float, default=0.5, help="chunk size ratio (1.0 = uniform chunks)")
     ap.add_argument("--cpu-t", type=int, default=10, help="steps of the CPU baseline sample (<= 10, BASELINE.md 5)")
     ap.add_argument("--cpu-runs", type=int, default=5)

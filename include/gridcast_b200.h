@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GC_ABI_VERSION 1
+#define GC_ABI_VERSION 2
 
 typedef enum {
     GC_OK = 0,
@@ -152,6 +152,15 @@ typedef struct {
      * windows of all shards sum (ncclReduce/AllReduce sum) to the single-GPU counts and
      * the epilogue then divides by the total particle count. */
     int32_t p_offset;
+    /* optional count-tile flags for the epilogue (gc_epilogue_args.d_count_tile_flags):
+     * (n_humans, n_tiles) zero-filled bytes over the epilogue's tile list (d_tiles, step t
+     * owning tiles [d_tile_start[t], d_tile_start[t+1]), row-major ceil((2 r_t + 1 + 2
+     * radius) / 32) tiles per row); K2 sets the flag of every tile holding a nonzero count
+     * (shared-memory window path: at its flush; global path: all flags).  NULL = off. */
+    int32_t radius;            /* the epilogue's smoothing radius (tile grid anchor) */
+    const int32_t *d_tile_start;
+    uint8_t *d_count_tile_flags;
+    int32_t n_tiles;           /* tiles per human (the epilogue's n_tiles) */
     int32_t _pad3;
 } gc_predict_args;
 
@@ -180,7 +189,37 @@ typedef struct {
     int32_t time_union;        /* running max over t of the union (sim.py:503-504) */
     int32_t tile_begin, tile_end; /* sub-range of d_tiles (0, 0 = all; tiles are ordered by step) */
     int32_t t_begin, t_end;    /* steps the time union covers (0-based, [t_begin, t_end); 0, 0 = all) */
+    int32_t _pad_e;
+    /* K2's count-tile flags (gc_predict_args.d_count_tile_flags) and the tile list's step
+     * starts, or NULL: a tile whose own and 8 neighbouring flags are clear holds no counts
+     * within the smoothing halo and is skipped without reading the count windows */
+    const uint8_t *d_count_tile_flags;
+    const int32_t *d_tile_start;
+    /* (steps, ceil(H/32), ceil(W/32)) zero-filled byte flags, or NULL: set to 1 for every
+     * 32 x 32 union tile of a layer that receives a nonzero value (gc_publish_tiles ships
+     * only those tiles to the host) */
+    uint8_t *d_union_tile_flags;
 } gc_epilogue_args;
+
+/* Tile-sparse device -> host publication of a (steps, H, W) union into a pinned host stack
+ * (the reference's PredictionStack layout, prediction.py:98-106) that lives across cycles:
+ * for every 32 x 32 tile of layers [t_begin, t_end) the kernel writes the device tile into
+ * the host stack when K3 flagged it nonzero this cycle, writes zeros where the host stack
+ * still holds a tile of an earlier cycle that is zero now, and otherwise moves nothing, so
+ * after the call the host stack equals the device union bit for bit.  The host stack must
+ * be page-locked and mapped (any cudaHostAlloc / pinned allocation under unified
+ * addressing) and start zero-filled with zeroed d_host_flags. */
+typedef struct {
+    int32_t steps, grid_w, grid_h;
+    int32_t t_begin, t_end;            /* 0-based layer range [t_begin, t_end) */
+    int32_t dtype_bytes;               /* 4 (float32) or 8 (float64) */
+    int32_t time_or;                   /* 1: layer t's tile is live if any layer <= t flagged it (time union) */
+    int32_t _pad;
+    const void *d_union;               /* (steps, H, W) device union */
+    const uint8_t *d_tile_flags;       /* this cycle's K3 flags (gc_epilogue_args.d_union_tile_flags) */
+    uint8_t *d_host_flags;             /* (steps, ceil(H/32), ceil(W/32)) tiles of the host stack holding nonzeros */
+    void *h_dst;                       /* (steps, H, W) pinned, mapped host stack */
+} gc_publish_args;
 
 /* Observation update of every human's joint belief (belief.py:159-198), one warp per
  * human: recover_control (agents.py:355-371) -> snap (agents.py:114-120) -> log-policy
@@ -288,6 +327,7 @@ gc_status gc_union_layers(const void *d_in, int32_t in_bytes, int32_t k, int64_t
 gc_status gc_time_union(void *d_union, int32_t dtype_bytes, int32_t t_begin, int32_t t_end, int64_t cells,
                         void *stream);
 gc_status gc_grid_epilogue(const gc_epilogue_args *args, void *stream);
+gc_status gc_publish_tiles(const gc_publish_args *args, void *stream);
 gc_status gc_belief_update(const gc_belief_args *args, void *stream);
 
 /* One propagate_step (prediction.py:165-211) of an explicit particle batch in reference

@@ -72,7 +72,8 @@ class PredictArgs(ctypes.Structure):
         ("max_win_cells", I32), ("_pad2", I32), ("d_counts", P),
         ("d_hyp_out", P), ("d_xy_out", P), ("d_error", P),
         ("t_begin", I32), ("t_end", I32), ("d_state_xy", P), ("d_state_hyp", P),
-        ("p_offset", I32), ("_pad3", I32),
+        ("p_offset", I32), ("radius", I32), ("d_tile_start", P), ("d_count_tile_flags", P),
+        ("n_tiles", I32), ("_pad3", I32),
     ]
 
 
@@ -86,6 +87,15 @@ class EpilogueArgs(ctypes.Structure):
         ("d_tiles", P), ("d_counts", P),
         ("d_layers64", P), ("d_union32", P), ("d_union64", P), ("time_union", I32),
         ("tile_begin", I32), ("tile_end", I32), ("t_begin", I32), ("t_end", I32),
+        ("_pad_e", I32), ("d_count_tile_flags", P), ("d_tile_start", P), ("d_union_tile_flags", P),
+    ]
+
+
+class PublishArgs(ctypes.Structure):
+    _fields_ = [
+        ("steps", I32), ("grid_w", I32), ("grid_h", I32), ("t_begin", I32), ("t_end", I32),
+        ("dtype_bytes", I32), ("time_or", I32), ("_pad", I32),
+        ("d_union", P), ("d_tile_flags", P), ("d_host_flags", P), ("h_dst", P),
     ]
 
 
@@ -144,7 +154,7 @@ EXPORTS = (
     "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
     "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
     "gc_collision_field", "gc_exact_predict", "gc_mppi_step", "gc_predict_naive",
-    "gc_union_layers", "gc_time_union",
+    "gc_union_layers", "gc_time_union", "gc_publish_tiles",
     "gc_peer_alloc", "gc_peer_free", "gc_peer_export", "gc_peer_import", "gc_peer_close",
 )
 
@@ -178,6 +188,7 @@ def lib():
     L.gc_predict_naive.argtypes = [ctypes.POINTER(NaiveArgs), P]
     L.gc_union_layers.argtypes = [P, I32, I32, I64, I64, I32, P, I32, P]
     L.gc_time_union.argtypes = [P, I32, I32, I32, I64, P]
+    L.gc_publish_tiles.argtypes = [ctypes.POINTER(PublishArgs), P]
     L.gc_peer_alloc.argtypes = [I64, ctypes.POINTER(P)]
     L.gc_peer_free.argtypes = [P]
     L.gc_peer_export.argtypes = [P, P]
@@ -186,7 +197,7 @@ def lib():
     for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
                "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field",
                "gc_exact_predict", "gc_mppi_step", "gc_predict_naive", "gc_union_layers",
-               "gc_time_union", "gc_peer_alloc", "gc_peer_free", "gc_peer_export", "gc_peer_import",
+               "gc_time_union", "gc_publish_tiles", "gc_peer_alloc", "gc_peer_free", "gc_peer_export", "gc_peer_import",
                "gc_peer_close"):
         getattr(L, fn).restype = ctypes.c_int
     L.gc_derive_seed.argtypes = [U64, P, I32]

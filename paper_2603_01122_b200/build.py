@@ -57,6 +57,8 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     os.makedirs(objdir, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
     extra = ["-DGC_CHECKED"] if checked else []
+    # GC_EXTRA_NVCC_FLAGS: extra defines for A/B builds of kernel variants (tuning knob)
+    extra += os.environ.get("GC_EXTRA_NVCC_FLAGS", "").split()
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")

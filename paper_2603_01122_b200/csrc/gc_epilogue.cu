@@ -34,6 +34,10 @@ struct EParams {
     double *layers64;
     float *union32;
     double *union64;
+    unsigned char *utile;  // union tile flags (steps, nty, ntx) or NULL
+    int utx;               // union tiles per row
+    const unsigned char *cflags;  // K2's count-tile flags (n_humans, n_tiles) or NULL
+    const int *tile_start;
 };
 
 __device__ __forceinline__ void cell_of_start(float x, float y, const EParams &P, int &ix, int &iy) {
@@ -68,6 +72,18 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
     if (X0 > min(P.grid_w - 1, x1 + rad) || X0 + ET - 1 < max(0, x0 - rad) ||
         Y0 > min(P.grid_h - 1, y1 + rad) || Y0 + ET - 1 < max(0, y0 - rad))
         return;
+    if (P.cflags) {
+        // no counts in this tile or its 8 neighbours (the halo, rad <= 16 < 32): all zero
+        const int nt = (2 * R + 1 + 2 * rad + ET - 1) / ET;
+        int live = 0;
+        if (threadIdx.x < 9) {
+            const int dx = threadIdx.x % 3 - 1, dy = threadIdx.x / 3 - 1;
+            const int nx = tl.y + dx, ny = tl.z + dy;
+            if ((rad > 0 || (dx == 0 && dy == 0)) && nx >= 0 && nx < nt && ny >= 0 && ny < nt)
+                live = P.cflags[(long long)h * P.n_tiles + __ldg(&P.tile_start[t]) + ny * nt + nx];
+        }
+        if (!__syncthreads_or(live)) return;
+    }
     const unsigned *cnt = P.counts + (long long)h * P.human_stride + __ldg(&P.step_off[t]);
     const double inv_n = 1.0 / (double)P.n;  // only used for smoothing (see below)
     (void)inv_n;
@@ -124,6 +140,9 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
             if (P.union64)
                 atomicMax(reinterpret_cast<unsigned long long *>(P.union64) + o,
                           (unsigned long long)__double_as_longlong(v));
+            // this union tile is nonzero this cycle (idempotent byte store; a warp's lanes
+            // mostly hit the same byte and coalesce)
+            if (P.utile) P.utile[((long long)t * ((P.grid_h + ET - 1) / ET) + (Y >> 5)) * P.utx + (X >> 5)] = 1;
         }
     }
 }
@@ -236,6 +255,10 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
     P.start_xy = a->d_start_xy; P.step_r = a->d_step_r; P.step_off = (const long long *)a->d_step_off;
     P.human_stride = a->human_stride; P.tiles = (const int4 *)a->d_tiles; P.counts = a->d_counts;
     P.layers64 = a->d_layers64; P.union32 = a->d_union32; P.union64 = a->d_union64;
+    P.utile = (a->d_union32 || a->d_union64) ? a->d_union_tile_flags : nullptr;
+    P.cflags = a->d_count_tile_flags; P.tile_start = a->d_tile_start;
+    GC_CHECK_ARG(!P.cflags || P.tile_start, "gc_grid_epilogue: count-tile flags need d_tile_start");
+    P.utx = (a->grid_w + ET - 1) / ET;
     const int E = ET + 2 * a->radius;
     const size_t smem = (size_t)(E * E + (a->radius > 0 ? ET * E : 0)) * sizeof(double);
     if (smem > 48 * 1024)
@@ -264,6 +287,60 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
         GC_TRY(cuda_check(cudaGetLastError(), "k_time_union launch"));
     }
     return GC_OK;
+}
+
+// ---- tile-sparse publication of a union into a pinned host stack -----------------------
+// one warp per (layer, 32 x 32 tile); lane = column, rows looped: every row of a tile is one
+// coalesced 128 / 256-byte write over PCIe (or one read of the device union)
+namespace gc {
+template <typename Tv>
+__global__ void __launch_bounds__(256) k_publish(const Tv *un, Tv *dst, const unsigned char *flags,
+                                                 unsigned char *hflags, int W, int H, int t0, int t1, int time_or) {
+    const int ntx = (W + ET - 1) / ET, nty = (H + ET - 1) / ET, per = ntx * nty;
+    const long long total = (long long)(t1 - t0) * per;
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += warps) {
+        const int t = t0 + (int)(w / per), tile = (int)(w % per);
+        bool live = flags[(long long)t * per + tile] != 0;
+        if (time_or && !live) {  // the time union spreads a tile to every later layer
+            for (int s = lane; s < t; s += 32) live |= flags[(long long)s * per + tile] != 0;
+            live = __any_sync(0xffffffffu, live);
+        }
+        const long long hf = (long long)t * per + tile;
+        const bool held = hflags[hf] != 0;
+        if (!live && !held) continue;  // zero on the device, zero on the host
+        const int X = (tile % ntx) * ET + lane, Y0 = (tile / ntx) * ET;
+        if (X < W) {
+            const long long base = (long long)t * H * W + X;
+            for (int r = 0; r < ET && Y0 + r < H; ++r) {
+                const long long o = base + (long long)(Y0 + r) * W;
+                dst[o] = live ? un[o] : Tv(0);
+            }
+        }
+        if (lane == 0) hflags[hf] = live ? 1 : 0;
+    }
+}
+}  // namespace gc
+
+extern "C" gc_status gc_publish_tiles(const gc_publish_args *a, void *stream) {
+    GC_CHECK_ARG(a && a->d_union && a->d_tile_flags && a->d_host_flags && a->h_dst, "gc_publish_tiles: missing buffers");
+    GC_CHECK_ARG(a->dtype_bytes == 4 || a->dtype_bytes == 8, "gc_publish_tiles: float32 or float64 layers");
+    GC_CHECK_ARG(a->grid_w >= 1 && a->grid_h >= 1 && a->steps >= 1, "gc_publish_tiles: bad sizes");
+    const int t0 = a->t_end > 0 ? a->t_begin : 0, t1 = a->t_end > 0 ? a->t_end : a->steps;
+    GC_CHECK_ARG(t0 >= 0 && t0 < t1 && t1 <= a->steps, "gc_publish_tiles: bad layer range");
+    cudaStream_t st = (cudaStream_t)stream;
+    // PCIe-bound: a few CTAs reach the link's write bandwidth (zero-copy stores)
+    const long long work = (long long)(t1 - t0) * ((a->grid_w + ET - 1) / ET) * ((a->grid_h + ET - 1) / ET);
+    const int blocks = (int)(work < 148 * 8 ? (work + 7) / 8 : 148);
+    if (a->dtype_bytes == 8)
+        k_publish<double><<<blocks, 256, 0, st>>>((const double *)a->d_union, (double *)a->h_dst, a->d_tile_flags,
+                                                  a->d_host_flags, a->grid_w, a->grid_h, t0, t1, a->time_or);
+    else
+        k_publish<float><<<blocks, 256, 0, st>>>((const float *)a->d_union, (float *)a->h_dst, a->d_tile_flags,
+                                                 a->d_host_flags, a->grid_w, a->grid_h, t0, t1, a->time_or);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_publish launch");
 }
 
 // ---- ordered union of k stacked layer sets (occupancy.py:162-192) --------------------

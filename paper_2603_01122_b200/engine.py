@@ -74,6 +74,11 @@ class EngineConfig:
     # shared-memory windows.  Off by default: at the cfg4 shard (T = 500, 2^20 particles
     # per human) the split measured 42.8 ms per cycle against 40.4 ms on the global path
     window_budget_kb: float = 0.0
+    # host read-back of the union (run_cycle / capture with d2h=...): "tiles" publishes only
+    # the 32 x 32 tiles that are nonzero now or were nonzero in the host stack's previous
+    # cycle (gc_publish_tiles: kernel stores into the pinned, mapped host stack); "dense"
+    # copies every layer.  The host stack is bit-identical either way.
+    d2h_mode: str = "tiles"
 
 
 class CycleEngine:
@@ -161,6 +166,10 @@ class CycleEngine:
         self._views = [self._host_views(b.numpy(), H) for b in self.h_ins]
         self._select(0)
         self.counts = torch.zeros(H * self.geo.human_stride, dtype=torch.int32, device=dev)
+        # K2 -> K3 count-tile flags (K3 reads only tiles holding counts); off under particle
+        # sharding, where the counts -- but not the flags -- are summed over ranks
+        self.cflags = (torch.zeros(H * self.geo.n_tiles, dtype=torch.uint8, device=dev)
+                       if counts_reduce is None else None)
         udt = torch.float32 if cfg.union_dtype == "float32" else torch.float64
         T, Hh, W = cfg.steps, grid_spec.height, grid_spec.width
         if peer is None:
@@ -174,6 +183,13 @@ class CycleEngine:
         self.layers = (torch.zeros((H, T, Hh, W), dtype=torch.float64, device=dev)
                        if cfg.per_human_layers or cfg.union_mode == "independent" else None)
         self.d_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        if cfg.d2h_mode not in ("tiles", "dense"):
+            raise ValueError(f"unknown d2h_mode {cfg.d2h_mode!r}")
+        # 32 x 32 union tiles K3 made nonzero this cycle, per union buffer (tile-sparse D2H)
+        self.tile_grid = (T, -(-Hh // 32), -(-W // 32))
+        self.utile = (torch.zeros((2,) + self.tile_grid, dtype=torch.uint8, device=dev)
+                      if cfg.d2h_mode == "tiles" and cfg.union_mode == "max" else None)
+        self._hflags = {}  # pinned host stack (data_ptr) -> its device-side tile-state flags
         self.blocked = None
         if cfg.robot_radius is not None:
             from .occupancy import disc_offsets
@@ -301,12 +317,16 @@ class CycleEngine:
         # running under K2 and are joined before the first epilogue
         with torch.cuda.stream(fill):
             self.counts.zero_()
+            if self.cflags is not None:
+                self.cflags.zero_()
             join = torch.cuda.Event()
             join.record(fill)
             if self.peer is None:
                 u.zero_()
             if self.layers is not None:
                 self.layers.zero_()
+            if self.utile is not None:
+                self.utile[buf].zero_()
             join_out = torch.cuda.Event()
             join_out.record(fill)
         if with_update:
@@ -335,6 +355,9 @@ class CycleEngine:
         a.d_step_r, a.d_step_off = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr()
         a.human_stride, a.max_win_cells = geo.human_stride, geo.max_win_cells
         a.d_counts, a.d_error = self.counts.data_ptr(), self.d_err.data_ptr()
+        if self.cflags is not None:
+            a.radius, a.n_tiles, a.d_tile_start = geo.radius, geo.n_tiles, geo.d_tile_start.data_ptr()
+            a.d_count_tile_flags = self.cflags.data_ptr()
         if len(bounds) > 1:
             a.d_state_xy, a.d_state_hyp = self.state_xy.data_ptr(), self.state_hyp.data_ptr()
         e = _lib.EpilogueArgs()
@@ -345,6 +368,8 @@ class CycleEngine:
         e.n_tiles, e.d_start_xy = geo.n_tiles, self.d_start.data_ptr()
         e.d_step_r, e.d_step_off, e.human_stride = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr(), geo.human_stride
         e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), self.counts.data_ptr()
+        if self.cflags is not None:
+            e.d_count_tile_flags, e.d_tile_start = self.cflags.data_ptr(), geo.d_tile_start.data_ptr()
         if self.layers is not None:
             e.d_layers64 = self.layers.data_ptr()
         ordered = cfg.union_mode == "independent"
@@ -355,12 +380,19 @@ class CycleEngine:
                 e.d_union32 = self.peer.ptr(buf)
             else:
                 e.d_union64 = self.peer.ptr(buf)
+            if self.utile is not None:  # this rank's nonzero tiles (OR-reduced to the owner for publish)
+                e.d_union_tile_flags = self.utile[buf].data_ptr()
         elif not ordered:  # max union by atomicMax inside K3
             if u.dtype == torch.float32:
                 e.d_union32 = u.data_ptr()
             else:
                 e.d_union64 = u.data_ptr()
             e.time_union = int(cfg.time_union)
+            if self.utile is not None:
+                e.d_union_tile_flags = self.utile[buf].data_ptr()
+        tiles = d2h is not None and self.utile is not None
+        if tiles:
+            pa = self._publish_args(buf, u, d2h)
         for ci, (t0, t1) in enumerate(bounds):
             a.t_begin, a.t_end = (t0, t1) if len(bounds) > 1 else (0, 0)
             a.max_win_cells = int(geo.win_cells[t1 - 2])  # this launch's largest window
@@ -400,11 +432,43 @@ class CycleEngine:
                 ev.record(stream)
                 copy_stream.wait_event(ev)
                 with torch.cuda.stream(copy_stream):
-                    d2h[t0 - 1:t1 - 1].copy_(u[t0 - 1:t1 - 1], non_blocking=True)
+                    if tiles:  # tile-sparse: kernel stores of the changed tiles into the host stack
+                        pa.t_begin, pa.t_end = t0 - 1, t1 - 1
+                        _lib.check(_lib.lib().gc_publish_tiles(ctypes.byref(pa), ctypes.c_void_p(
+                            copy_stream.cuda_stream)), "gc_publish_tiles")
+                    else:
+                        d2h[t0 - 1:t1 - 1].copy_(u[t0 - 1:t1 - 1], non_blocking=True)
         if events is not None:
             events[2].record(stream)
         if d2h is not None:
             stream.wait_stream(copy_stream)  # the cycle ends when its layers are on the host
+
+    def _publish_args(self, buf, union, d2h, time_or=None):
+        if d2h.dtype != union.dtype or tuple(d2h.shape) != tuple(union.shape) or not d2h.is_pinned():
+            raise ValueError("d2h must be a pinned host tensor shaped and typed like the union")
+        hf = self._hflags.get(d2h.data_ptr())
+        if hf is None:  # a new host stack: zero it once, then only changed tiles move
+            d2h.zero_()
+            hf = torch.zeros(self.tile_grid, dtype=torch.uint8, device=self.dev)
+            self._hflags[d2h.data_ptr()] = hf
+        pa = _lib.PublishArgs()
+        pa.steps, pa.grid_w, pa.grid_h = self.cfg.steps, self.spec.width, self.spec.height
+        pa.dtype_bytes = union.element_size()
+        pa.time_or = int(self.cfg.time_union if time_or is None else time_or)
+        pa.d_union, pa.d_tile_flags = union.data_ptr(), self.utile[buf].data_ptr()
+        pa.d_host_flags, pa.h_dst = hf.data_ptr(), d2h.data_ptr()
+        return pa
+
+    def publish(self, buf: int, d2h, union=None, stream=None, time_or=None):
+        """Tile-sparse copy of a union (default: this engine's union ``buf``; e.g. the fused
+        grid after ``fused_reduce`` with the tile flags OR-reduced too) into the pinned host
+        stack ``d2h`` on ``stream`` (gc_publish_tiles): afterwards ``d2h`` equals the union."""
+        if self.utile is None:
+            raise RuntimeError("publish() needs EngineConfig(d2h_mode='tiles', union_mode='max')")
+        union = self.unions[buf] if union is None else union
+        s = stream or torch.cuda.current_stream(self.dev)
+        pa = self._publish_args(buf, union, d2h, time_or)
+        _lib.check(_lib.lib().gc_publish_tiles(ctypes.byref(pa), ctypes.c_void_p(s.cuda_stream)), "gc_publish_tiles")
 
     def run_cycle(self, buf: int = 0, with_h2d: bool = True, with_update: bool = True, stream=None,
                   events=None, chunks: int = 1, d2h=None, copy_stream=None):

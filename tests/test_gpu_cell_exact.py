@@ -25,4 +25,4 @@ def test_div_rn_recip_equals_ieee_division_exhaustively(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("mismatches: 0 of") >= 12
+    assert out.stdout.count("cell mismatches: 0 of") >= 12
