@@ -152,15 +152,6 @@ typedef struct {
      * windows of all shards sum (ncclReduce/AllReduce sum) to the single-GPU counts and
      * the epilogue then divides by the total particle count. */
     int32_t p_offset;
-    /* optional count-tile flags for the epilogue (gc_epilogue_args.d_count_tile_flags):
-     * (n_humans, n_tiles) zero-filled bytes over the epilogue's tile list (d_tiles, step t
-     * owning tiles [d_tile_start[t], d_tile_start[t+1]), row-major ceil((2 r_t + 1 + 2
-     * radius) / 32) tiles per row); K2 sets the flag of every tile holding a nonzero count
-     * (shared-memory window path: at its flush; global path: all flags).  NULL = off. */
-    int32_t radius;            /* the epilogue's smoothing radius (tile grid anchor) */
-    const int32_t *d_tile_start;
-    uint8_t *d_count_tile_flags;
-    int32_t n_tiles;           /* tiles per human (the epilogue's n_tiles) */
     int32_t _pad3;
 } gc_predict_args;
 
@@ -190,11 +181,6 @@ typedef struct {
     int32_t tile_begin, tile_end; /* sub-range of d_tiles (0, 0 = all; tiles are ordered by step) */
     int32_t t_begin, t_end;    /* steps the time union covers (0-based, [t_begin, t_end); 0, 0 = all) */
     int32_t _pad_e;
-    /* K2's count-tile flags (gc_predict_args.d_count_tile_flags) and the tile list's step
-     * starts, or NULL: a tile whose own and 8 neighbouring flags are clear holds no counts
-     * within the smoothing halo and is skipped without reading the count windows */
-    const uint8_t *d_count_tile_flags;
-    const int32_t *d_tile_start;
     /* (steps, ceil(H/32), ceil(W/32)) zero-filled byte flags, or NULL: set to 1 for every
      * 32 x 32 union tile of a layer that receives a nonzero value (gc_publish_tiles ships
      * only those tiles to the host) */

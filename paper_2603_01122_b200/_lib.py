@@ -72,8 +72,7 @@ class PredictArgs(ctypes.Structure):
         ("max_win_cells", I32), ("_pad2", I32), ("d_counts", P),
         ("d_hyp_out", P), ("d_xy_out", P), ("d_error", P),
         ("t_begin", I32), ("t_end", I32), ("d_state_xy", P), ("d_state_hyp", P),
-        ("p_offset", I32), ("radius", I32), ("d_tile_start", P), ("d_count_tile_flags", P),
-        ("n_tiles", I32), ("_pad3", I32),
+        ("p_offset", I32), ("_pad3", I32),
     ]
 
 
@@ -87,7 +86,7 @@ class EpilogueArgs(ctypes.Structure):
         ("d_tiles", P), ("d_counts", P),
         ("d_layers64", P), ("d_union32", P), ("d_union64", P), ("time_union", I32),
         ("tile_begin", I32), ("tile_end", I32), ("t_begin", I32), ("t_end", I32),
-        ("_pad_e", I32), ("d_count_tile_flags", P), ("d_tile_start", P), ("d_union_tile_flags", P),
+        ("_pad_e", I32), ("d_union_tile_flags", P),
     ]
 
 

@@ -36,8 +36,6 @@ struct EParams {
     double *union64;
     unsigned char *utile;  // union tile flags (steps, nty, ntx) or NULL
     int utx;               // union tiles per row
-    const unsigned char *cflags;  // K2's count-tile flags (n_humans, n_tiles) or NULL
-    const int *tile_start;
 };
 
 __device__ __forceinline__ void cell_of_start(float x, float y, const EParams &P, int &ix, int &iy) {
@@ -72,18 +70,6 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
     if (X0 > min(P.grid_w - 1, x1 + rad) || X0 + ET - 1 < max(0, x0 - rad) ||
         Y0 > min(P.grid_h - 1, y1 + rad) || Y0 + ET - 1 < max(0, y0 - rad))
         return;
-    if (P.cflags) {
-        // no counts in this tile or its 8 neighbours (the halo, rad <= 16 < 32): all zero
-        const int nt = (2 * R + 1 + 2 * rad + ET - 1) / ET;
-        int live = 0;
-        if (threadIdx.x < 9) {
-            const int dx = threadIdx.x % 3 - 1, dy = threadIdx.x / 3 - 1;
-            const int nx = tl.y + dx, ny = tl.z + dy;
-            if ((rad > 0 || (dx == 0 && dy == 0)) && nx >= 0 && nx < nt && ny >= 0 && ny < nt)
-                live = P.cflags[(long long)h * P.n_tiles + __ldg(&P.tile_start[t]) + ny * nt + nx];
-        }
-        if (!__syncthreads_or(live)) return;
-    }
     const unsigned *cnt = P.counts + (long long)h * P.human_stride + __ldg(&P.step_off[t]);
     const double inv_n = 1.0 / (double)P.n;  // only used for smoothing (see below)
     (void)inv_n;
@@ -256,8 +242,6 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
     P.human_stride = a->human_stride; P.tiles = (const int4 *)a->d_tiles; P.counts = a->d_counts;
     P.layers64 = a->d_layers64; P.union32 = a->d_union32; P.union64 = a->d_union64;
     P.utile = (a->d_union32 || a->d_union64) ? a->d_union_tile_flags : nullptr;
-    P.cflags = a->d_count_tile_flags; P.tile_start = a->d_tile_start;
-    GC_CHECK_ARG(!P.cflags || P.tile_start, "gc_grid_epilogue: count-tile flags need d_tile_start");
     P.utx = (a->grid_w + ET - 1) / ET;
     const int E = ET + 2 * a->radius;
     const size_t smem = (size_t)(E * E + (a->radius > 0 ? ET * E : 0)) * sizeof(double);

@@ -36,9 +36,6 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 #ifndef GC_FFMA2
 #define GC_FFMA2 1  // packed FP32x2 heading loop (sm_100 FFMA2)
 #endif
-#ifndef GC_MARK_TILES
-#define GC_MARK_TILES 1  // K2 marks the epilogue tiles holding counts at its flush
-#endif
 #ifndef GC_WORLD_CELLS
 #define GC_WORLD_CELLS 1  // production particles in float32 world coordinates, exact cells
 #endif
@@ -83,9 +80,6 @@ struct KParams {
     int dyn_smem; // dynamic shared memory bytes of the launch (bounds checks)
     int t_begin, t_end;          // steps [t_begin, t_end) of this launch (1-based)
     int p_offset;                // global index of this launch's first particle (particle sharding)
-    int radius, n_tiles;         // the epilogue's tile grid (count-tile flags)
-    const int *tile_start;
-    unsigned char *cflags;       // (n_humans, n_tiles) count-tile flags or NULL
     float2 *state_xy;            // particle state between horizon chunks
     unsigned char *state_hyp;
     int *hyp_out;
@@ -125,27 +119,6 @@ __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, fl
     ix = floor_clamp((x - P.ox) * P.inv_res, P.wm1f);
     iy = floor_clamp((y - P.oy) * P.inv_res, P.hm1f);
 #endif
-}
-
-// mark the epilogue tiles holding the nonzero cells of a flushed window word wi (cells 2 wi
-// and 2 wi + 1, row-major in the clamped window of width ww).  K3's tile grid for (human,
-// step) is anchored at the unclamped window grown by the smoothing radius (bx, by: the
-// clamped window's offset in it), ceil((2R + 1 + 2 radius) / 32) tiles per row.  Only the
-// flush runs this (a few words per CTA-step) and it is not inlined, so the hot loop keeps
-// its registers; the row division is a float one: c and ww are small integers and
-// (c + 0.5) / ww stays >= 1 / (2 ww) away from any integer.
-static __device__ __noinline__ void mark_word_tiles(unsigned char *cflags, const int *tile_start, int n_tiles,
-                                                    int radius, int h, int t, int R, int bx, int by, int ww, int wi,
-                                                    unsigned lo, unsigned hi) {
-    const int nt = (2 * R + 1 + 2 * radius + 31) >> 5;
-    const long long base = (long long)h * n_tiles + __ldg(&tile_start[t - 1]);
-    for (int j = 0; j < 2; ++j) {
-        if (!(j ? hi : lo)) continue;
-        const int c = 2 * wi + j;
-        const int row = (int)__fdividef((float)c + 0.5f, (float)ww), col = c - row * ww;
-        GC_DCHECK(((col + bx) >> 5) < nt && ((row + by) >> 5) < nt);
-        cflags[base + ((row + by) >> 5) * nt + ((col + bx) >> 5)] = 1;
-    }
 }
 
 // MODE_REF / MODE_GEN: per-action rows compacted over keep (dynamic shared memory,
@@ -904,9 +877,6 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 GC_DCHECK(2 * wi + (hi ? 1 : 0) < ww * wh);
                 if (lo) atomicAdd(&gcount[2 * wi], lo);
                 if (hi) atomicAdd(&gcount[2 * wi + 1], hi);
-                if (GC_MARK_TILES && P.cflags)  // the epilogue reads only tiles with counts (and their halos)
-                    mark_word_tiles(P.cflags, P.tile_start, P.n_tiles, P.radius, h, t, R, x0 - cx + R + P.radius,
-                                    y0 - cy + R + P.radius, ww, wi, lo, hi);
             }
             __syncthreads();
         }
@@ -1113,9 +1083,6 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     GC_CHECK_ARG(a->p_offset >= 0 && (long long)a->p_offset + a->n < (1ll << 31), "gc_predict: bad particle offset");
     GC_CHECK_ARG(a->p_offset % 4 == 0, "gc_predict: particle shards must start at a multiple of 4");
     P.p_offset = a->p_offset;
-    P.radius = a->radius; P.n_tiles = a->n_tiles; P.tile_start = a->d_tile_start; P.cflags = a->d_count_tile_flags;
-    GC_CHECK_ARG(!P.cflags || (P.tile_start && P.n_tiles >= 1 && P.radius >= 0),
-                 "gc_predict: count-tile flags need d_tile_start, n_tiles and radius");
 
     // particles per thread K and particles per CTA: enough CTAs to fill 148 SMs x 3
     // resident CTAs, then grow K to amortise the per-step window flush
@@ -1140,10 +1107,6 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();
     P.smem_window = (win_bytes <= 64 * 1024 && !force_global) ? 1 : 0;
     P.win_cap_words = (int)(win_bytes / 4);
-    if (P.cflags && !P.smem_window) {  // global-histogram path: no flush to mark from, so every tile is live
-        GC_CUDA(cudaMemsetAsync(P.cflags, 1, (size_t)a->n_humans * P.n_tiles, (cudaStream_t)stream));
-        P.cflags = nullptr;
-    }
     P.act_off = P.smem_window ? (int)((win_bytes + 15) & ~(size_t)15) : 0;  // 16-byte aligned rows
     const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;
     bool wth = false;

@@ -166,10 +166,6 @@ class CycleEngine:
         self._views = [self._host_views(b.numpy(), H) for b in self.h_ins]
         self._select(0)
         self.counts = torch.zeros(H * self.geo.human_stride, dtype=torch.int32, device=dev)
-        # K2 -> K3 count-tile flags (K3 reads only tiles holding counts); off under particle
-        # sharding, where the counts -- but not the flags -- are summed over ranks
-        self.cflags = (torch.zeros(H * self.geo.n_tiles, dtype=torch.uint8, device=dev)
-                       if counts_reduce is None else None)
         udt = torch.float32 if cfg.union_dtype == "float32" else torch.float64
         T, Hh, W = cfg.steps, grid_spec.height, grid_spec.width
         if peer is None:
@@ -317,8 +313,6 @@ class CycleEngine:
         # running under K2 and are joined before the first epilogue
         with torch.cuda.stream(fill):
             self.counts.zero_()
-            if self.cflags is not None:
-                self.cflags.zero_()
             join = torch.cuda.Event()
             join.record(fill)
             if self.peer is None:
@@ -355,9 +349,6 @@ class CycleEngine:
         a.d_step_r, a.d_step_off = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr()
         a.human_stride, a.max_win_cells = geo.human_stride, geo.max_win_cells
         a.d_counts, a.d_error = self.counts.data_ptr(), self.d_err.data_ptr()
-        if self.cflags is not None:
-            a.radius, a.n_tiles, a.d_tile_start = geo.radius, geo.n_tiles, geo.d_tile_start.data_ptr()
-            a.d_count_tile_flags = self.cflags.data_ptr()
         if len(bounds) > 1:
             a.d_state_xy, a.d_state_hyp = self.state_xy.data_ptr(), self.state_hyp.data_ptr()
         e = _lib.EpilogueArgs()
@@ -368,8 +359,6 @@ class CycleEngine:
         e.n_tiles, e.d_start_xy = geo.n_tiles, self.d_start.data_ptr()
         e.d_step_r, e.d_step_off, e.human_stride = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr(), geo.human_stride
         e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), self.counts.data_ptr()
-        if self.cflags is not None:
-            e.d_count_tile_flags, e.d_tile_start = self.cflags.data_ptr(), geo.d_tile_start.data_ptr()
         if self.layers is not None:
             e.d_layers64 = self.layers.data_ptr()
         ordered = cfg.union_mode == "independent"

@@ -243,7 +243,6 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     d_pre, d_plen = up(pre, np.uint32), up(plen, np.int32)
     d_tid = up([j.table for j in jobs], np.int32)
     counts = torch.zeros(H * geo.human_stride, dtype=torch.int32, device=dev)
-    cflags = torch.zeros(H * geo.n_tiles, dtype=torch.uint8, device=dev)  # K2 -> K3 count-tile flags
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     out = {}
     if want_hyp:
@@ -269,8 +268,6 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     a.d_step_r, a.d_step_off = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr()
     a.human_stride, a.max_win_cells = geo.human_stride, geo.max_win_cells
     a.d_counts = counts.data_ptr()
-    a.radius, a.n_tiles, a.d_tile_start, a.d_count_tile_flags = (geo.radius, geo.n_tiles, geo.d_tile_start.data_ptr(),
-                                                                  cflags.data_ptr())
     a.d_hyp_out = out["hyp"].data_ptr() if want_hyp else None
     a.d_xy_out = out["xy"].data_ptr() if want_xy else None
     a.d_error = err.data_ptr()
@@ -285,7 +282,6 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     e.n_tiles, e.d_start_xy = geo.n_tiles, d_start.data_ptr()
     e.d_step_r, e.d_step_off, e.human_stride = geo.d_step_r.data_ptr(), geo.d_step_off.data_ptr(), geo.human_stride
     e.d_tiles, e.d_counts = geo.d_tiles.data_ptr(), counts.data_ptr()
-    e.d_count_tile_flags, e.d_tile_start = cflags.data_ptr(), geo.d_tile_start.data_ptr()
     ordered = union_mode == "independent" and (union64 or union32)
     if per_human_layers or ordered:
         out["layers"] = torch.zeros((H, steps, spec.height, spec.width), dtype=torch.float64, device=dev)

@@ -255,7 +255,6 @@ class Geometry:
         self.d_step_r = dev(self.step_r)
         self.d_step_off = dev(self.step_off)
         self.d_tiles = dev(np.asarray(tiles, dtype=np.int32))
-        self.d_tile_start = dev(self.tile_start.astype(np.int32))
         self.d_kernel = dev(k.astype(np.float64))
         self.d_zx = dev(1.0 / zmass(self.W))  # reciprocal column masses (kernels multiply)
         self.d_zy = dev(1.0 / zmass(self.H))
