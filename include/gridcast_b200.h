@@ -376,6 +376,8 @@ const char *gc_last_error(void);
 int32_t gc_abi_version(void);
 /* Number of kernel launches issued through this library since load (for bench claims). */
 uint64_t gc_launch_count(void);
+/* cudaMemsetAsync(d_ptr, 0, bytes, stream): the engine's per-cycle output / count fills. */
+gc_status gc_fill_zero(void *d_ptr, int64_t bytes, void *stream);
 
 #ifdef __cplusplus
 }

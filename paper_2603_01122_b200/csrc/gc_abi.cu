@@ -25,6 +25,13 @@ const char *gc_last_error(void) { return gc::g_err.c_str(); }
 int32_t gc_abi_version(void) { return GC_ABI_VERSION; }
 uint64_t gc_launch_count(void) { return gc::g_launches.load(); }
 
+// stream-ordered zero fill of a device buffer (graph-capturable memset node)
+gc_status gc_fill_zero(void *d_ptr, int64_t bytes, void *stream) {
+    GC_CHECK_ARG(d_ptr != nullptr && bytes >= 0, "gc_fill_zero: bad buffer");
+    if (bytes == 0) return GC_OK;
+    return gc::cuda_check(cudaMemsetAsync(d_ptr, 0, (size_t)bytes, (cudaStream_t)stream), "gc_fill_zero");
+}
+
 // rng.derive_seed (rng.py:34-39)
 uint64_t gc_derive_seed(uint64_t seed, const uint32_t *h_path, int32_t path_len) {
     gc::SSPool s = gc::ss_pool_init(seed);

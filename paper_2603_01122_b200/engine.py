@@ -312,15 +312,18 @@ class CycleEngine:
         # K2 waits only for the counts; the union / layer fills (160 MB at cfg3) keep
         # running under K2 and are joined before the first epilogue
         with torch.cuda.stream(fill):
-            self.counts.zero_()
+            zero = lambda t: _lib.check(_lib.lib().gc_fill_zero(  # noqa: E731  (memset nodes)
+                ctypes.c_void_p(t.data_ptr()), t.numel() * t.element_size(), ctypes.c_void_p(fill.cuda_stream)),
+                "gc_fill_zero")
+            zero(self.counts)
             join = torch.cuda.Event()
             join.record(fill)
             if self.peer is None:
-                u.zero_()
+                zero(u)
             if self.layers is not None:
-                self.layers.zero_()
+                zero(self.layers)
             if self.utile is not None:
-                self.utile[buf].zero_()
+                zero(self.utile[buf])
             join_out = torch.cuda.Event()
             join_out.record(fill)
         if with_update:

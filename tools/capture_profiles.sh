@@ -25,4 +25,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_c
 python tools/sanitize_run.py > gpurun_out/plain_aux.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none -k regex:"k_(union|time_union|naive|emplace|smooth|sample_hyp|propagate_step)" -c 12 \
     -o gpurun_out/aux python tools/sanitize_run.py > gpurun_out/ncu_aux.log 2>&1
-tail -n 2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_k2.log gpurun_out/ncu_ref.log gpurun_out/ncu_extras.log
+# the tile-sparse D2H publication of the e2e cycle (f64 union)
+timeout 900 ncu --set full --clock-control none -k regex:k_publish -s 8 -c 4 -o gpurun_out/publish \
+    $B --no-e2e-alt > gpurun_out/ncu_publish.log 2>&1
+tail -n 2 gpurun_out/ncu_launch.log gpurun_out/ncu_publish.log gpurun_out/ncu_full.log gpurun_out/ncu_k2.log gpurun_out/ncu_ref.log gpurun_out/ncu_extras.log

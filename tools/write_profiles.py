@@ -56,8 +56,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--out", default="gpurun_out")
+    ap.add_argument("--prof-dir", default=None, help="write here instead of profiles/ (e.g. on the GPU box)")
     a = ap.parse_args()
-    prof = os.path.join(ROOT, "profiles")
+    prof = a.prof_dir or os.path.join(ROOT, "profiles")
+    os.makedirs(prof, exist_ok=True)
     src = os.path.join(ROOT, a.out)
 
     shares = launch_shares(os.path.join(src, "launches.csv"))
@@ -138,6 +140,12 @@ def main():
             "smooth,\n# sample_hypotheses, propagate_step) at tools/sanitize_run.py's small sizes: latency-bound "
             "utility launches,\n# listed for completeness (tools/capture_profiles.sh; per-launch values)\n"
             + capture(ncu_summary.main, aux))
+    pub = os.path.join(src, "publish.ncu-rep")
+    if os.path.exists(pub):
+        open(os.path.join(prof, f"{a.tag}_ncu_publish.txt"), "w").write(
+            "# ncu --set full of k_publish (tile-sparse D2H of the f64 fused union into the pinned host stack, "
+            "one launch per horizon chunk of the e2e cycle; kernel stores over PCIe)\n"
+            "# (tools/capture_profiles.sh; per-launch values)\n" + capture(ncu_summary.main, pub))
     # SASS of the cycle kernels and the static summary of every kernel in the library
     import sass_extract
     import sass_summary
