@@ -34,6 +34,8 @@ GC_Q_DEFAULT = 2
 GC_Q_TABLE = 3
 GC_UNION_MAX, GC_UNION_INDEPENDENT, GC_UNION_MISS, GC_UNION_COMPLEMENT = 0, 1, 2, 3
 
+GC_HIST_GLOBAL, GC_HIST_SMEM = 0, 1
+
 GC_RNG_REFERENCE = 0
 GC_RNG_UNIFORMS = 1
 GC_RNG_PRODUCTION = 2
@@ -72,7 +74,7 @@ class PredictArgs(ctypes.Structure):
         ("max_win_cells", I32), ("_pad2", I32), ("d_counts", P),
         ("d_hyp_out", P), ("d_xy_out", P), ("d_error", P),
         ("t_begin", I32), ("t_end", I32), ("d_state_xy", P), ("d_state_hyp", P),
-        ("p_offset", I32), ("_pad3", I32),
+        ("p_offset", I32), ("hist_path", I32),
     ]
 
 

@@ -36,6 +36,9 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 #ifndef GC_FFMA2
 #define GC_FFMA2 1  // packed FP32x2 heading loop (sm_100 FFMA2)
 #endif
+#ifndef GC_REF_MIN_CTAS
+#define GC_REF_MIN_CTAS 2  // resident CTAs per SM of the reference-arithmetic K2 (119 regs, no spills: 6 % faster than 4)
+#endif
 #ifndef GC_WORLD_CELLS
 #define GC_WORLD_CELLS 1  // production particles in float32 world coordinates, exact cells
 #endif
@@ -555,7 +558,7 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
 // particles, so a per-CTA cell count cannot overflow its half-word)
 template <int MODE, int K, bool WTH>
-__global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
+__global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : 4) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ SmemTabs S;
     // the factorised sampler keeps particles in grid units u = (x - origin) / res: the
@@ -857,9 +860,15 @@ __global__ void __launch_bounds__(NT, 4) k_predict(const KParams P) {
                 const unsigned old = atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
                                                (off & 2u) ? 0x10000u : 1u);
                 fwr[k] = (has && old == 0u) ? (local >> 1) : -1;
-            } else if (local >= 0) {
-                GC_DCHECK(local < ww * wh);
-                atomicAdd(&gcount[local], 1u);
+            } else {
+                // global-histogram path (GC_HIST_GLOBAL): the lanes of a warp adding to the
+                // same cell this step combine into one reduction (coherent particle clouds
+                // would otherwise serialise on the same L2 addresses)
+                const unsigned same = __match_any_sync(0xffffffffu, local);
+                if (local >= 0 && (int)(tid & 31) == __ffs(same) - 1) {
+                    GC_DCHECK(local < ww * wh);
+                    atomicAdd(&gcount[local], (unsigned)__popc(same));
+                }
             }
         }
         if (P.smem_window) {
@@ -1102,10 +1111,12 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     const long long grid = (long long)P.ctas_per_human * a->n_humans;
     GC_CHECK_ARG(grid < (1ll << 31), "gc_predict: too many particles");
     const size_t win_bytes = (size_t)(((a->max_win_cells + 1) / 2 + 1 + 3) & ~3) * 4;  // + sink word
-    // shared-memory windows whenever they fit (robust to coherent particle clouds);
-    // GC_PREDICT_GLOBAL_HIST=1 forces direct global reductions (tuning knob)
+    // GC_HIST_SMEM: shared-memory windows when they fit; GC_HIST_GLOBAL (default): warp-
+    // aggregated reductions straight into the count windows.  GC_PREDICT_GLOBAL_HIST=1
+    // forces the global form for any launch (tuning knob).
     static const int force_global = [] { const char *e = getenv("GC_PREDICT_GLOBAL_HIST"); return e ? atoi(e) : 0; }();
-    P.smem_window = (win_bytes <= 64 * 1024 && !force_global) ? 1 : 0;
+    GC_CHECK_ARG(a->hist_path == GC_HIST_GLOBAL || a->hist_path == GC_HIST_SMEM, "gc_predict: unknown hist_path");
+    P.smem_window = (a->hist_path == GC_HIST_SMEM && win_bytes <= 64 * 1024 && !force_global) ? 1 : 0;
     P.win_cap_words = (int)(win_bytes / 4);
     P.act_off = P.smem_window ? (int)((win_bytes + 15) & ~(size_t)15) : 0;  // 16-byte aligned rows
     const bool needs_act = a->rng_mode != GC_RNG_PRODUCTION || !fact;

@@ -201,7 +201,8 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
                 sigma: float, spec: GridSpec, mode: str, per_human_layers: bool = True,
                 union64: bool = False, union32: bool = False, time_union: bool = False,
                 uniforms: Optional[torch.Tensor] = None, hyp_in: Optional[torch.Tensor] = None,
-                hyp_u: Optional[torch.Tensor] = None, want_hyp: bool = False, want_xy: bool = False, stream=None, union_mode: str = "max"):
+                hyp_u: Optional[torch.Tensor] = None, want_hyp: bool = False, want_xy: bool = False,
+                stream=None, union_mode: str = "max", hist_path: str = "global"):
     """Batched K2 + K3 launch; returns a dict of device tensors.  union_mode "max" merges
     the humans by atomicMax inside K3; "independent" (1 - prod(1 - p), occupancy.py:180-184)
     merges the per-human float64 layers afterwards in human order (gc_union_layers).
@@ -271,6 +272,9 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     a.d_hyp_out = out["hyp"].data_ptr() if want_hyp else None
     a.d_xy_out = out["xy"].data_ptr() if want_xy else None
     a.d_error = err.data_ptr()
+    if hist_path not in ("global", "smem"):
+        raise ValueError(f"unknown hist_path {hist_path!r}")
+    a.hist_path = _lib.GC_HIST_SMEM if hist_path == "smem" else _lib.GC_HIST_GLOBAL
     sh = stream_handle(stream)
     _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")
 

@@ -28,7 +28,7 @@ class _Geo:
     def __init__(self, steps, budget_kb, cells=400, res=0.1, dt=0.02, reduce=None):
         from paper_2603_01122_b200.occupancy import GridSpec
         from paper_2603_01122_b200.tables import Geometry
-        self.cfg = EngineConfig(steps=steps, window_budget_kb=budget_kb)
+        self.cfg = EngineConfig(steps=steps, window_budget_kb=budget_kb, hist_path="smem")
         self.geo = Geometry(GridSpec(cells, cells, res), steps, 1.4 * dt, 0.1, "cpu")
         self.counts_reduce = reduce
 

@@ -68,6 +68,7 @@ def test_predict_rejects_hypothesis_counts_outside_1_to_128():
 
 def test_predict_rejects_underreported_window_capacity():
     a, keep = _args([4], max_win_cells=0)
+    a.hist_path = _lib.GC_HIST_SMEM  # the shared-memory window is sized from max_win_cells
     word, total = _run(a, keep)
     assert word & _lib.GC_ERRBIT_WINDOW_CAPACITY and total == 0
     with pytest.raises(ValueError):

@@ -32,11 +32,11 @@ def window_sums(eng):
     return out
 
 
-def run(name, mode="production", chunks=0, humans=8, n=None, stationary=(), budget_kb=0.0):
+def run(name, mode="production", chunks=0, humans=8, n=None, stationary=(), budget_kb=0.0, hist_path="global"):
     sc = make_scene(name, cycles=2, humans=humans)
     n = n or sc.n
     cfg = EngineConfig(n=n, steps=sc.steps, dt=sc.dt, smoothing_sigma=0.1, seed=3, mode=mode,
-                       window_budget_kb=budget_kb)
+                       window_budget_kb=budget_kb, hist_path=hist_path)
     eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, cfg)
     eng.prime(sc.prev_xy)
     obs = sc.track[0].copy()
@@ -55,9 +55,10 @@ def run(name, mode="production", chunks=0, humans=8, n=None, stationary=(), budg
     return eng
 
 
-def test_cfg3_production_cycle_conserves_particles_and_bounds():
-    """cfg3: 8 humans x 262,144 particles x 250 steps (shared-memory window path)."""
-    eng = run("cfg3")
+@pytest.mark.parametrize("hist_path", ["global", "smem"])
+def test_cfg3_production_cycle_conserves_particles_and_bounds(hist_path):
+    """cfg3: 8 humans x 262,144 particles x 250 steps (both histogram paths)."""
+    eng = run("cfg3", hist_path=hist_path)
     np.testing.assert_array_equal(window_sums(eng), eng.cfg.n)
     u = eng.unions[0]
     assert torch.isfinite(u).all() and float(u.min()) >= 0.0 and float(u.max()) <= 1.0
@@ -88,11 +89,11 @@ def test_cfg4_shard_global_histogram_path_conserves_particles():
 
 @pytest.mark.parametrize("mode", ["production", "reference"])
 def test_long_horizon_window_split_equals_global_path(mode):
-    """T = 500 (cfg4 shape): the engine runs steps 1..264 on shared-memory windows and the
-    rest on global atomics (two launches, particle state handed over); bit-identical to
-    the whole horizon on the global path (window_budget_kb=0)."""
+    """T = 500 (cfg4 shape): with hist_path="smem" the engine runs steps 1..264 on shared-
+    memory windows and the rest on global reductions (two launches, particle state handed
+    over); bit-identical to the whole horizon on the (default) global path."""
     n = 65536 if mode == "production" else 4096
-    a = run("cfg4_rank", mode=mode, humans=2, n=n, budget_kb=46.0)
+    a = run("cfg4_rank", mode=mode, humans=2, n=n, budget_kb=46.0, hist_path="smem")
     assert a.window_bounds() == [(1, 265), (265, 501)]
     np.testing.assert_array_equal(window_sums(a), n)
     ua = a.unions[0].cpu().numpy()

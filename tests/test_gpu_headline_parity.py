@@ -93,11 +93,12 @@ def sha(a):
 
 # ---- K = 2 / K = 4 launches of replicated golden humans --------------------------------
 
-REPLICATED = [(name, k) for name in ("cfg2_t30", "cfg1_s0", "ragged_w", "max_sizes") for k in (2, 4)]
+REPLICATED = [(name, k, hp) for name in ("cfg2_t30", "cfg1_s0", "ragged_w", "max_sizes") for k in (2, 4)
+              for hp in ("global", "smem")]
 
 
-@pytest.mark.parametrize("name,k", REPLICATED)
-def test_replicated_golden_humans_bit_exact_at_k(name, k):
+@pytest.mark.parametrize("name,k,hist_path", REPLICATED)
+def test_replicated_golden_humans_bit_exact_at_k(name, k, hist_path):
     c, cs, space, q, spec = golden_objects(name)
     thr = NT * (k // 2) * 2 * 4 * 148  # smallest launch gc_predict runs with k particles per thread
     humans = -(-thr // c.n)
@@ -106,7 +107,7 @@ def test_replicated_golden_humans_bit_exact_at_k(name, k):
     tab = PR.action_tables(cs, q, c.dt, dev)
     job = PR.HumanJob(G.HumanState(*c.z0), c.log_w, space.beta_of, space.goal_xy_of, c.seed, c.prefix, 0)
     out = PR.run_predict([job] * humans, [tab], c.n, c.steps, c.dt, 0.0, spec, "reference",
-                         per_human_layers=False, want_hyp=True, want_xy=True)
+                         per_human_layers=False, want_hyp=True, want_xy=True, hist_path=hist_path)
     geo = out["geometry"]
     hyp, xy = out["hyp"], out["xy"]
     assert bool((hyp == hyp[0]).all()) and bool((xy == xy[0]).all())
@@ -136,10 +137,11 @@ def cfg3_jobs(meta, tabs):
     return jobs
 
 
-def test_cfg3_scene_reference_mode_bit_exact():
+@pytest.mark.parametrize("hist_path", ["global", "smem"])
+def test_cfg3_scene_reference_mode_bit_exact(hist_path):
     """run_predict of the 8 cfg3 humans in one K = 4 launch vs the live reference: per-human
     counts, hypothesis draws and final positions bit for bit, smoothed layers, max union and
-    time union <= 1e-15."""
+    time union <= 1e-15 (both histogram paths)."""
     z, meta = cfg3_golden()
     cs, q = G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5)
     dev = torch.device("cuda")
@@ -149,7 +151,7 @@ def test_cfg3_scene_reference_mode_bit_exact():
     assert launch_k(len(jobs) * n) == 4
     spec = G.GridSpec(400, 400, 0.1)
     out = PR.run_predict(jobs, tabs, n, T, meta["dt"], meta["sigma"], spec, "reference", per_human_layers=True,
-                         union64=True, want_hyp=True, want_xy=True)
+                         union64=True, want_hyp=True, want_xy=True, hist_path=hist_path)
     geo = out["geometry"]
     rows = out["counts"].view(len(jobs), geo.human_stride).cpu().numpy().view(np.uint32).astype(np.int64)
     for i, (j, hm) in enumerate(zip(jobs, meta["humans"])):

@@ -22,8 +22,16 @@ def main():
     ap.add_argument("--n", type=int, default=262144)
     ap.add_argument("--cycles", type=int, default=2)
     ap.add_argument("--summary", action="store_true", help="one line: mean K2 ms over cycles 1..")
+    ap.add_argument("--uniform", action="store_true", help="keep the uniform prior (no belief updates)")
+    ap.add_argument("--betas", default=None, help="comma-separated rationality set (default log_spaced(5))")
+    ap.add_argument("--goal-radius", type=float, default=None)
     a = ap.parse_args()
-    sc = make_scene("cfg3", cycles=4, humans=a.humans)
+    sc = make_scene("cfg3", cycles=4, humans=a.humans, goal_radius=a.goal_radius)
+    if a.betas:
+        from paper_2603_01122_b200.agents import RationalitySet
+        from paper_2603_01122_b200.belief import HypothesisSpace
+        rs = RationalitySet(tuple(float(b) for b in a.betas.split(",")))
+        sc.spaces = [HypothesisSpace(rs, sp.goals) for sp in sc.spaces]
     eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec,
                       EngineConfig(n=a.n, steps=a.steps, dt=sc.dt, mode=a.mode))
     eng.prime(sc.warmup_track[0])
@@ -31,7 +39,7 @@ def main():
     k2 = []
     for k in range(a.cycles):
         eng.stage(sc.warmup_track[1 + k], buf=0)
-        eng.run_cycle(buf=0, events=ev)
+        eng.run_cycle(buf=0, events=ev, with_update=not a.uniform)
         torch.cuda.synchronize()
         k2.append(ev[0].elapsed_time(ev[1]))
         if not a.summary:
