@@ -150,7 +150,7 @@ def main():
     import sass_extract
     import sass_summary
     so = os.path.join(ROOT, "paper_2603_01122_b200", "_lib", "libgridcast_b200.so")
-    for name, fn in (("k_predict_production", "_ZN2gc9k_predictILi3ELi4ELb0EEEvNS_7KParamsE"),
+    for name, fn in (("k_predict_production", "_ZN2gc9k_predictILi3ELi4ELb0ELb0EEEvNS_7KParamsE"),
                      ("k_epilogue", "_ZN2gc10k_epilogueILi3EEEvNS_7EParamsE"),
                      ("k_belief", "_ZN2gc8k_beliefENS_7BParamsE")):
         open(os.path.join(prof, f"{a.tag}_sass_{name}.txt"), "w").write(sass_extract.extract(so, fn) + "\n")
