@@ -36,6 +36,9 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 #ifndef GC_FFMA2
 #define GC_FFMA2 1  // packed FP32x2 heading loop (sm_100 FFMA2)
 #endif
+#ifndef GC_PROD_MIN_CTAS
+#define GC_PROD_MIN_CTAS 4  // resident CTAs per SM of the production K2 (64 registers)
+#endif
 #ifndef GC_REF_MIN_CTAS
 #define GC_REF_MIN_CTAS 2  // resident CTAs per SM of the reference-arithmetic K2 (119 regs, no spills: 6 % faster than 4)
 #endif
@@ -558,7 +561,7 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
 // particles, so a per-CTA cell count cannot overflow its half-word)
 template <int MODE, int K, bool WTH, bool HSM>
-__global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : 4) k_predict(const KParams P) {
+__global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PROD_MIN_CTAS) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ SmemTabs S;
     // the factorised sampler keeps particles in grid units u = (x - origin) / res: the
