@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GC_ABI_VERSION 2
+#define GC_ABI_VERSION 3
 
 typedef enum {
     GC_OK = 0,
@@ -159,6 +159,14 @@ typedef struct {
      * Both give identical counts; the global form measured 3-5 % faster on every belief
      * shape tried and keeps its speed at long horizons whose windows exceed shared memory. */
     int32_t hist_path;
+    /* reference RNG modes (GC_RNG_REFERENCE / GC_RNG_UNIFORMS): each particle-step first
+     * evaluates the action weights with the hardware ex2 and accepts the pick only when the
+     * uniform lies outside a proven error margin around the bracketing cdf entries (then the
+     * reference's numpy-exp pick is the same); otherwise it runs numpy's exp.  The results
+     * are bit-identical either way.  ref_exact_only = 1 always runs numpy's exp (A/B). */
+    int32_t ref_exact_only;
+    /* optional (1,) counter: reference-mode particle-steps that took the numpy-exp path */
+    uint64_t *d_ref_fallbacks;
 } gc_predict_args;
 
 enum { GC_HIST_GLOBAL = 0, GC_HIST_SMEM = 1 };

@@ -75,6 +75,7 @@ class PredictArgs(ctypes.Structure):
         ("d_hyp_out", P), ("d_xy_out", P), ("d_error", P),
         ("t_begin", I32), ("t_end", I32), ("d_state_xy", P), ("d_state_hyp", P),
         ("p_offset", I32), ("hist_path", I32),
+        ("ref_exact_only", I32), ("d_ref_fallbacks", P),
     ]
 
 

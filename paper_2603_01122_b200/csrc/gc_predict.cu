@@ -40,7 +40,7 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 #define GC_PROD_MIN_CTAS 4  // resident CTAs per SM of the production K2 (64 registers)
 #endif
 #ifndef GC_REF_MIN_CTAS
-#define GC_REF_MIN_CTAS 2  // resident CTAs per SM of the reference-arithmetic K2 (119 regs, no spills: 6 % faster than 4)
+#define GC_REF_MIN_CTAS 3  // resident CTAs per SM of the reference-arithmetic K2 (79 regs, no spills; 44.7 ms at cfg3 vs 47.8 at 2, 48.6 at 4)
 #endif
 #ifndef GC_WORLD_CELLS
 #define GC_WORLD_CELLS 1  // production particles in float32 world coordinates, exact cells
@@ -83,6 +83,7 @@ struct KParams {
     int smem_window;
     int win_cap_words;  // u32 words the host allocated for the window (incl. the sink word)
     int act_off;  // byte offset of SmemAct in dynamic shared memory (REF/GEN modes)
+    int ref_off;  // byte offset of SmemRefState (MODE_REF)
     int dyn_smem; // dynamic shared memory bytes of the launch (bounds checks)
     int t_begin, t_end;          // steps [t_begin, t_end) of this launch (1-based)
     int p_offset;                // global index of this launch's first particle (particle sharding)
@@ -91,6 +92,8 @@ struct KParams {
     int *hyp_out;
     float *xy_out;
     unsigned *error;
+    int ref_filter;                        // MODE_REF: MUFU filter + exact fallback (ref_pick)
+    unsigned long long *ref_fallbacks;     // MODE_REF: particle-steps resolved by the exact path, or NULL
     // headings shared by every table of a factorised launch (constant-bank operands)
     float hcos[NBF], hsin[NBF], hth2[NBF];
 };
@@ -133,6 +136,13 @@ struct alignas(16) SmemAct {
     float ax[MAXM], ay[MAXM], aat[MAXM], adx[MAXM], ady[MAXM];
 };
 
+// MODE_REF: per-slot particle state of the runtime slot loop (dynamic shared memory, after
+// SmemAct)
+struct alignas(16) SmemRefState {
+    float2 pos[4 * 256];  // float32 world position of particle slot k*NT+tid
+    int fwr[4 * 256];     // GC_HIST_SMEM: the window word slot k*NT+tid added to first, or -1
+};
+
 struct SmemTabs {
     // production: (goal x, goal y, k log2e, c log2e) per hypothesis -- one LDS.128;
     // MODE_FACTS: (goal x, goal y, k log2e, Ka) and hq = (Kb, Kc, c log2e, sum_b H_b)
@@ -147,14 +157,9 @@ struct SmemTabs {
     int n_hyp, m_keep, q_kind, n_speeds;
     float wth;
     unsigned char phyp[4 * 256];  // hypothesis index of particle slot k*NT+tid (frees registers)
-    // MODE_REF: the CTA's particles counting-sorted by hypothesis (slot -> particle offset)
-    unsigned short perm[4 * 256];
-    unsigned char shyp[4 * 256];
-    int hcnt[MAXH];
 };
 
 // ---- reference float32 step (prediction.py:147-162), 3 passes, no stored row --------
-constexpr float EXP_NP_ZERO = -103.97208404541015625f;  // exp_np(x) == 0 for every x below this
 __device__ __forceinline__ float ref_logit(const SmemAct &S, int k, float rx, float ry, float d2,
                                            float beta, int qk) {
     float L;
@@ -189,22 +194,15 @@ __device__ __forceinline__ float2 ref_logit2(const SmemAct &S, int k, float rx, 
     return make_float2(__fmul_rn(L.x, beta), __fmul_rn(L.y, beta));
 }
 
-__device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
-    const float rx = __fsub_rn(x, H.hgx[h]), ry = __fsub_rn(y, H.hgy[h]);
-    const float d2 = __fadd_rn(__fmul_rn(rx, rx), __fmul_rn(ry, ry));
-    const float beta = H.hb[h];
-    const int mk = H.m_keep, qk = H.q_kind;
-    float M = -__int_as_float(0x7f800000);
-    int k = 0;
-    for (; k + 1 < mk; k += 2) {  // action pairs on the packed FP32x2 pipe
-        const float2 L = ref_logit2(S, k, rx, ry, d2, beta, qk);
-        M = fmaxf(M, fmaxf(L.x, L.y));
-    }
-    if (k < mk) M = fmaxf(M, ref_logit(S, k, rx, ry, d2, beta, qk));
-    // pass 2: the sequential cumsum, remembering it at the end of each of NBLK blocks of
-    // B actions -- values of the same chain, so the search below is bit-identical to a
-    // scan from the first action but recomputes only the one block that holds r.  B is
-    // even so the action pairs stay 8-byte aligned; the sum itself stays sequential.
+// Passes 2-3 of the reference step given the max logit M: numpy's exp per action, the
+// sequential float32 cumsum, inverse CDF (prediction.py:152-160).  The running sum is
+// remembered at the end of each of NBLK blocks of B actions -- values of the same chain,
+// so the search is bit-identical to a scan from the first action but recomputes only the
+// one block that holds r.  B is even so the action pairs stay 8-byte aligned; the sum
+// itself stays sequential.  Not inlined: behind the filter (ref_pick) it runs for a small
+// fraction of the particle-steps, and one copy serves the K unrolled particle slots.
+static __device__ __noinline__ int ref_pick_exact(const SmemAct &S, float rx, float ry, float d2, float beta, int mk,
+                                           int qk, float M, float u) {
     constexpr int NBLK = 12;
     const int B = 2 * ((mk + 2 * NBLK - 1) / (2 * NBLK));
     float blk[NBLK];
@@ -215,13 +213,7 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
         int kk = j * B;
         for (; kk + 1 < k1; kk += 2) {
             const float2 L = ref_logit2(S, kk, rx, ry, d2, beta, qk);
-            const float2 xm = px_add(L, px2(-M));
-            // numpy's float32 exp is exactly 0 below -103.97208404541015625 (App. A.2) and
-            // c + 0 == c: when every lane's pair underflows the pair is skipped -- bit-exact.
-            // (The CTA's particles are sorted by hypothesis, so a warp's lanes share their
-            // logit profile and the vote succeeds for the far-from-goal actions of large beta.)
-            if (__all_sync(__activemask(), xm.x < EXP_NP_ZERO && xm.y < EXP_NP_ZERO)) continue;
-            const float2 w = exp_np2(xm);
+            const float2 w = exp_np2(px_add(L, px2(-M)));
             c = (kk == 0) ? w.x : __fadd_rn(c, w.x);
             c = __fadd_rn(c, w.y);
         }
@@ -239,7 +231,7 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
     for (int j = 0; j < NBLK - 1; ++j) {
         if (blk[j] < r) { jb = j + 1; cc = blk[j]; }
     }
-    k = jb * B;
+    int k = jb * B;
     const int kend = min(mk, (jb + 1) * B);
     for (; k < kend; ++k) {
         const float w = exp_np(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M));
@@ -248,6 +240,93 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
     }
     if (k == kend && kend < mk) k = mk;  // cannot happen for a monotone chain: keep the clamp semantics
     return k < mk - 1 ? k : mk - 1;
+}
+
+// Error budget of the reference-mode filter (ref_pick).  With w_k = exp_np(x_k) the
+// reference's weight and w~_k = ex2.approx.ftz(fl(x_k log2e)) the filter's (x_k = fl(L_k - M)
+// <= 0 identical in both):
+//   |w~_k - e^x_k| <= EPS_MUFU e^x_k + A_W   (tools/cuda_checks/ex2_filter_err.cu,
+//                                            exhaustive over every float32 x in [-104, 0])
+//   |w_k - e^x_k|  <= EPS_NP e^x_k           (numpy's float32 exp, exhaustive on the CPU:
+//                                            2.13e-7 max relative error)
+// so |w~_k - w_k| <= EPS_W w_k + A_W.  Each chain's sequential float32 sum c_k is within
+// (m - 1) 2^-24 C of the exact sum of its weights (C >= every total; C >= 1 because the
+// argmax has x = 0 and weight exactly 1 in both), hence |c_k - c~_k| <= D with
+// D = C (2 (m - 1) 2^-24 + EPS_W) + m A_W, and |r - r~| <= D + 2^-23 C for r = fl(u c_N).
+// If the filter's pick k has c~_{k-1} < r~ - G and c~_k > r~ + G with G = 2D + 2^-23 C, then
+// c_{k-1} < r <= c_k: the reference picks the same k (first cdf entry >= r).  G is
+// evaluated with a 1.002 safety factor on C~ (covers C* vs C~ and the float evaluation of
+// the margins).
+#define GC_REF_FILTER_EPS_W 6.0e-7f  // EPS_MUFU + EPS_NP with slack (measured 2.13e-7 + see tool)
+#define GC_REF_FILTER_A_W 4.0e-8f    // argument rounding |x| e^x 7.3e-8 <= 2.7e-8, FTZ 2^-126
+
+// The reference float32 step (prediction.py:147-162): per-action logit, max shift, numpy
+// exp, sequential cumsum, first cdf entry >= u * total.  The logits and the max are
+// computed exactly as the reference does; the exponentials are then first evaluated with
+// the MUFU ex2 (one instruction instead of numpy's ~30-instruction float32 exp), and the
+// decision is accepted only when r lies farther than the proven error margin G from both
+// cdf entries that bracket it -- the reference's decision is then the same (see the error
+// budget above).  Otherwise (a few % of particle-steps) the exact passes run.  The result is
+// bit-identical to ref_pick_exact alone for every input; `filter` = false forces the exact
+// path (A/B and tests), `fallbacks` counts the particle-steps that took it.
+__device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u,
+                                        bool filter = true, unsigned long long *fallbacks = nullptr) {
+    const float rx = __fsub_rn(x, H.hgx[h]), ry = __fsub_rn(y, H.hgy[h]);
+    const float d2 = __fadd_rn(__fmul_rn(rx, rx), __fmul_rn(ry, ry));
+    const float beta = H.hb[h];
+    const int mk = H.m_keep, qk = H.q_kind;
+    float M = -__int_as_float(0x7f800000);
+    int k = 0;
+#pragma unroll 4
+    for (; k + 1 < mk; k += 2) {  // action pairs on the packed FP32x2 pipe
+        const float2 L = ref_logit2(S, k, rx, ry, d2, beta, qk);
+        M = fmaxf(M, fmaxf(L.x, L.y));
+    }
+    if (k < mk) M = fmaxf(M, ref_logit(S, k, rx, ry, d2, beta, qk));
+    if (filter) {
+        constexpr float L2E = 1.4426950408889634f;
+        constexpr int NBLK = 12;
+        const int B = 2 * ((mk + 2 * NBLK - 1) / (2 * NBLK));
+        float blk[NBLK];
+        float c = 0.f;
+#pragma unroll
+        for (int j = 0; j < NBLK; ++j) {
+            const int k1 = min(mk, (j + 1) * B);
+            int kk = j * B;
+#pragma unroll 2
+            for (; kk + 1 < k1; kk += 2) {
+                const float2 L = ref_logit2(S, kk, rx, ry, d2, beta, qk);
+                const float2 t = px_mul(px_add(L, px2(-M)), px2(L2E));
+                c = __fadd_rn(c, ex2_approx(t.x));
+                c = __fadd_rn(c, ex2_approx(t.y));
+            }
+            if (kk < k1) c = __fadd_rn(c, ex2_approx(__fmul_rn(__fsub_rn(ref_logit(S, kk, rx, ry, d2, beta, qk), M), L2E)));
+            blk[j] = c;
+        }
+        const float r = __fmul_rn(u, c);
+        int jb = 0;
+        float cc = 0.f;
+#pragma unroll
+        for (int j = 0; j < NBLK - 1; ++j) {
+            if (blk[j] < r) { jb = j + 1; cc = blk[j]; }
+        }
+        // rescan the block holding r with the same operations (the same chain values)
+        k = jb * B;
+        const int kend = min(mk, (jb + 1) * B);
+        float lower = cc;
+        for (; k < kend; ++k) {
+            lower = cc;
+            cc = __fadd_rn(cc, ex2_approx(__fmul_rn(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M), L2E)));
+            if (!(cc < r)) break;
+        }
+        const float fm = (float)(mk - 1);
+        const float grel = 1.002f * (2.f * (2.f * fm * 0x1p-24f + GC_REF_FILTER_EPS_W) + 0x1p-23f);
+        const float G = fmaf(c, grel, 2.002f * (fm + 1.f) * GC_REF_FILTER_A_W);
+        // NaN-safe: any NaN fails the comparisons and takes the exact path
+        if (k < kend && __fsub_rn(cc, r) > G && (k == 0 || __fsub_rn(r, lower) > G)) return k < mk - 1 ? k : mk - 1;
+    }
+    if (fallbacks) atomicAdd(fallbacks, 1ull);
+    return ref_pick_exact(S, rx, ry, d2, beta, mk, qk, M, u);
 }
 
 // ---- production generic per-action softmax ------------------------------------------
@@ -760,57 +839,111 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             if (P.hyp_out) P.hyp_out[(long long)h * P.n + p] = hi;
         }
     }
-    // MODE_REF: the CTA's particles are re-dealt to the slots in hypothesis order (counting
-    // sort), so the 32 lanes of a warp's slot mostly share a hypothesis -- and with it the
-    // shape of the per-action logits, which lets ref_pick skip exp evaluations that are
-    // exactly 0 for the whole warp.  Which thread steps which particle does not change any
-    // result: a particle's draws are keyed by its own index, counts are integer sums.
-    // pp[k]: the CTA-relative particle index of slot k (-1: padded slot).
+    // pp[k]: the CTA-relative particle index of slot k (-1: padded slot)
     int pp[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) pp[k] = (pbase + tid * K + k < P.n && tid * K + k < P.ppc) ? tid * K + k : -1;
-    if (MODE == MODE_REF) {
-        for (int i = tid; i < MAXH; i += NT) S.hcnt[i] = 0;
-        __syncthreads();
-        int rank[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) rank[k] = pp[k] >= 0 ? atomicAdd(&S.hcnt[ph[k]], 1) : 0;
-        __syncthreads();
-        if (tid == 0) {  // exclusive scan over the (<= 128) hypotheses
-            int acc = 0;
-            for (int i = 0; i < nh; ++i) { const int c = S.hcnt[i]; S.hcnt[i] = acc; acc += c; }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (pp[k] < 0) continue;
-            const int slot = S.hcnt[ph[k]] + rank[k];
-            S.perm[slot] = (unsigned short)pp[k];
-            S.shyp[slot] = (unsigned char)ph[k];
-        }
-        __syncthreads();
-        const int nvalid = min(P.ppc, P.n - pbase);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int slot = tid * K + k;
-            pp[k] = slot < nvalid ? (int)S.perm[slot] : -1;
-            ph[k] = slot < nvalid ? (int)S.shyp[slot] : 0;
-            if (P.t_begin > 1 && pp[k] >= 0) {  // a resumed chunk: this slot's particle state
-                const long long g = (long long)h * P.n + pbase + pp[k];
-                const float2 st = P.state_xy[g];
-                px[k] = st.x; py[k] = st.y;
-            } else {
-                px[k] = sx0; py[k] = sy0;
-            }
-        }
-    }
     SSPool pool_step;
     if (MODE == MODE_REF) { pool_step = pool_pre; ss_absorb(pool_step, 1u); }  // STEP_DRAWS
 
     const long long hbase = (long long)h * P.human_stride;
+    bool overflow = false;  // a particle outside its reachable window (reported once at exit)
+    if constexpr (MODE == MODE_REF) {
+        // Reference arithmetic: one copy of the step code for the K particle slots (a
+        // runtime slot loop; positions and first-touch words in shared memory) -- the
+        // per-particle step is long (filter + exact fallback), so the K-fold unrolled form
+        // overflowed the instruction cache and held 121 registers.
+        SmemRefState &RS = *reinterpret_cast<SmemRefState *>(smem_dyn + P.ref_off);
+#pragma unroll
+        for (int k = 0; k < K; ++k) RS.pos[k * NT + tid] = make_float2(px[k], py[k]);
+        // the thread's K particles are consecutive and aligned to K (ppc, p_offset % 4 == 0),
+        // so their numpy float32 draws j0 .. j0 + K - 1 of the 1024-particle chunk stream are
+        // u32 halves of words (j0 >> 1) .. of ONE Philox4x64 block: one block per thread-step
+        const int pg0 = pbase + tid * K + P.p_offset;
+        const int j0 = pg0 & 1023;
+        for (int t = P.t_begin; t < P.t_end; ++t) {
+            const int R = __ldg(&P.step_r[t - 1]);
+            const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
+            const int y0 = max(0, cy - R), y1 = min(P.grid_h - 1, cy + R);
+            const int ww = x1 - x0 + 1, wh = y1 - y0 + 1;
+            unsigned *gcount = P.counts + hbase + __ldg(&P.step_off[t - 1]);
+            GC_DCHECK(__ldg(&P.step_off[t - 1]) + (long long)ww * wh <= P.human_stride);
+            uint64_t blkw[4] = {0, 0, 0, 0};
+            if (!P.uniforms) {
+                SSPool s = pool_step;
+                ss_absorb(s, (unsigned)t);
+                ss_absorb(s, (unsigned)(pg0 >> 10));
+                uint64_t sk0, sk1;
+                ss_key(s, sk0, sk1);
+                philox4x64((uint64_t)(j0 >> 3) + 1, sk0, sk1, blkw);
+            }
+#pragma unroll 1
+            for (int k = 0; k < K; ++k) {
+                const int p = pbase + tid * K + k;
+                const bool valid = p < P.n && tid * K + k < P.ppc;
+                int local = -1;
+                if (valid) {
+                    float2 xy = RS.pos[k * NT + tid];
+                    float u;
+                    if (P.uniforms) {
+                        u = __ldg(&P.uniforms[((long long)h * P.steps + (t - 1)) * P.n + p]);
+                    } else {
+                        const int j = j0 + k, w = (j >> 1) & 3;
+                        const uint64_t wd = w == 0 ? blkw[0] : (w == 1 ? blkw[1] : (w == 2 ? blkw[2] : blkw[3]));
+                        const uint32_t u32 = (j & 1) ? (uint32_t)(wd >> 32) : (uint32_t)wd;
+                        u = (float)(u32 >> 8) * (1.0f / 16777216.0f);  // random(dtype=float32)
+                    }
+                    const int a = ref_pick(S, A, xy.x, xy.y, S.phyp[k * NT + tid], u, P.ref_filter != 0,
+                                           P.ref_fallbacks);
+                    xy.x = __fadd_rn(xy.x, A.adx[a]);
+                    xy.y = __fadd_rn(xy.y, A.ady[a]);
+                    RS.pos[k * NT + tid] = xy;
+                    int ix, iy;
+                    cell_ref(xy.x, xy.y, P, ix, iy);
+                    const int lx = ix - x0, ly = iy - y0;
+                    if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) overflow = true;
+                    else local = ly * ww + lx;
+                }
+                if (HSM) {
+                    const bool has = local >= 0;
+                    const unsigned off = has ? 2u * (unsigned)local : 4u * (unsigned)words;
+                    GC_DCHECK(!has || (local < ww * wh && (int)(off >> 2) < words));
+                    const unsigned old = atomicAdd(reinterpret_cast<unsigned *>(reinterpret_cast<char *>(win) + (off & ~3u)),
+                                                   (off & 2u) ? 0x10000u : 1u);
+                    RS.fwr[k * NT + tid] = (has && old == 0u) ? (local >> 1) : -1;
+                } else {
+                    const unsigned same = __match_any_sync(0xffffffffu, local);
+                    if (local >= 0 && (int)(tid & 31) == __ffs(same) - 1) {
+                        GC_DCHECK(local < ww * wh);
+                        atomicAdd(&gcount[local], (unsigned)__popc(same));
+                    }
+                }
+            }
+            if (HSM) {
+                __syncthreads();
+#pragma unroll 1
+                for (int k = 0; k < K; ++k) {
+                    const int wi = RS.fwr[k * NT + tid];
+                    if (wi < 0) continue;
+                    GC_DCHECK(wi < words);
+                    const unsigned w = win[wi];
+                    win[wi] = 0u;
+                    const unsigned lo = w & 0xFFFFu, hi = w >> 16;
+                    GC_DCHECK(2 * wi + (hi ? 1 : 0) < ww * wh);
+                    if (lo) atomicAdd(&gcount[2 * wi], lo);
+                    if (hi) atomicAdd(&gcount[2 * wi + 1], hi);
+                }
+                __syncthreads();
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const float2 q = RS.pos[k * NT + tid];
+            px[k] = q.x; py[k] = q.y;
+        }
+    } else {
     const float yres = recip_nr(P.res);  // production cell map: the quotient's reciprocal
     U4 rbk = U4{0u, 0u, 0u, 0u};  // K < 4: the block this lane drew for its turn (see below)
-    bool overflow = false;  // a particle outside its reachable window (reported once at exit)
     for (int t = P.t_begin; t < P.t_end; ++t) {
         const int R = __ldg(&P.step_r[t - 1]);
         const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
@@ -818,8 +951,6 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
         const int ww = x1 - x0 + 1, wh = y1 - y0 + 1;
         unsigned *gcount = P.counts + hbase + __ldg(&P.step_off[t - 1]);
         GC_DCHECK(__ldg(&P.step_off[t - 1]) + (long long)ww * wh <= P.human_stride);
-        uint64_t sk0 = 0, sk1 = 0;
-        int key_chunk = -1;
         // fwr[k]: the window word particle slot k added to first this step, or -1 (this
         // thread then owns that word's flush)
         int fwr[K];
@@ -834,7 +965,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
         // that step's words from the lane holding them (shuffles) -- one block per lane
         // per G steps instead of G lanes drawing the same block every step.
         U4 rb = U4{0u, 0u, 0u, 0u};
-        if (MODE != MODE_REF) {
+        {
             const unsigned g4 = (unsigned)((pbase + tid * K + P.p_offset) >> 2);
             if (K == 4) {
                 rb = philox4x32(U4{g4, (unsigned)(t - 1), sc2, sk_hi ^ 0xA11CEu}, PHK0, PHK1);
@@ -852,10 +983,10 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int p = pbase + (MODE == MODE_REF ? pp[k] : tid * K + k);
-            const bool valid = MODE == MODE_REF ? pp[k] >= 0 : (p < P.n && tid * K + k < P.ppc);
+            const int p = pbase + tid * K + k;
+            const bool valid = pp[k] >= 0;
             int local = -1;
-            if (MODE != MODE_REF) {
+            {
                 // production: padded lanes compute too (no divergence), they just do not count
                 float x = px[k], y = py[k];
                 // word (p % 4) of this step's block (K = 4: word k; K < 4: the thread's slice)
@@ -882,32 +1013,6 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
                 const bool inside = lx < (unsigned)ww && ly < (unsigned)wh;
                 overflow |= valid && !inside;
                 local = (valid && inside) ? (int)(ly * ww + lx) : -1;
-            } else if (valid) {
-                float x = px[k], y = py[k];
-                float u;
-                if (P.uniforms) {
-                    u = __ldg(&P.uniforms[((long long)h * P.steps + (t - 1)) * P.n + p]);
-                } else {
-                    const int pg = p + P.p_offset;  // global particle index keys the stream
-                    const int c = pg >> 10;
-                    if (c != key_chunk) {
-                        SSPool s = pool_step;
-                        ss_absorb(s, (unsigned)t);
-                        ss_absorb(s, (unsigned)c);
-                        ss_key(s, sk0, sk1);
-                        key_chunk = c;
-                    }
-                    u = philox64_f32(sk0, sk1, (uint64_t)(pg & 1023));
-                }
-                const int a = ref_pick(S, A, x, y, ph[k], u);
-                x = __fadd_rn(x, A.adx[a]);
-                y = __fadd_rn(y, A.ady[a]);
-                px[k] = x; py[k] = y;
-                int ix, iy;
-                cell_ref(x, y, P, ix, iy);
-                const int lx = ix - x0, ly = iy - y0;
-                if (lx < 0 || lx >= ww || ly < 0 || ly >= wh) overflow = true;
-                else local = ly * ww + lx;
             }
             // the thread whose add finds a window word zero owns that word's flush this
             // step: it remembers the word in a register (no list, no ballot)
@@ -960,11 +1065,12 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             __syncthreads();
         }
     }
+    }  // production step loop
     if (overflow && P.error) atomicOr(P.error, GC_ERRBIT_WINDOW_OVERFLOW);
     if (P.t_end <= P.steps && P.state_xy) {  // hand the particles to the next chunk
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int p = pbase + (MODE == MODE_REF ? pp[k] : tid * K + k);
+            const int p = pbase + tid * K + k;
             if (pp[k] >= 0) {
                 const long long g = (long long)h * P.n + p;
                 P.state_xy[g] = make_float2(px[k], py[k]);
@@ -975,7 +1081,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
     if (P.xy_out) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const int p = pbase + (MODE == MODE_REF ? pp[k] : tid * K + k);
+            const int p = pbase + tid * K + k;
             if (pp[k] >= 0) {
                 P.xy_out[((long long)h * P.n + p) * 2] = GRIDU ? fmaf(px[k], P.res, P.ox) : px[k];
                 P.xy_out[((long long)h * P.n + p) * 2 + 1] = GRIDU ? fmaf(py[k], P.res, P.oy) : py[k];
@@ -1062,7 +1168,8 @@ gc_status launch_predict(const KParams &P, int grid, size_t smem, cudaStream_t s
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(configured.load(std::memory_order_acquire) & bit)) {
         const int extra = (int)(sizeof(SmemAct) > (size_t)MAXH * NBF * 4 ? sizeof(SmemAct) : (size_t)MAXH * NBF * 4);
-        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 + extra));
+        GC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     64 * 1024 + extra + (MODE == MODE_REF ? (int)sizeof(SmemRefState) : 0)));
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     fn<<<grid, NT, smem, st>>>(P);
@@ -1167,6 +1274,8 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     P.step_r = a->d_step_r; P.step_off = (const long long *)a->d_step_off;
     P.human_stride = a->human_stride; P.counts = a->d_counts;
     P.hyp_out = a->d_hyp_out; P.xy_out = a->d_xy_out; P.error = a->d_error;
+    P.ref_filter = a->ref_exact_only ? 0 : 1;
+    P.ref_fallbacks = (unsigned long long *)a->d_ref_fallbacks;
     P.t_begin = a->t_begin > 0 ? a->t_begin : 1;
     P.t_end = a->t_end > 0 ? a->t_end : a->steps + 1;
     GC_CHECK_ARG(P.t_begin < P.t_end && P.t_end <= a->steps + 1, "gc_predict: bad step range");
@@ -1210,7 +1319,9 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     bool stdh = fact;
     for (int b = 0; stdh && b < NBF; ++b) stdh = P.hcos[b] == hStdCos[b] && P.hsin[b] == hStdSin[b];
     const size_t htab = (a->rng_mode == GC_RNG_PRODUCTION && stdh && wth) ? (size_t)MAXH * NBF * 4 : 0;
-    const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : htab);
+    const bool refm = a->rng_mode != GC_RNG_PRODUCTION;
+    P.ref_off = P.act_off + (int)sizeof(SmemAct);  // SmemAct is a multiple of 16 bytes
+    const size_t smem = (size_t)P.act_off + (needs_act ? sizeof(SmemAct) : htab) + (refm ? sizeof(SmemRefState) : 0);
     P.dyn_smem = (int)smem;
     cudaStream_t st = (cudaStream_t)stream;
     const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? (stdh ? MODE_FACTS : MODE_FACT) : MODE_GEN)

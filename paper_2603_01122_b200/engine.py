@@ -79,6 +79,10 @@ class EngineConfig:
     # shape measured) -- or "smem" -- shared-memory windows where they fit
     # (window_budget_kb then splits long horizons)
     hist_path: str = "global"
+    # reference RNG mode: K2 evaluates the action weights with the hardware ex2 and runs
+    # numpy's exp only where the pick is within the proven error margin (bit-identical
+    # either way, gc_predict_args.ref_exact_only); False = numpy's exp everywhere
+    ref_filter: bool = True
     # host read-back of the union (run_cycle / capture with d2h=...): "tiles" publishes only
     # the 32 x 32 tiles that are nonzero now or were nonzero in the host stack's previous
     # cycle (gc_publish_tiles: kernel stores into the pinned, mapped host stack); "dense"
@@ -347,6 +351,7 @@ class CycleEngine:
         a.n_humans, a.n, a.steps, a.rng_mode = H, self.n_local, cfg.steps, MODES[cfg.mode]
         a.p_offset = self.p_offset
         a.hist_path = _lib.GC_HIST_SMEM if cfg.hist_path == "smem" else _lib.GC_HIST_GLOBAL
+        a.ref_exact_only = 0 if cfg.ref_filter else 1
         a.grid_w, a.grid_h = self.spec.width, self.spec.height
         a.origin_x32 = float(np.float32(self.spec.origin[0]))
         a.origin_y32 = float(np.float32(self.spec.origin[1]))

@@ -202,14 +202,19 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
                 union64: bool = False, union32: bool = False, time_union: bool = False,
                 uniforms: Optional[torch.Tensor] = None, hyp_in: Optional[torch.Tensor] = None,
                 hyp_u: Optional[torch.Tensor] = None, want_hyp: bool = False, want_xy: bool = False,
-                stream=None, union_mode: str = "max", hist_path: str = "global"):
+                stream=None, union_mode: str = "max", hist_path: str = "global",
+                ref_exact_only: bool = False, ref_fallbacks: Optional[torch.Tensor] = None):
     """Batched K2 + K3 launch; returns a dict of device tensors.  union_mode "max" merges
     the humans by atomicMax inside K3; "independent" (1 - prod(1 - p), occupancy.py:180-184)
     merges the per-human float64 layers afterwards in human order (gc_union_layers).
 
     ``uniforms`` (humans, steps, n) float32 and ``hyp_u`` (humans, n) float64 select
     GC_RNG_UNIFORMS: the reference arithmetic driven by caller-supplied draws (e.g. the
-    reference's own rng.stream draws, prediction.py:128-131, :186-192)."""
+    reference's own rng.stream draws, prediction.py:128-131, :186-192).
+
+    ``ref_exact_only`` runs numpy's exp for every reference-mode particle-step instead of
+    the MUFU filter with exact fallback (bit-identical results; A/B); ``ref_fallbacks`` (a
+    (1,) int64 device tensor) accumulates the particle-steps that took the exact path."""
     if hyp_u is not None and uniforms is None:
         raise ValueError("hyp_u needs uniforms (GC_RNG_UNIFORMS)")
     if uniforms is not None:
@@ -275,6 +280,11 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     if hist_path not in ("global", "smem"):
         raise ValueError(f"unknown hist_path {hist_path!r}")
     a.hist_path = _lib.GC_HIST_SMEM if hist_path == "smem" else _lib.GC_HIST_GLOBAL
+    a.ref_exact_only = int(bool(ref_exact_only))
+    if ref_fallbacks is not None:
+        if ref_fallbacks.dtype != torch.int64 or ref_fallbacks.numel() < 1 or not ref_fallbacks.is_cuda:
+            raise ValueError("ref_fallbacks must be a (1,) int64 device tensor")
+        a.d_ref_fallbacks = ref_fallbacks.data_ptr()
     sh = stream_handle(stream)
     _lib.check(_lib.lib().gc_predict(ctypes.byref(a), sh), "gc_predict")
 

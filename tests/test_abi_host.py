@@ -46,7 +46,7 @@ def test_library_is_sm100a(L):
 
 
 def test_abi_version(L):
-    assert L.gc_abi_version() == 2
+    assert L.gc_abi_version() == 3
 
 
 def test_abi_rng_matches_reference_streams(L):

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--uniform", action="store_true", help="keep the uniform prior (no belief updates)")
     ap.add_argument("--betas", default=None, help="comma-separated rationality set (default log_spaced(5))")
     ap.add_argument("--goal-radius", type=float, default=None)
+    ap.add_argument("--ref-exact", action="store_true", help="reference mode: numpy exp everywhere (no filter)")
     a = ap.parse_args()
     sc = make_scene("cfg3", cycles=4, humans=a.humans, goal_radius=a.goal_radius)
     if a.betas:
@@ -33,7 +34,7 @@ def main():
         rs = RationalitySet(tuple(float(b) for b in a.betas.split(",")))
         sc.spaces = [HypothesisSpace(rs, sp.goals) for sp in sc.spaces]
     eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec,
-                      EngineConfig(n=a.n, steps=a.steps, dt=sc.dt, mode=a.mode))
+                      EngineConfig(n=a.n, steps=a.steps, dt=sc.dt, mode=a.mode, ref_filter=not a.ref_exact))
     eng.prime(sc.warmup_track[0])
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     k2 = []
