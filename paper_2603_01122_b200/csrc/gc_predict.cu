@@ -246,19 +246,24 @@ static __device__ __noinline__ int ref_pick_exact(const SmemAct &S, float rx, fl
 // reference's weight and w~_k = ex2.approx.ftz(fl(x_k log2e)) the filter's (x_k = fl(L_k - M)
 // <= 0 identical in both):
 //   |w~_k - e^x_k| <= EPS_MUFU e^x_k + A_W   (tools/cuda_checks/ex2_filter_err.cu,
-//                                            exhaustive over every float32 x in [-104, 0])
+//                                            exhaustive over every float32 x in [-104, 0]:
+//                                            EPS_MUFU = 3e-7 holds with an additive excess
+//                                            of at most 3.7e-10)
 //   |w_k - e^x_k|  <= EPS_NP e^x_k           (numpy's float32 exp, exhaustive on the CPU:
-//                                            2.13e-7 max relative error)
-// so |w~_k - w_k| <= EPS_W w_k + A_W.  Each chain's sequential float32 sum c_k is within
-// (m - 1) 2^-24 C of the exact sum of its weights (C >= every total; C >= 1 because the
-// argmax has x = 0 and weight exactly 1 in both), hence |c_k - c~_k| <= D with
-// D = C (2 (m - 1) 2^-24 + EPS_W) + m A_W, and |r - r~| <= D + 2^-23 C for r = fl(u c_N).
-// If the filter's pick k has c~_{k-1} < r~ - G and c~_k > r~ + G with G = 2D + 2^-23 C, then
-// c_{k-1} < r <= c_k: the reference picks the same k (first cdf entry >= r).  G is
-// evaluated with a 1.002 safety factor on C~ (covers C* vs C~ and the float evaluation of
-// the margins).
-#define GC_REF_FILTER_EPS_W 6.0e-7f  // EPS_MUFU + EPS_NP with slack (measured 2.13e-7 + see tool)
-#define GC_REF_FILTER_A_W 4.0e-8f    // argument rounding |x| e^x 7.3e-8 <= 2.7e-8, FTZ 2^-126
+//                                            2.13e-7 max relative error, normal results)
+// so |w~_k - w_k| <= EPS_W w_k + A_W.  A sequential float32 sum is within 2^-24 sum_{j<=k} c_j
+// of the exact sum of its terms (each add rounds by at most 2^-24 of its result, the
+// first term is exact), so with T~_k = sum_{j<=k} c~_j (bounded from the block sums: every
+// c~_j of block b is <= blk[b]) the two chains differ at index k by at most
+//   D_k = 2^-23 T~_k + EPS_W c~_k + (k + 1) A_W,
+// and r = fl(u c_N) differs from r~ = fl(u c~_N) by at most D_r = u D_N + 2^-23 r~.  If the
+// filter's pick k has r~ - c~_{k-1} > D_{k-1} + D_r and c~_k - r~ > D_k + D_r, then
+// c_{k-1} < r <= c_k: the reference picks the same k (its first cdf entry >= r).  The
+// margins carry a 1.002 factor and a 1e-9 C~ term for the second-order terms (the
+// reference chain's T_k vs T~_k, EPS_W S_k vs EPS_W c~_k, the float evaluation of the
+// margins).  NaN / inf anywhere fails a comparison and takes the exact path.
+#define GC_REF_FILTER_EPS_W 6.0e-7f  // EPS_MUFU + EPS_NP = 5.13e-7, with slack
+#define GC_REF_FILTER_A_W 1.0e-9f    // measured additive excess <= 3.7e-10 (FTZ, argument rounding)
 
 // The reference float32 step (prediction.py:147-162): per-action logit, max shift, numpy
 // exp, sequential cumsum, first cdf entry >= u * total.  The logits and the max are
@@ -305,10 +310,11 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
         }
         const float r = __fmul_rn(u, c);
         int jb = 0;
-        float cc = 0.f;
+        float cc = 0.f, tpre = 0.f, tall = blk[NBLK - 1];
 #pragma unroll
         for (int j = 0; j < NBLK - 1; ++j) {
-            if (blk[j] < r) { jb = j + 1; cc = blk[j]; }
+            tall = __fadd_rn(tall, blk[j]);
+            if (blk[j] < r) { jb = j + 1; cc = blk[j]; tpre = __fadd_rn(tpre, blk[j]); }
         }
         // rescan the block holding r with the same operations (the same chain values)
         k = jb * B;
@@ -319,11 +325,19 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
             cc = __fadd_rn(cc, ex2_approx(__fmul_rn(__fsub_rn(ref_logit(S, k, rx, ry, d2, beta, qk), M), L2E)));
             if (!(cc < r)) break;
         }
-        const float fm = (float)(mk - 1);
-        const float grel = 1.002f * (2.f * (2.f * fm * 0x1p-24f + GC_REF_FILTER_EPS_W) + 0x1p-23f);
-        const float G = fmaf(c, grel, 2.002f * (fm + 1.f) * GC_REF_FILTER_A_W);
-        // NaN-safe: any NaN fails the comparisons and takes the exact path
-        if (k < kend && __fsub_rn(cc, r) > G && (k == 0 || __fsub_rn(r, lower) > G)) return k < mk - 1 ? k : mk - 1;
+        // error margins of the two bracketing cdf entries and of r (error budget above);
+        // all inputs non-negative, evaluated in float with the 1.002 factor
+        const float fB = (float)B, kin = (float)(k - jb * B);
+        const float tb = fB * tpre;                                   // >= T~ of the earlier blocks
+        const float t_lo = fmaf(kin, lower, tb), t_hi = fmaf(kin + 1.f, cc, tb);
+        const float d_r = fmaf(u, fmaf(0x1p-23f, fB * tall, fmaf(GC_REF_FILTER_EPS_W, c, (float)mk * GC_REF_FILTER_A_W)),
+                               0x1p-23f * r);
+        const float d_lo = fmaf(0x1p-23f, t_lo, fmaf(GC_REF_FILTER_EPS_W, lower, (float)k * GC_REF_FILTER_A_W));
+        const float d_hi = fmaf(0x1p-23f, t_hi, fmaf(GC_REF_FILTER_EPS_W, cc, (float)(k + 1) * GC_REF_FILTER_A_W));
+        const float slack = 1e-9f * c;
+        if (k < kend && __fsub_rn(cc, r) > fmaf(1.002f, d_hi + d_r, slack) &&
+            (k == 0 || __fsub_rn(r, lower) > fmaf(1.002f, d_lo + d_r, slack)))
+            return k < mk - 1 ? k : mk - 1;
     }
     if (fallbacks) atomicAdd(fallbacks, 1ull);
     return ref_pick_exact(S, rx, ry, d2, beta, mk, qk, M, u);

@@ -17,10 +17,10 @@
 using namespace gc;
 
 #ifndef EPS_W
-#define EPS_W 3.0e-7  // must match gc_predict.cu GC_REF_FILTER_EPS_W minus numpy's part
+#define EPS_W 3.0e-7  // EPS_MUFU: gc_predict.cu GC_REF_FILTER_EPS_W = EPS_MUFU + numpy (2.13e-7) + slack
 #endif
 #ifndef A_W
-#define A_W 4.0e-8
+#define A_W 1.0e-9
 #endif
 
 __device__ __forceinline__ void amax(unsigned *p, double v) {
