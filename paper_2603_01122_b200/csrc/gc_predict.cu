@@ -134,6 +134,7 @@ __device__ __forceinline__ void cell_fast(float x, float y, const KParams &P, fl
 // after the window; absent from the production kernel)
 struct alignas(16) SmemAct {
     float ax[MAXM], ay[MAXM], aat[MAXM], adx[MAXM], ady[MAXM];
+    float4 axy[MAXM / 2];  // MODE_REF: (ax[2i], ax[2i+1], ay[2i], ay[2i+1]) -- one LDS.128 per action pair
 };
 
 // MODE_REF: per-slot particle state of the runtime slot loop (dynamic shared memory, after
@@ -265,6 +266,94 @@ static __device__ __noinline__ int ref_pick_exact(const SmemAct &S, float rx, fl
 #define GC_REF_FILTER_EPS_W 6.0e-7f  // EPS_MUFU + EPS_NP = 5.13e-7, with slack
 #define GC_REF_FILTER_A_W 1.0e-9f    // measured additive excess <= 3.7e-10 (FTZ, argument rounding)
 
+// Pre-beta logits Q'(k), Q'(k + 1) of an action pair for a compile-time utility kind, op
+// for op the reference's (ref_logit2 before its beta product); (ax, ay) from one LDS.128.
+template <int QK>
+__device__ __forceinline__ float2 ref_q2(const SmemAct &S, int k, float rx, float ry, float d2) {
+    const float2 at = *reinterpret_cast<const float2 *>(&S.aat[k]);
+    if (QK == GC_Q_DEFAULT) return px_add(px2(-d2), make_float2(-at.x, -at.y));
+    const float4 a = S.axy[k >> 1];
+    float2 L = px_fma(px2(ry), make_float2(a.z, a.w), px_mul(px2(rx), make_float2(a.x, a.y)));
+    L = px_mul(L, px2(-2.0f));
+    L = px_add(L, make_float2(-at.x, -at.y));
+    if (QK == GC_Q_GOAL_PROGRESS_FULL) L = px_add(L, px2(-d2));
+    return L;
+}
+
+// The filter for a compile-time utility kind and block size B (m_keep == 12 B, e.g. the
+// 96-action grid or its 72 moving actions): every loop fully unrolled.  The max of the
+// beta-scaled logits is taken before the product -- fl(beta x) is monotone in x for
+// beta > 0 (RationalitySet requires it), so max_k fl(beta Q'_k) = fl(beta max_k Q'_k) bit for
+// bit.  Returns the pick, or -1 when the margin test fails (M is then the reference's max
+// for the exact path).  Margins as in the error budget above.
+template <int QK, int B>
+__device__ __forceinline__ int ref_fast_spec(const SmemAct &S, float rx, float ry, float d2, float beta, float u,
+                                             float &M) {
+    constexpr int NBLK = 12, MK = NBLK * B;
+    constexpr float L2E = 1.4426950408889634f;
+    float qa = -__int_as_float(0x7f800000), qb = qa;
+#pragma unroll 2
+    for (int k = 0; k < MK; k += 4) {  // two independent max chains
+        const float2 q0 = ref_q2<QK>(S, k, rx, ry, d2);
+        qa = fmaxf(qa, fmaxf(q0.x, q0.y));
+        if (k + 2 < MK) {
+            const float2 q1 = ref_q2<QK>(S, k + 2, rx, ry, d2);
+            qb = fmaxf(qb, fmaxf(q1.x, q1.y));
+        }
+    }
+    M = __fmul_rn(fmaxf(qa, qb), beta);
+    const float2 nM = px2(-M);
+    float blk[NBLK];
+    float c = 0.f;
+#pragma unroll
+    for (int j = 0; j < NBLK; ++j) {
+#pragma unroll
+        for (int i = 0; i < B; i += 2) {
+            const float2 q = ref_q2<QK>(S, j * B + i, rx, ry, d2);
+            const float2 t = px_mul(px_add(make_float2(__fmul_rn(q.x, beta), __fmul_rn(q.y, beta)), nM), px2(L2E));
+            c = __fadd_rn(c, ex2_approx(t.x));
+            c = __fadd_rn(c, ex2_approx(t.y));
+        }
+        blk[j] = c;
+    }
+    const float r = __fmul_rn(u, c);
+    int jb = 0;
+    float cc = 0.f, tpre = 0.f, tall = blk[NBLK - 1];
+#pragma unroll
+    for (int j = 0; j < NBLK - 1; ++j) {
+        tall = __fadd_rn(tall, blk[j]);
+        if (blk[j] < r) { jb = j + 1; cc = blk[j]; tpre = __fadd_rn(tpre, blk[j]); }
+    }
+    // rescan the block holding r with the same operations (the same chain values)
+    float lower = cc;
+    int i = 0;
+#pragma unroll
+    for (; i < B; i += 2) {
+        const float2 q = ref_q2<QK>(S, jb * B + i, rx, ry, d2);
+        const float2 t = px_mul(px_add(make_float2(__fmul_rn(q.x, beta), __fmul_rn(q.y, beta)), nM), px2(L2E));
+        const float w0 = ex2_approx(t.x), w1 = ex2_approx(t.y);
+        lower = cc;
+        cc = __fadd_rn(cc, w0);
+        if (!(cc < r)) break;
+        lower = cc;
+        cc = __fadd_rn(cc, w1);
+        if (!(cc < r)) { ++i; break; }
+    }
+    const int k = jb * B + i;
+    const float fB = (float)B, kin = (float)i;
+    const float tb = fB * tpre;
+    const float t_lo = fmaf(kin, lower, tb), t_hi = fmaf(kin + 1.f, cc, tb);
+    const float d_r = fmaf(u, fmaf(0x1p-23f, fB * tall, fmaf(GC_REF_FILTER_EPS_W, c, (float)MK * GC_REF_FILTER_A_W)),
+                           0x1p-23f * r);
+    const float d_lo = fmaf(0x1p-23f, t_lo, fmaf(GC_REF_FILTER_EPS_W, lower, (float)k * GC_REF_FILTER_A_W));
+    const float d_hi = fmaf(0x1p-23f, t_hi, fmaf(GC_REF_FILTER_EPS_W, cc, (float)(k + 1) * GC_REF_FILTER_A_W));
+    const float slack = 1e-9f * c;
+    if (i < B && __fsub_rn(cc, r) > fmaf(1.002f, d_hi + d_r, slack) &&
+        (k == 0 || __fsub_rn(r, lower) > fmaf(1.002f, d_lo + d_r, slack)))
+        return k < MK - 1 ? k : MK - 1;
+    return -1;
+}
+
 // The reference float32 step (prediction.py:147-162): per-action logit, max shift, numpy
 // exp, sequential cumsum, first cdf entry >= u * total.  The logits and the max are
 // computed exactly as the reference does; the exponentials are then first evaluated with
@@ -281,6 +370,18 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
     const float beta = H.hb[h];
     const int mk = H.m_keep, qk = H.q_kind;
     float M = -__int_as_float(0x7f800000);
+    if (filter && mk == 96 && qk == GC_Q_GOAL_PROGRESS) {  // the standard 96-action grid
+        const int a = ref_fast_spec<GC_Q_GOAL_PROGRESS, 8>(S, rx, ry, d2, beta, u, M);
+        if (a >= 0) return a;
+        if (fallbacks) atomicAdd(fallbacks, 1ull);
+        return ref_pick_exact(S, rx, ry, d2, beta, mk, qk, M, u);
+    }
+    if (filter && mk == 72 && qk == GC_Q_GOAL_PROGRESS_FULL) {  // its 72 moving actions (mask_stationary)
+        const int a = ref_fast_spec<GC_Q_GOAL_PROGRESS_FULL, 6>(S, rx, ry, d2, beta, u, M);
+        if (a >= 0) return a;
+        if (fallbacks) atomicAdd(fallbacks, 1ull);
+        return ref_pick_exact(S, rx, ry, d2, beta, mk, qk, M, u);
+    }
     int k = 0;
 #pragma unroll 4
     for (; k + 1 < mk; k += 2) {  // action pairs on the packed FP32x2 pipe
@@ -699,6 +800,11 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             const int j = __ldg(&T.keep[k]);
             A.ax[k] = __ldg(&T.sx[j]);
             A.ay[k] = __ldg(&T.sy[j]);
+            if (MODE == MODE_REF) {
+                float *axyf = reinterpret_cast<float *>(A.axy);
+                axyf[(k >> 1) * 4 + (k & 1)] = A.ax[k];
+                axyf[(k >> 1) * 4 + 2 + (k & 1)] = A.ay[k];
+            }
             A.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? __ldg(&T.pen[j]) : __ldg(&T.at[j]);
             A.adx[k] = __ldg(&T.dispx[j]);
             A.ady[k] = __ldg(&T.dispy[j]);
