@@ -74,7 +74,11 @@ typedef struct {
     int32_t m;
     int32_t m_keep;
     int32_t q_kind;            /* GC_Q_* */
-    int32_t _pad;
+    /* reference modes: R > 0 when the kept actions are the first R speed rows of a
+     * ControlSet.grid-shaped set (action a*24 + b = speed row a, heading -pi + b pi/12) and
+     * the heading weight is 0: K2 then guesses the max logit from the headings bracketing
+     * the goal direction (verified against the full max, so any value is safe); 0 = none */
+    int32_t ref_grid_rows;
     const float *d_sx, *d_sy;  /* float32 step_x*tau, step_y*tau (agents.py:279-280) */
     const float *d_at;         /* float32 action term incl. weights (agents.py:284-287) */
     const float *d_pen;        /* float32 q_default penalty (agents.py:256) */

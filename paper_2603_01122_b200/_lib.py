@@ -50,7 +50,7 @@ F64 = ctypes.c_double
 
 class ActionTable(ctypes.Structure):
     _fields_ = [
-        ("m", I32), ("m_keep", I32), ("q_kind", I32), ("_pad", I32),
+        ("m", I32), ("m_keep", I32), ("q_kind", I32), ("ref_grid_rows", I32),
         ("d_sx", P), ("d_sy", P), ("d_at", P), ("d_pen", P), ("d_dispx", P), ("d_dispy", P),
         ("d_keep", P),
         ("n_speeds", I32), ("n_headings", I32),

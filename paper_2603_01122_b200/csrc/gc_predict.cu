@@ -52,6 +52,7 @@ enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2, MODE_FACTS = 3 };  // FACTS: s
 
 struct KTable {
     int m, m_keep, q_kind, n_speeds, n_headings;
+    int grid_rows;  // gc_action_table.ref_grid_rows
     float dv, tau, w_v, w_th;
     const float *sx, *sy, *at, *pen, *dispx, *dispy;
     const int *keep, *a_index;
@@ -156,6 +157,7 @@ struct SmemTabs {
     double cdf[MAXH];
     float hb[MAXH], hgx[MAXH], hgy[MAXH];
     int n_hyp, m_keep, q_kind, n_speeds;
+    int ref_rows;  // MODE_REF: KTable.grid_rows of this CTA's table
     float wth;
     unsigned char phyp[4 * 256];  // hypothesis index of particle slot k*NT+tid (frees registers)
 };
@@ -280,42 +282,87 @@ __device__ __forceinline__ float2 ref_q2(const SmemAct &S, int k, float rx, floa
     return L;
 }
 
-// The filter for a compile-time utility kind and block size B (m_keep == 12 B, e.g. the
-// 96-action grid or its 72 moving actions): every loop fully unrolled.  The max of the
+// Guess of max_k Q'_k for a grid table (gc_action_table.ref_grid_rows = R): without a
+// heading weight the best action of every speed row points along one of the two headings
+// that bracket the direction to the goal, so the exact Q' of those 2R actions is evaluated
+// (reference float ops).  The bracket comes from a coarse atan2 (|error| < 0.004 rad
+// against a half heading step of 0.13 rad: the nearest heading is always in it).  Only a
+// guess -- ref_fast_spec checks it against the max of every beta-scaled logit it computes.
+template <int QK>
+__device__ __forceinline__ float ref_qmax_guess(const SmemAct &S, float rx, float ry, float d2, int rows) {
+    const float gx = -rx, gy = -ry;  // particle -> goal
+    const float ax = fabsf(gx), ay = fabsf(gy);
+    const float mn = fminf(ax, ay), mx = fmaxf(ax, ay);
+    const float a = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+    float ang = a * fmaf(0.2733f, 1.f - a, 0.78539816f);  // atan(a), a in [0, 1]
+    if (ay > ax) ang = 1.57079633f - ang;
+    if (gx < 0.f) ang = 3.14159265f - ang;
+    if (gy < 0.f) ang = -ang;
+    int b = (int)floorf((ang + 3.14159265f) * (12.f / 3.14159265f));  // heading b: -pi + b pi/12
+    b = b < 0 ? 0 : (b > 23 ? 23 : b);
+    const int b2 = b == 23 ? 0 : b + 1;
+    float q = -__int_as_float(0x7f800000);
+#pragma unroll 1
+    for (int r = 0; r < rows; ++r) {
+        const int k0 = r * 24 + b, k1 = r * 24 + b2;
+        float L0 = __fmul_rn(__fmaf_rn(ry, S.ay[k0], __fmul_rn(rx, S.ax[k0])), -2.0f);
+        float L1 = __fmul_rn(__fmaf_rn(ry, S.ay[k1], __fmul_rn(rx, S.ax[k1])), -2.0f);
+        L0 = __fsub_rn(L0, S.aat[k0]);
+        L1 = __fsub_rn(L1, S.aat[k1]);
+        if (QK == GC_Q_GOAL_PROGRESS_FULL) { L0 = __fsub_rn(L0, d2); L1 = __fsub_rn(L1, d2); }
+        q = fmaxf(q, fmaxf(L0, L1));
+    }
+    return q;
+}
+
+// The filter for a compile-time utility kind and block size B (m_keep == 12 B: the
+// 96-action grid or the 48 slow actions mask_stationary keeps): every loop fully unrolled.  The max of the
 // beta-scaled logits is taken before the product -- fl(beta x) is monotone in x for
 // beta > 0 (RationalitySet requires it), so max_k fl(beta Q'_k) = fl(beta max_k Q'_k) bit for
 // bit.  Returns the pick, or -1 when the margin test fails (M is then the reference's max
 // for the exact path).  Margins as in the error budget above.
 template <int QK, int B>
 __device__ __forceinline__ int ref_fast_spec(const SmemAct &S, float rx, float ry, float d2, float beta, float u,
-                                             float &M) {
+                                             int rows, float &M) {
     constexpr int NBLK = 12, MK = NBLK * B;
     constexpr float L2E = 1.4426950408889634f;
-    float qa = -__int_as_float(0x7f800000), qb = qa;
+    float qmax;
+    if (rows > 0) {
+        qmax = ref_qmax_guess<QK>(S, rx, ry, d2, rows);  // checked below
+    } else {
+        float qa = -__int_as_float(0x7f800000), qb = qa;
 #pragma unroll 2
-    for (int k = 0; k < MK; k += 4) {  // two independent max chains
-        const float2 q0 = ref_q2<QK>(S, k, rx, ry, d2);
-        qa = fmaxf(qa, fmaxf(q0.x, q0.y));
-        if (k + 2 < MK) {
-            const float2 q1 = ref_q2<QK>(S, k + 2, rx, ry, d2);
-            qb = fmaxf(qb, fmaxf(q1.x, q1.y));
+        for (int k = 0; k < MK; k += 4) {  // two independent max chains
+            const float2 q0 = ref_q2<QK>(S, k, rx, ry, d2);
+            qa = fmaxf(qa, fmaxf(q0.x, q0.y));
+            if (k + 2 < MK) {
+                const float2 q1 = ref_q2<QK>(S, k + 2, rx, ry, d2);
+                qb = fmaxf(qb, fmaxf(q1.x, q1.y));
+            }
         }
+        qmax = fmaxf(qa, qb);
     }
-    M = __fmul_rn(fmaxf(qa, qb), beta);
+    M = __fmul_rn(qmax, beta);
     const float2 nM = px2(-M);
     float blk[NBLK];
     float c = 0.f;
+    float lm = -__int_as_float(0x7f800000);  // max of the beta-scaled logits (the guess check)
 #pragma unroll
     for (int j = 0; j < NBLK; ++j) {
 #pragma unroll
         for (int i = 0; i < B; i += 2) {
             const float2 q = ref_q2<QK>(S, j * B + i, rx, ry, d2);
-            const float2 t = px_mul(px_add(make_float2(__fmul_rn(q.x, beta), __fmul_rn(q.y, beta)), nM), px2(L2E));
+            const float2 L = make_float2(__fmul_rn(q.x, beta), __fmul_rn(q.y, beta));
+            lm = fmaxf(lm, fmaxf(L.x, L.y));
+            const float2 t = px_mul(px_add(L, nM), px2(L2E));
             c = __fadd_rn(c, ex2_approx(t.x));
             c = __fadd_rn(c, ex2_approx(t.y));
         }
         blk[j] = c;
     }
+    // the guessed max must be the reference's max (numpy's logits.max), or every x_k
+    // differs from the reference's: the exact path then runs with the true max
+    if (lm != M) { M = lm; return -1; }
     const float r = __fmul_rn(u, c);
     int jb = 0;
     float cc = 0.f, tpre = 0.f, tall = blk[NBLK - 1];
@@ -371,13 +418,13 @@ __device__ __forceinline__ int ref_pick(const SmemTabs &H, const SmemAct &S, flo
     const int mk = H.m_keep, qk = H.q_kind;
     float M = -__int_as_float(0x7f800000);
     if (filter && mk == 96 && qk == GC_Q_GOAL_PROGRESS) {  // the standard 96-action grid
-        const int a = ref_fast_spec<GC_Q_GOAL_PROGRESS, 8>(S, rx, ry, d2, beta, u, M);
+        const int a = ref_fast_spec<GC_Q_GOAL_PROGRESS, 8>(S, rx, ry, d2, beta, u, H.ref_rows, M);
         if (a >= 0) return a;
         if (fallbacks) atomicAdd(fallbacks, 1ull);
         return ref_pick_exact(S, rx, ry, d2, beta, mk, qk, M, u);
     }
-    if (filter && mk == 72 && qk == GC_Q_GOAL_PROGRESS_FULL) {  // its 72 moving actions (mask_stationary)
-        const int a = ref_fast_spec<GC_Q_GOAL_PROGRESS_FULL, 6>(S, rx, ry, d2, beta, u, M);
+    if (filter && mk == 48 && qk == GC_Q_GOAL_PROGRESS_FULL) {  // its 48 slow actions (mask_stationary)
+        const int a = ref_fast_spec<GC_Q_GOAL_PROGRESS_FULL, 4>(S, rx, ry, d2, beta, u, H.ref_rows, M);
         if (a >= 0) return a;
         if (fallbacks) atomicAdd(fallbacks, 1ull);
         return ref_pick_exact(S, rx, ry, d2, beta, mk, qk, M, u);
@@ -789,6 +836,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
     // ---- stage tables in shared memory ----
     if (tid == 0) {
         S.n_hyp = nh; S.m_keep = T.m_keep; S.q_kind = T.q_kind; S.n_speeds = T.n_speeds;
+        S.ref_rows = T.grid_rows;
         S.wth = T.w_th * 1.4426950408889634f;
     }
     SmemAct &A = *reinterpret_cast<SmemAct *>(smem_dyn + P.act_off);
@@ -1271,6 +1319,7 @@ __global__ void k_sample_hyp(const double *cdf, int n_hyp, int n, uint64_t k0, u
 static KTable to_ktable(const gc_action_table &a) {
     KTable t;
     t.m = a.m; t.m_keep = a.m_keep; t.q_kind = a.q_kind; t.n_speeds = a.n_speeds;
+    t.grid_rows = a.ref_grid_rows;
     t.n_headings = a.n_headings; t.dv = a.dv; t.tau = a.tau; t.w_v = a.w_v; t.w_th = a.w_th;
     t.sx = a.d_sx; t.sy = a.d_sy; t.at = a.d_at; t.pen = a.d_pen; t.dispx = a.d_dispx;
     t.dispy = a.d_dispy; t.keep = a.d_keep; t.a_index = a.d_a_index;

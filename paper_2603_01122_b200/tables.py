@@ -189,6 +189,13 @@ class ActionTables:
             t.h_sin_h = self.h_sin.ctypes.data
             t.h_theta_h = self.h_theta.ctypes.data
             self.headings = heads
+            # reference-mode max-logit guess (gc_action_table.ref_grid_rows): the standard
+            # 24 headings, action a*24 + b, no heading weight
+            std = -np.pi + np.arange(24) * (np.pi / 12)
+            if (len(heads) == 24 and np.allclose(heads, std, rtol=0, atol=1e-9) and lq.w_th == 0.0
+                    and np.array_equal(a_index, np.arange(na * 24, dtype=np.int32).reshape(na, 24))
+                    and np.array_equal(keep, np.arange(na * 24))):
+                t.ref_grid_rows = na
         self.struct = t
 
 
