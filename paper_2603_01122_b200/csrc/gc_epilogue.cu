@@ -133,6 +133,118 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
     }
 }
 
+// K3 for a compile-time smoothing radius 1..3 (the bench's sigma = 1 cell is RAD = 3):
+// warp w owns rows, lane = column, so the count loads of a row are coalesced and need no
+// index division; each thread issues all of its count loads before using any (the
+// round-1 loop waited on each load in turn: 40 % long-scoreboard stalls), the vertical
+// pass keeps a sliding column of 4 + 2 RAD inputs in registers (4 outputs per column from
+// 4 + 2 RAD shared loads instead of 4 (2 RAD + 1)), the kernel taps live in registers, zero
+// outputs are not written (the outputs are zero-filled), and the union-tile flags are
+// OR-reduced per CTA (at most 4 union tiles per output tile) instead of one byte store per
+// nonzero cell.  Same arithmetic as k_epilogue: identical results.
+template <int RAD>
+__global__ void __launch_bounds__(ENT) k_epilogue_r(const EParams P) {
+    constexpr int E = ET + 2 * RAD;          // input tile edge
+    constexpr int NW = ENT / 32;             // warps
+    constexpr int LR = (E + NW - 1) / NW;    // input rows per warp
+    constexpr int RPW = ET / NW;             // output rows per warp
+    __shared__ double vin[E][E];
+    __shared__ double vmid[ET][E];
+    __shared__ unsigned utmask;
+    const int h = blockIdx.y;
+    const int4 tl = P.tiles[blockIdx.x];
+    const int t = tl.x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int cx, cy;
+    cell_of_start(__ldg(&P.start_xy[2 * h]), __ldg(&P.start_xy[2 * h + 1]), P, cx, cy);
+    const int R = __ldg(&P.step_r[t]);
+    const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
+    const int y0 = max(0, cy - R), y1 = min(P.grid_h - 1, cy + R);
+    const int ww = x1 - x0 + 1;
+    const int X0 = cx - R - RAD + tl.y * ET, Y0 = cy - R - RAD + tl.z * ET;
+    if (X0 > min(P.grid_w - 1, x1 + RAD) || X0 + ET - 1 < max(0, x0 - RAD) ||
+        Y0 > min(P.grid_h - 1, y1 + RAD) || Y0 + ET - 1 < max(0, y0 - RAD))
+        return;
+    const unsigned *cnt = P.counts + (long long)h * P.human_stride + __ldg(&P.step_off[t]);
+    if (threadIdx.x == 0) utmask = 0u;
+    // ---- counts: all loads in flight first ----
+    unsigned c0[LR], c1[LR];
+#pragma unroll
+    for (int i = 0; i < LR; ++i) {
+        const int r = w + NW * i, Y = Y0 - RAD + r;
+        const int Xa = X0 - RAD + lane, Xb = Xa + 32;
+        const bool rowok = r < E && Y >= y0 && Y <= y1;
+        const unsigned *row = cnt + (long long)(Y - y0) * ww - x0;
+        GC_DCHECK(!(rowok && Xa >= x0 && Xa <= x1) || __ldg(&P.step_off[t]) + (long long)(Y - y0) * ww + (Xa - x0) < P.human_stride);
+        c0[i] = (rowok && Xa >= x0 && Xa <= x1) ? __ldg(row + Xa) : 0u;
+        c1[i] = (rowok && lane < 2 * RAD && Xb >= x0 && Xb <= x1) ? __ldg(row + Xb) : 0u;
+    }
+    int any = 0;
+    const double dn = (double)P.n;
+#pragma unroll
+    for (int i = 0; i < LR; ++i) {
+        const int r = w + NW * i, Y = Y0 - RAD + r;
+        if (r < E) {
+            const int Xa = X0 - RAD + lane;
+            double va = 0.0, vb = 0.0;
+            if (c0[i]) { va = (double)c0[i] / dn * __ldg(&P.zy[Y]) * __ldg(&P.zx[Xa]); any = 1; }
+            if (c1[i]) { vb = (double)c1[i] / dn * __ldg(&P.zy[Y]) * __ldg(&P.zx[Xa + 32]); any = 1; }
+            vin[r][lane] = va;
+            if (lane < 2 * RAD) vin[r][lane + 32] = vb;
+        }
+    }
+    if (!__syncthreads_or(any)) return;
+    double kr[2 * RAD + 1];
+#pragma unroll
+    for (int o = 0; o < 2 * RAD + 1; ++o) kr[o] = __ldg(&P.kernel[o]);
+    // ---- pass along y: vmid[yy][c] = sum_o k[o] vin[yy + RAD - o][c], rows RPW w .. ----
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        const int c = lane + 32 * half;
+        if (half == 1 && lane >= 2 * RAD) break;
+        double a[RPW + 2 * RAD];
+#pragma unroll
+        for (int j = 0; j < RPW + 2 * RAD; ++j) a[j] = vin[RPW * w + j][c];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int o = -RAD; o <= RAD; ++o) s = fma(kr[o + RAD], a[i + RAD - o], s);
+            vmid[RPW * w + i][c] = s;
+        }
+    }
+    __syncthreads();
+    // ---- pass along x, clamp, outputs ----
+    const int X = X0 + lane;
+    const bool colok = X >= 0 && X < P.grid_w;
+    unsigned um = 0u;
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+        const int yy = RPW * w + i, Y = Y0 + yy;
+        double s = 0.0;
+#pragma unroll
+        for (int o = -RAD; o <= RAD; ++o) s = fma(kr[o + RAD], vmid[yy][lane + RAD - o], s);
+        const double v = s > 0.0 ? s : 0.0;  // np.maximum(out, 0) (occupancy.py:153)
+        if (!colok || Y < 0 || Y >= P.grid_h || !(v > 0.0)) continue;
+        const long long cell = (long long)Y * P.grid_w + X;
+        if (P.layers64) P.layers64[((long long)h * P.steps + t) * P.grid_h * P.grid_w + cell] = v;
+        const long long o = (long long)t * P.grid_h * P.grid_w + cell;
+        if (P.union32) atomicMax(reinterpret_cast<unsigned *>(P.union32) + o, __float_as_uint((float)v));
+        if (P.union64)
+            atomicMax(reinterpret_cast<unsigned long long *>(P.union64) + o, (unsigned long long)__double_as_longlong(v));
+        um |= 1u << (2 * ((Y >> 5) - (Y0 >> 5)) + ((X >> 5) - (X0 >> 5)));
+    }
+    if (P.utile) {
+        um = __reduce_or_sync(0xffffffffu, um);
+        if (lane == 0 && um) atomicOr(&utmask, um);
+        __syncthreads();
+        if (threadIdx.x < 4 && (utmask >> threadIdx.x) & 1u) {
+            const int uy = (Y0 >> 5) + (threadIdx.x >> 1), ux = (X0 >> 5) + (threadIdx.x & 1);
+            P.utile[((long long)t * ((P.grid_h + ET - 1) / ET) + uy) * P.utx + ux] = 1;
+        }
+    }
+}
+
 // conservative time union: layer t <- max over t' <= t (np.maximum.accumulate, axis 0)
 template <typename Tv>
 __global__ void k_time_union(Tv *u, int t0, int t1, long long cells) {
@@ -255,9 +367,9 @@ extern "C" gc_status gc_grid_epilogue(const gc_epilogue_args *a, void *stream) {
     dim3 grid(te - tb, a->n_humans);
     switch (a->radius) {
         case 0: k_epilogue<0><<<grid, ENT, smem, st>>>(P); break;
-        case 1: k_epilogue<1><<<grid, ENT, smem, st>>>(P); break;
-        case 2: k_epilogue<2><<<grid, ENT, smem, st>>>(P); break;
-        case 3: k_epilogue<3><<<grid, ENT, smem, st>>>(P); break;
+        case 1: k_epilogue_r<1><<<grid, ENT, 0, st>>>(P); break;
+        case 2: k_epilogue_r<2><<<grid, ENT, 0, st>>>(P); break;
+        case 3: k_epilogue_r<3><<<grid, ENT, 0, st>>>(P); break;
         default: k_epilogue<-1><<<grid, ENT, smem, st>>>(P); break;
     }
     count_launch();
