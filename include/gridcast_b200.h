@@ -42,10 +42,12 @@ typedef enum {
  *   HYPOTHESES       a human with d_hyp_off[h+1] - d_hyp_off[h] outside 1..GC_MAX_HYPOTHESES
  *                    (its CTAs return without counting anything);
  *   WINDOW_CAPACITY  max_win_cells under-reports the windows of the launch's steps (the
- *                    shared-memory window would not fit; the launch counts nothing). */
+ *                    shared-memory window would not fit; the launch counts nothing);
+ *   TABLE_ID         a human's d_table_id outside 0..n_tables-1 (its CTAs return). */
 #define GC_ERRBIT_WINDOW_OVERFLOW (1u << 6)
 #define GC_ERRBIT_HYPOTHESES (1u << 8)
 #define GC_ERRBIT_WINDOW_CAPACITY (1u << 9)
+#define GC_ERRBIT_TABLE_ID (1u << 10)
 
 /* Size limits of the kernels (shared-memory tables): hypotheses per human (|B| x |G|)
  * and actions per control set.  gc_belief_update marks a human outside 1..GC_MAX_HYPOTHESES

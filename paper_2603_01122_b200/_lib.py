@@ -26,6 +26,7 @@ GC_WINDOW_OVERFLOW = 6
 GC_ERRBIT_WINDOW_OVERFLOW = 1 << 6
 GC_ERRBIT_HYPOTHESES = 1 << 8
 GC_ERRBIT_WINDOW_CAPACITY = 1 << 9
+GC_ERRBIT_TABLE_ID = 1 << 10
 GC_MAX_HYPOTHESES = 128
 
 GC_Q_GOAL_PROGRESS = 0
@@ -227,6 +228,8 @@ def check_error_word(word: int, what: str = "gc_predict"):
         raise ValueError(f"{what}: every human needs 1..{GC_MAX_HYPOTHESES} hypotheses")
     if word & GC_ERRBIT_WINDOW_CAPACITY:
         raise ValueError(f"{what}: max_win_cells is smaller than the launch's reachable-cell windows")
+    if word & GC_ERRBIT_TABLE_ID:
+        raise ValueError(f"{what}: a human's action-table id is outside the launch's tables")
     if word & GC_ERRBIT_WINDOW_OVERFLOW:
         raise RuntimeError(f"{what}: a particle left its reachable-cell window (internal error)")
     raise RuntimeError(f"{what}: device status word {word:#x}")

@@ -12,6 +12,7 @@
 // The reference rescales each smoothed layer by before/after sums; the banded operator
 // conserves mass exactly in real arithmetic, so that rescale only corrects rounding
 // (<= 1e-16 relative) and is omitted: parity tests bound the difference at 1e-15 abs.
+#include <cstdlib>
 #include "gc_common.cuh"
 #include "gc_internal.h"
 
@@ -426,9 +427,15 @@ extern "C" gc_status gc_publish_tiles(const gc_publish_args *a, void *stream) {
     const int t0 = a->t_end > 0 ? a->t_begin : 0, t1 = a->t_end > 0 ? a->t_end : a->steps;
     GC_CHECK_ARG(t0 >= 0 && t0 < t1 && t1 <= a->steps, "gc_publish_tiles: bad layer range");
     cudaStream_t st = (cudaStream_t)stream;
-    // PCIe-bound: a few CTAs reach the link's write bandwidth (zero-copy stores)
+    // PCIe-bound: a few CTAs reach the link's write bandwidth (zero-copy stores), and every
+    // CTA of this kernel holds an SM slot the concurrently running K2 cannot use
+    static const int max_ctas = [] {
+        const char *e = getenv("GC_PUBLISH_CTAS");  // tuning knob
+        const int v = e ? atoi(e) : 32;  // 32: 5.066 ms e2e graph vs 5.086 at 148 (cfg3, f64)
+        return v < 1 ? 1 : v;
+    }();
     const long long work = (long long)(t1 - t0) * ((a->grid_w + ET - 1) / ET) * ((a->grid_h + ET - 1) / ET);
-    const int blocks = (int)(work < 148 * 8 ? (work + 7) / 8 : 148);
+    const int blocks = (int)(work < (long long)max_ctas * 8 ? (work + 7) / 8 : max_ctas);
     if (a->dtype_bytes == 8)
         k_publish<double><<<blocks, 256, 0, st>>>((const double *)a->d_union, (double *)a->h_dst, a->d_tile_flags,
                                                   a->d_host_flags, a->grid_w, a->grid_h, t0, t1, a->time_or);

@@ -823,6 +823,10 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
     const int h = blockIdx.x / P.ctas_per_human;
     const int blk = blockIdx.x - h * P.ctas_per_human;
     const int tsel = __ldg(&P.table_id[h]);
+    if (tsel < 0 || tsel >= P.n_tables) {  // uniform over the CTA, before any write
+        if (threadIdx.x == 0 && P.error) atomicOr(P.error, GC_ERRBIT_TABLE_ID);
+        return;
+    }
     const KTable &T = P.tab[tsel];
     const int h0 = __ldg(&P.hyp_off[h]);
     const int nh = __ldg(&P.hyp_off[h + 1]) - h0;

@@ -163,7 +163,9 @@ class CycleEngine:
         self._nb = H * 5 * 8 + H * 8 + H * 2 * 4 + H * 4
         self._nb = (self._nb + 15) // 16 * 16
         # two pinned staging buffers so the host can pack cycle k+1 while cycle k runs
-        self.h_ins = [torch.empty(self._nb, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        # zero-filled: a buffer captured or run before its first stage() holds a benign cycle
+        # (start (0, 0), table 0) instead of uninitialised pinned memory
+        self.h_ins = [torch.zeros(self._nb, dtype=torch.uint8).pin_memory() for _ in range(2)]
         self.h_in = self.h_ins[0]
         self.d_in = torch.empty(self._nb, dtype=torch.uint8, device=dev)
         o = 0
@@ -242,6 +244,8 @@ class CycleEngine:
         sets ``stationary`` only once ``last_xy`` exists).  ``run_cycle`` honours this;
         a captured graph always contains the update, so replay it only on primed cycles."""
         obs_xy = np.asarray(obs_xy, dtype=float)
+        if obs_xy.shape != (self.n_humans, 2) or not np.isfinite(obs_xy).all():
+            raise ValueError(f"stage(): observations must be a finite ({self.n_humans}, 2) array")
         if self._h2d_done[buf] is not None:
             self._h2d_done[buf].synchronize()  # the previous cycle's copy out of this buffer is done
             self._h2d_done[buf] = None
@@ -503,8 +507,12 @@ class CycleEngine:
                None if events is None else id(events))
         if key in self.graphs:
             return self.graphs[key][0]
-        s = torch.cuda.Stream()
-        cp = torch.cuda.Stream() if d2h is not None else None
+        # stream priorities are captured into the kernel nodes: the cycle's kernels run at high
+        # priority and the chunk publications at low priority, so a publication CTA only takes
+        # an SM slot no K2 CTA is waiting for (the last wave's idle slots) instead of delaying
+        # K2 CTAs -- and with them the chunk's end -- by its whole PCIe-bound duration
+        s = torch.cuda.Stream(priority=-1)
+        cp = torch.cuda.Stream(priority=0) if d2h is not None else None
         s.wait_stream(torch.cuda.current_stream())
         # warm the library once outside capture (function attributes, lazy loading)
         self.run_cycle(buf, with_h2d, with_update, stream=s, chunks=chunks, d2h=d2h, copy_stream=cp)

@@ -75,6 +75,31 @@ def test_predict_rejects_underreported_window_capacity():
         _lib.check_error_word(word)
 
 
+@pytest.mark.parametrize("bad", [1, -1, 7])
+def test_predict_rejects_table_ids_outside_the_launch(bad):
+    """A human whose table id does not name one of the launch's tables is not predicted
+    (no read past the parameter bank's tables) and the launch reports it."""
+    a, keep = _args([4, 4])
+    keep["tid"][1] = bad
+    word, total = _run(a, keep)
+    assert word & _lib.GC_ERRBIT_TABLE_ID and total == 512 * 6  # human 0 only
+    with pytest.raises(ValueError):
+        _lib.check_error_word(word)
+
+
+def test_engine_stage_rejects_non_finite_observations():
+    from paper_2603_01122_b200.engine import CycleEngine, EngineConfig
+    from paper_2603_01122_b200.scenario import make_scene
+    sc = make_scene("cfg2", cycles=2, humans=2)
+    eng = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec, EngineConfig(n=1024, steps=8, dt=sc.dt))
+    bad = np.array(sc.warmup_track[1], dtype=float)
+    bad[1, 0] = np.nan
+    with pytest.raises(ValueError):
+        eng.stage(bad)
+    with pytest.raises(ValueError):
+        eng.stage(sc.warmup_track[1][:1])
+
+
 def test_belief_update_rejects_too_many_hypotheses():
     from paper_2603_01122_b200.belief import belief_tables, launch_belief_update
     dev = torch.device("cuda")

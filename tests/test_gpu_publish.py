@@ -61,3 +61,4 @@ def test_graph_replay_with_tile_publication():
         g[b].replay()
         torch.cuda.synchronize()
         np.testing.assert_array_equal(host[b].numpy(), eng.unions[b].cpu().numpy())
+
