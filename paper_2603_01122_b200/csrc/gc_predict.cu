@@ -1011,10 +1011,11 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             if (P.hyp_out) P.hyp_out[(long long)h * P.n + p] = hi;
         }
     }
-    // pp[k]: the CTA-relative particle index of slot k (-1: padded slot)
-    int pp[K];
+    // bit k: particle slot k holds a particle (padded slots of a CTA's last block step but
+    // never count) -- one register instead of a per-step recomputation
+    unsigned vmask = 0u;
 #pragma unroll
-    for (int k = 0; k < K; ++k) pp[k] = (pbase + tid * K + k < P.n && tid * K + k < P.ppc) ? tid * K + k : -1;
+    for (int k = 0; k < K; ++k) vmask |= (pbase + tid * K + k < P.n && tid * K + k < P.ppc) ? (1u << k) : 0u;
     SSPool pool_step;
     if (MODE == MODE_REF) { pool_step = pool_pre; ss_absorb(pool_step, 1u); }  // STEP_DRAWS
 
@@ -1156,7 +1157,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + tid * K + k;
-            const bool valid = pp[k] >= 0;
+            const bool valid = (vmask >> k) & 1u;
             int local = -1;
             {
                 // production: padded lanes compute too (no divergence), they just do not count
@@ -1183,7 +1184,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
                 }
                 const unsigned lx = (unsigned)(ix - x0), ly = (unsigned)(iy - y0);
                 const bool inside = lx < (unsigned)ww && ly < (unsigned)wh;
-                overflow |= valid && !inside;
+                overflow |= !inside;  // padded slots are ordinary particles too: always inside
                 local = (valid && inside) ? (int)(ly * ww + lx) : -1;
             }
             // the thread whose add finds a window word zero owns that word's flush this
@@ -1243,7 +1244,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + tid * K + k;
-            if (pp[k] >= 0) {
+            if ((vmask >> k) & 1u) {
                 const long long g = (long long)h * P.n + p;
                 P.state_xy[g] = make_float2(px[k], py[k]);
                 P.state_hyp[g] = (unsigned char)ph[k];
@@ -1254,7 +1255,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const int p = pbase + tid * K + k;
-            if (pp[k] >= 0) {
+            if ((vmask >> k) & 1u) {
                 P.xy_out[((long long)h * P.n + p) * 2] = GRIDU ? fmaf(px[k], P.res, P.ox) : px[k];
                 P.xy_out[((long long)h * P.n + p) * 2 + 1] = GRIDU ? fmaf(py[k], P.res, P.oy) : py[k];
             }
