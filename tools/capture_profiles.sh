@@ -3,9 +3,12 @@
 # of the f-row kernels (collision field, MPPI, exact enumeration).  Then, here:
 #   python tools/write_profiles.py --tag rNN   (profiles/ + ncu_summary.json)
 set -x
+# PART=a|b splits the captures over two gpurun calls (each call brings back <= 64 MiB)
+PART=${PART:-all}
 # launch list of the bench's cycle (latency percentiles over --steps only: under ncu every
 # launch is serialised and replayed, so the default 1000 latency cycles would take an hour)
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-ref-mode --lat-cycles 0"
+if [ "$PART" != b ]; then
 $B > gpurun_out/plain_bench.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     $B > gpurun_out/ncu_launch.log 2>&1
@@ -14,6 +17,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_p
     -o gpurun_out/cycle_cfg3 python tools/profile_predict.py --steps 250 --cycles 3 > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
     -o gpurun_out/k2_cfg3 python tools/profile_predict.py --steps 250 --cycles 2 > gpurun_out/ncu_k2.log 2>&1
+fi
+[ "$PART" = a ] && exit 0
 python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/plain_ref.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
     -o gpurun_out/k2_refmode python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/ncu_ref.log 2>&1
