@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
     // ---- stage tables in shared memory ----
     if (tid == 0) {
         S.n_hyp = nh; S.m_keep = T.m_keep; S.q_kind = T.q_kind; S.n_speeds = T.n_speeds;
-        S.ref_rows = T.grid_rows;
+        S.ref_rows = max(0, min(T.grid_rows, T.m_keep / 24));  // any caller value stays in the table
         S.wth = T.w_th * 1.4426950408889634f;
     }
     SmemAct &A = *reinterpret_cast<SmemAct *>(smem_dyn + P.act_off);
