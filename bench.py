@@ -8,8 +8,10 @@ every human (K2: 262,144 particles x 250 steps, dt 0.02) + smoothing and max-uni
 the shared 400x400 grid (K3).  N GPUs: weak scaling, 8 humans per rank (one process per
 GPU; ``--gpus N`` without torchrun re-launches itself under torch.distributed.run); with
 N > 1 the per-rank unions are merged into one fused grid each cycle, by an NCCL
-max-reduce (``--fused-path nccl``) or by every rank's K3 writing rank 0's grid over
-NVLink peer memory (``--fused-path peer``).
+max-reduce of the nonzero 32 x 32 tiles only (``--fused-path nccl``: the ranks' tile flags
+OR-ed, the flagged tiles packed, reduced and scattered back; ``nccl-dense`` reduces the
+whole grid) or by every rank's K3 writing rank 0's grid over NVLink peer memory
+(``--fused-path peer``).
 
 ``value``  -- particle-steps/s of the whole job, inputs resident in HBM (CUDA graph
               replay, CUDA events, max over ranks);  ``hz`` = cycles/s, ``p99_ms``.
@@ -347,7 +349,7 @@ def run_ours(args):
     fused_path = args.fused_path if fused else None
     if rank == 0 and distributed:
         print(f"bench.py: {world} rank(s), fused grid: "
-              f"{'none' if not fused else ('NVLink peer-memory atomicMax (peer.PeerUnion)' if fused_path == 'peer' else 'NCCL max-reduce to rank 0')}",
+              f"{'none' if not fused else ('NVLink peer-memory atomicMax (peer.PeerUnion)' if fused_path == 'peer' else ('NCCL max-reduce of the whole grid to rank 0' if fused_path == 'nccl-dense' else 'NCCL max-reduce of the nonzero tiles to rank 0'))}",
               file=sys.stderr, flush=True)
 
     def make_engine(union_dtype, peer=None):
@@ -370,6 +372,12 @@ def run_ours(args):
         peer = PeerUnion((scene.steps, scene.spec.height, scene.spec.width), udt)
     eng = make_engine(args.union_dtype, peer)
 
+    def sparse_tiles(e, b):
+        """The union-tile flags the sparse NCCL reduce moves by, or None (dense reduce)."""
+        if fused_path != "nccl" or e.utile is None or e.cfg.time_union:
+            return None
+        return e.utile[b]
+
     def device_cycle(g, e, b=0):
         """One graph-replayed cycle plus the fused-grid merge (on the current stream)."""
         if peer is not None:
@@ -380,7 +388,7 @@ def run_ours(args):
         else:
             g.replay()
             if fused:
-                fused_reduce(e.unions[b], dst=0)
+                fused_reduce(e.unions[b], dst=0, tiles=sparse_tiles(e, b))
 
     def barrier():
         if distributed:
@@ -430,6 +438,7 @@ def run_ours(args):
         t_end.record(stream)
     barrier()
     ms = t_start.elapsed_time(t_end) / K
+    launches_timed = _lib.lib().gc_launch_count() - launches0  # eager launches in the timed cycles
     ms = max_over_ranks(ms)
     per_cycle = [a.elapsed_time(b) for a, b in cyc_ev]
     # latency percentiles over >= LAT_CYCLES cycles: extra untimed-for-value replays
@@ -446,8 +455,10 @@ def run_ours(args):
     p50 = max_over_ranks(float(np.percentile(per_cycle, 50)))
     # graph replays do not pass through the C ABI launch counter: 3 kernels per cycle
     # (K1 belief, K2 predict, K3 epilogue) are captured in the graph
-    gpu_launches = 3 * K
-    assert _lib.lib().gc_launch_count() == launches0  # nothing eager snuck in
+    # plus, with N > 1 and the sparse fused reduce, the eager tile gather (every rank) and
+    # scatter (rank 0) of gc_union_tiles around the NCCL reduce -- nothing else runs eagerly
+    gpu_launches = 3 * K + launches_timed
+    assert launches_timed <= (2 * K if fused and fused_path == "nccl" else 0), launches_timed
 
     psteps_rank = hpg * scene.n * scene.steps
     psteps = psteps_rank * world
@@ -522,9 +533,10 @@ def run_ours(args):
                         staged_ok[b].record(stream)
                         if e.peer is not None:
                             e.peer.barrier()      # every rank's K3 writes precede rank 0's read
-                        else:
-                            fused_reduce(e.unions[b], dst=0)
-                        if e.utile is not None:   # the fused grid's nonzero tiles: OR of the ranks'
+                        else:  # (the sparse reduce also OR-s the ranks' tile flags)
+                            fused_reduce(e.unions[b], dst=0, tiles=sparse_tiles(e, b))
+                        if e.utile is not None and (e.peer is not None or sparse_tiles(e, b) is None):
+                            # the fused grid's nonzero tiles: OR of the ranks'
                             dist.reduce(e.utile[b], dst=0, op=dist.ReduceOp.MAX)
                         done[b].record(stream)
                     with torch.cuda.stream(copy):
@@ -700,8 +712,9 @@ def main():
     ap.add_argument("--no-fused", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="take the multi-GPU path (NCCL group, fused reduce) even with one rank")
-    ap.add_argument("--fused-path", default="nccl", choices=["nccl", "peer"],
-                    help="N > 1 fused grid: NCCL max-reduce, or K3 writes over NVLink peer memory")
+    ap.add_argument("--fused-path", default="nccl", choices=["nccl", "nccl-dense", "peer"],
+                    help="N > 1 fused grid: NCCL max-reduce of the nonzero tiles (or of the whole grid), "
+                         "or K3 writes over NVLink peer memory")
     ap.add_argument("--no-ref-mode", action="store_true")
     ap.add_argument("--lat-cycles", type=int, default=LAT_CYCLES,
                     help="cycles the p50/p99 latencies are taken over (at least --steps)")

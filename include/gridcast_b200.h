@@ -336,6 +336,16 @@ gc_status gc_time_union(void *d_union, int32_t dtype_bytes, int32_t t_begin, int
                         void *stream);
 gc_status gc_grid_epilogue(const gc_epilogue_args *args, void *stream);
 gc_status gc_publish_tiles(const gc_publish_args *args, void *stream);
+
+/* Sparse form of the cross-GPU max-union (the fused grid of sim.py:500-502 over ranks):
+ * gathers (unpack = 0) the listed 32 x 32 tiles of a (steps, H, W) union into d_packed
+ * (count, 32, 32) -- zeros outside the grid -- or scatters (unpack = 1) them back, in-grid
+ * cells only.  Tile id (t * ceil(H/32) + ty) * ceil(W/32) + tx, the layout of the union-tile
+ * flags; every rank packs the same ids (the OR of the ranks' flags), so an ncclReduce(max) of
+ * the packed buffers equals the dense reduce on those tiles, and every other tile is zero
+ * on every rank. */
+gc_status gc_union_tiles(void *d_union, int32_t dtype_bytes, int32_t steps, int32_t grid_w, int32_t grid_h,
+                         const int32_t *d_tile_ids, int32_t count, void *d_packed, int32_t unpack, void *stream);
 gc_status gc_belief_update(const gc_belief_args *args, void *stream);
 
 /* One propagate_step (prediction.py:165-211) of an explicit particle batch in reference

@@ -157,7 +157,7 @@ EXPORTS = (
     "gc_sample_hypotheses", "gc_derive_seed", "gc_stream_f32", "gc_last_error",
     "gc_abi_version", "gc_launch_count", "gc_emplace_counts", "gc_smooth_layers",
     "gc_collision_field", "gc_exact_predict", "gc_mppi_step", "gc_predict_naive",
-    "gc_union_layers", "gc_time_union", "gc_publish_tiles", "gc_fill_zero",
+    "gc_union_layers", "gc_time_union", "gc_publish_tiles", "gc_fill_zero", "gc_union_tiles",
     "gc_peer_alloc", "gc_peer_free", "gc_peer_export", "gc_peer_import", "gc_peer_close",
 )
 
@@ -193,6 +193,7 @@ def lib():
     L.gc_time_union.argtypes = [P, I32, I32, I32, I64, P]
     L.gc_publish_tiles.argtypes = [ctypes.POINTER(PublishArgs), P]
     L.gc_fill_zero.argtypes = [P, I64, P]
+    L.gc_union_tiles.argtypes = [P, I32, I32, I32, I32, P, I32, P, I32, P]
     L.gc_peer_alloc.argtypes = [I64, ctypes.POINTER(P)]
     L.gc_peer_free.argtypes = [P]
     L.gc_peer_export.argtypes = [P, P]
@@ -201,7 +202,7 @@ def lib():
     for fn in ("gc_predict", "gc_grid_epilogue", "gc_belief_update", "gc_propagate_step",
                "gc_sample_hypotheses", "gc_emplace_counts", "gc_smooth_layers", "gc_collision_field",
                "gc_exact_predict", "gc_mppi_step", "gc_predict_naive", "gc_union_layers",
-               "gc_time_union", "gc_publish_tiles", "gc_fill_zero", "gc_peer_alloc", "gc_peer_free", "gc_peer_export", "gc_peer_import",
+               "gc_time_union", "gc_publish_tiles", "gc_fill_zero", "gc_union_tiles", "gc_peer_alloc", "gc_peer_free", "gc_peer_export", "gc_peer_import",
                "gc_peer_close"):
         getattr(L, fn).restype = ctypes.c_int
     L.gc_derive_seed.argtypes = [U64, P, I32]

@@ -446,6 +446,53 @@ extern "C" gc_status gc_publish_tiles(const gc_publish_args *a, void *stream) {
     return cuda_check(cudaGetLastError(), "k_publish launch");
 }
 
+// ---- union tiles <-> packed buffer (the sparse cross-GPU max-reduce of the fused grid) ----
+// tile id = (t * nty + ty) * ntx + tx over the (T, H, W) union's 32 x 32 tiles (the layout of
+// the union-tile flags); packed[i] is tile ids[i] as a 32 x 32 block, zero outside the grid.
+// One warp per tile, lane = column, rows looped: coalesced rows both ways.
+namespace gc {
+template <typename Tv>
+__global__ void __launch_bounds__(256) k_union_tiles(Tv *un, Tv *packed, const int *ids, int count, int W, int H,
+                                                     int unpack) {
+    const int ntx = (W + ET - 1) / ET, nty = (H + ET - 1) / ET;
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < count; w += warps) {
+        const int id = __ldg(&ids[w]);
+        const int t = id / (ntx * nty), rem = id - t * ntx * nty;
+        const int X = (rem % ntx) * ET + lane, Y0 = (rem / ntx) * ET;
+        Tv *pk = packed + w * ET * ET + lane;
+        const long long base = (long long)t * H * W + X;
+        if (unpack) {
+            if (X < W)
+                for (int r = 0; r < ET && Y0 + r < H; ++r) un[base + (long long)(Y0 + r) * W] = pk[r * ET];
+        } else {
+            for (int r = 0; r < ET; ++r)
+                pk[r * ET] = (X < W && Y0 + r < H) ? un[base + (long long)(Y0 + r) * W] : Tv(0);
+        }
+    }
+}
+}  // namespace gc
+
+extern "C" gc_status gc_union_tiles(void *d_union, int32_t dtype_bytes, int32_t steps, int32_t grid_w, int32_t grid_h,
+                                    const int32_t *d_tile_ids, int32_t count, void *d_packed, int32_t unpack,
+                                    void *stream) {
+    GC_CHECK_ARG(d_union && d_packed && d_tile_ids && count >= 0, "gc_union_tiles: bad arguments");
+    GC_CHECK_ARG(dtype_bytes == 4 || dtype_bytes == 8, "gc_union_tiles: float32 or float64 layers");
+    GC_CHECK_ARG(steps >= 1 && grid_w >= 1 && grid_h >= 1, "gc_union_tiles: bad sizes");
+    if (count == 0) return GC_OK;
+    const int blocks = (int)(((long long)count + 7) / 8 < 148 * 8 ? ((long long)count + 7) / 8 : 148 * 8);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype_bytes == 8)
+        k_union_tiles<double><<<blocks, 256, 0, st>>>((double *)d_union, (double *)d_packed, d_tile_ids, count, grid_w,
+                                                      grid_h, unpack);
+    else
+        k_union_tiles<float><<<blocks, 256, 0, st>>>((float *)d_union, (float *)d_packed, d_tile_ids, count, grid_w,
+                                                     grid_h, unpack);
+    count_launch();
+    return cuda_check(cudaGetLastError(), "k_union_tiles launch");
+}
+
 // ---- ordered union of k stacked layer sets (occupancy.py:162-192) --------------------
 // input i = in + i * stride (elements), `cells` elements each; float64 arithmetic in the
 // reference's order: max, or miss = 1 - clip(p_0); miss *= 1 - clip(p_i); out = 1 - miss.

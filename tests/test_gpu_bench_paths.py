@@ -81,3 +81,12 @@ def test_bench_distributed_path_one_rank_peer_union():
                "--no-ref-mode", "--no-e2e-alt"])
     _check(d)
     assert d["fused_grid"] == "peer" and d["n_gpus"] == 1
+
+
+def test_bench_distributed_path_one_rank_dense_reduce():
+    d = _line([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+               "--master-addr", "127.0.0.1", "--master-port", "29545", "bench.py", "--gpus", "1", "--force-dist",
+               "--fused-path", "nccl-dense", "--steps", "5", "--warmup", "3", "--lat-cycles", "10",
+               "--no-cpu-baseline", "--no-ref-mode", "--no-e2e-alt"])
+    _check(d)
+    assert d["fused_grid"] == "nccl-dense" and d["n_gpus"] == 1

@@ -1,0 +1,84 @@
+"""GPU: gc_union_tiles, the gather / scatter of the sparse cross-GPU max-reduce of the fused
+grid (engine.sparse_max_reduce), against a torch restatement -- partial edge tiles, both
+dtypes -- and the sparse merge of two engines' unions (human shards) against one engine's
+union over all humans."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2603_01122_b200.engine import CycleEngine, EngineConfig, union_tiles  # noqa: E402
+from paper_2603_01122_b200.scenario import make_scene  # noqa: E402
+
+
+def _ref_pack(u, ids):
+    T, H, W = u.shape
+    ntx, nty = -(-W // 32), -(-H // 32)
+    out = torch.zeros((len(ids), 32, 32), dtype=u.dtype)
+    for i, tid in enumerate(ids):
+        t, rem = divmod(int(tid), ntx * nty)
+        ty, tx = divmod(rem, ntx)
+        blk = u[t, ty * 32:(ty + 1) * 32, tx * 32:(tx + 1) * 32]
+        out[i, :blk.shape[0], :blk.shape[1]] = blk
+    return out
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_union_tiles_gather_scatter(dtype):
+    g = torch.Generator().manual_seed(5)
+    T, H, W = 7, 100, 70  # 4 x 3 tiles per layer, partial edge tiles
+    u = torch.rand((T, H, W), generator=g, dtype=torch.float64).to(dtype)
+    u[u < 0.5] = 0
+    ntiles = T * 4 * 3
+    ids = torch.randperm(ntiles, generator=g)[:30].sort().values.to(torch.int32)
+    du = u.cuda()
+    packed = torch.full((len(ids), 32, 32), -1.0, dtype=dtype, device="cuda")
+    union_tiles(du, ids.cuda(), packed, unpack=False)
+    torch.testing.assert_close(packed.cpu(), _ref_pack(u, ids), rtol=0, atol=0)
+    # scatter: every listed tile's in-grid cells overwritten, everything else untouched
+    dst = torch.full_like(du, 3.0)
+    union_tiles(dst, ids.cuda(), packed, unpack=True)
+    want = torch.full_like(u, 3.0)
+    ntx, nty = 3, 4
+    for tid in ids.tolist():
+        t, rem = divmod(tid, ntx * nty)
+        ty, tx = divmod(rem, ntx)
+        want[t, ty * 32:(ty + 1) * 32, tx * 32:(tx + 1) * 32] = u[t, ty * 32:(ty + 1) * 32, tx * 32:(tx + 1) * 32]
+    torch.testing.assert_close(dst.cpu(), want, rtol=0, atol=0)
+
+
+def test_sparse_merge_of_human_shards_equals_one_engine():
+    """Two engines with disjoint humans (the multi-GPU human sharding, global human ids in
+    the streams) merged by OR-ing their union-tile flags, packing the flagged tiles, taking
+    the max and scattering back -- what sparse_max_reduce does over NCCL -- equal one
+    engine's fused union over all humans, bit for bit."""
+    sc = make_scene("cfg2", cycles=4, humans=4)
+    cfg = EngineConfig(n=8192, steps=24, dt=sc.dt, union_dtype="float64")
+    track = np.concatenate([sc.warmup_track[1:], sc.track])
+
+    def run(ids):
+        eng = CycleEngine(sc.control_set, sc.q, [sc.spaces[i] for i in ids], sc.spec, cfg, human_ids=ids)
+        eng.prime(sc.warmup_track[0][ids])
+        for k in range(3):
+            eng.stage(track[k][ids], buf=0)
+            eng.run_cycle(buf=0)
+        torch.cuda.synchronize()
+        eng.check_errors()
+        return eng
+
+    full = run([0, 1, 2, 3])
+    a, b = run([0, 2]), run([1, 3])
+    flags = torch.maximum(a.utile[0], b.utile[0])
+    ids = torch.nonzero(flags.reshape(-1)).reshape(-1).to(torch.int32)
+    pa = torch.empty((len(ids), 32, 32), dtype=torch.float64, device="cuda")
+    pb = torch.empty_like(pa)
+    union_tiles(a.unions[0], ids, pa, unpack=False)
+    union_tiles(b.unions[0], ids, pb, unpack=False)
+    merged = a.unions[0].clone()
+    union_tiles(merged, ids, torch.maximum(pa, pb), unpack=True)
+    torch.cuda.synchronize()
+    assert torch.equal(merged, full.unions[0])
+    assert torch.equal(flags, full.utile[0])
+    assert 0 < len(ids) < flags.numel()

@@ -149,3 +149,69 @@ def test_independent_union_partials_multiply_across_ranks(tmp_path):
     layers = r.uniform(0.0, 0.3, size=(5, T, 12, 12))
     ref = OP.union_independent(list(layers))
     np.testing.assert_allclose(1.0 - np.load(path), ref, rtol=0, atol=1e-15)
+
+
+def _torch_tile_op(union, ids, packed, unpack):
+    """CPU restatement of gc_union_tiles (test infrastructure): tile id
+    (t * nty + ty) * ntx + tx, 32 x 32 blocks, zeros outside the grid."""
+    T, H, W = union.shape
+    ntx, nty = -(-W // 32), -(-H // 32)
+    for i, tid in enumerate(ids.tolist()):
+        t, rem = divmod(tid, ntx * nty)
+        ty, tx = divmod(rem, ntx)
+        y0, x0 = ty * 32, tx * 32
+        h, w = min(32, H - y0), min(32, W - x0)
+        if unpack:
+            union[t, y0:y0 + h, x0:x0 + w] = packed[i, :h, :w]
+        else:
+            packed[i].zero_()
+            packed[i, :h, :w] = union[t, y0:y0 + h, x0:x0 + w]
+
+
+def _tile_flags(u):
+    T, H, W = u.shape
+    ntx, nty = -(-W // 32), -(-H // 32)
+    f = torch.zeros((T, nty, ntx), dtype=torch.uint8)
+    for ty in range(nty):
+        for tx in range(ntx):
+            f[:, ty, tx] = (u[:, ty * 32:(ty + 1) * 32, tx * 32:(tx + 1) * 32] > 0).flatten(1).any(1).to(torch.uint8)
+    return f
+
+
+def _sparse_worker(rank, world, port, shards, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_01122_b200.engine import sparse_max_reduce
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, DT, model.QSpec())
+    hs = humans()
+    local = np.zeros((T, GRID.height, GRID.width))
+    for i in shards[rank]:
+        np.maximum(local, layers_of(i, hs[i], tb), out=local)
+    u = torch.from_numpy(local)
+    flags = _tile_flags(u)
+    own = flags.clone()
+    sparse_max_reduce(u, flags, dst=0, tile_op=_torch_tile_op)
+    # the flags are OR-ed over the ranks: they cover this rank's own tiles
+    assert bool((flags >= own).all())
+    if rank == 0:
+        np.save(result_path, u.numpy())
+        np.save(result_path + ".flags.npy", flags.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shards", [([0, 1, 2], [3, 4]), ([4], [0, 1, 2, 3])])
+def test_sparse_tile_reduce_equals_single_process_union(tmp_path, shards):
+    """engine.sparse_max_reduce (OR of the tile flags, pack the flagged tiles, max-reduce the
+    packed buffers, scatter back) gives rank 0 the same fused grid as the dense reduce --
+    the single-process union over all humans -- with a 60 x 60 grid whose edge tiles are
+    partial (28 cells)."""
+    path = str(tmp_path / "fused_sparse.npy")
+    mp.spawn(_sparse_worker, args=(2, _free_port(), shards, path), nprocs=2, join=True)
+    fused = np.load(path)
+    v, th = model.control_grid(4, 24, 1.4)
+    tb = model.make_tables(v, th, DT, model.QSpec())
+    ref = OP.union_max([layers_of(i, h, tb) for i, h in enumerate(humans())])
+    np.testing.assert_array_equal(fused, ref)
+    np.testing.assert_array_equal(np.load(path + ".flags.npy"), _tile_flags(torch.from_numpy(ref)).numpy())
