@@ -4,8 +4,9 @@
 
 Grid of particles n = 2^10 .. 2^24 (every 2 powers) x horizon T in {20, 100, 250, 1000}
 (dt 0.02) x grid {100^2, 400^2, 1000^2} @ 0.1 m, one human with |H| = 20 (4 goals x 5
-betas) after 10 observations, production mode.  Per point: K2 time (CUDA events on the
-launching stream, mean of 3 eager cycles), full cycle time (CUDA graph replay, mean of 5),
+betas) after 10 observations, production mode.  Per point: K2 time (event-record nodes
+inside the replayed cycle graph: the last of 5 back-to-back replays, mean of 3 such runs), full
+cycle time (the same back-to-back CUDA graph replays, mean of the last 5),
 particle-steps/s, and the issue-rate roofline fraction of the whole cycle (K1+K2+K3 time)
 using the lane-instructions per particle-step of the cfg3 ncu capture
 (profiles/ncu_summary.json; an approximation away from cfg3, where the histogram share
@@ -38,21 +39,24 @@ def point(n, T, cells, humans):
         eng.stage(sc.warmup_track[k], buf=0)
         eng.run_cycle(buf=0)
     s = torch.cuda.Stream()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(3)]
-    for e in ev:
-        eng.run_cycle(buf=0, with_h2d=False, stream=s, events=e)
-    s.synchronize()
-    k2 = sum(e[0].elapsed_time(e[1]) for e in ev) / len(ev)
-    g = eng.capture(buf=0, with_h2d=False)
+    # K2 timed by event-record nodes inside the replayed cycle graph (the clock of the cycle
+    # time itself, as bench.py does): eager events would include host launch gaps
+    kev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
+    g = eng.capture(buf=0, with_h2d=False, events=kev)
     reps = 5
+    k2s = []
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(s):
         g.replay()
-        a.record(s)
-        for _ in range(reps):
-            g.replay()
-        b.record(s)
-    s.synchronize()
+        s.synchronize()
+        for _ in range(3):  # K2 of the last of back-to-back replays (the cycle's own regime)
+            a.record(s)
+            for _ in range(reps):
+                g.replay()
+            b.record(s)
+            s.synchronize()
+            k2s.append(kev[0].elapsed_time(kev[1]))
+    k2 = sum(k2s) / len(k2s)
     eng.check_errors()
     cyc = a.elapsed_time(b) / reps
     del eng, g
