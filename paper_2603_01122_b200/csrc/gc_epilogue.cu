@@ -452,13 +452,14 @@ extern "C" gc_status gc_publish_tiles(const gc_publish_args *a, void *stream) {
 // One warp per tile, lane = column, rows looped: coalesced rows both ways.
 namespace gc {
 template <typename Tv>
-__global__ void __launch_bounds__(256) k_union_tiles(Tv *un, Tv *packed, const int *ids, int count, int W, int H,
-                                                     int unpack) {
+__global__ void __launch_bounds__(256) k_union_tiles(Tv *un, Tv *packed, const int *ids, int count, int T, int W,
+                                                     int H, int unpack) {
     const int ntx = (W + ET - 1) / ET, nty = (H + ET - 1) / ET;
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < count; w += warps) {
         const int id = __ldg(&ids[w]);
+        if (id < 0 || id >= T * ntx * nty) continue;  // not a tile of this union: left alone
         const int t = id / (ntx * nty), rem = id - t * ntx * nty;
         const int X = (rem % ntx) * ET + lane, Y0 = (rem / ntx) * ET;
         Tv *pk = packed + w * ET * ET + lane;
@@ -484,11 +485,11 @@ extern "C" gc_status gc_union_tiles(void *d_union, int32_t dtype_bytes, int32_t 
     const int blocks = (int)(((long long)count + 7) / 8 < 148 * 8 ? ((long long)count + 7) / 8 : 148 * 8);
     cudaStream_t st = (cudaStream_t)stream;
     if (dtype_bytes == 8)
-        k_union_tiles<double><<<blocks, 256, 0, st>>>((double *)d_union, (double *)d_packed, d_tile_ids, count, grid_w,
-                                                      grid_h, unpack);
+        k_union_tiles<double><<<blocks, 256, 0, st>>>((double *)d_union, (double *)d_packed, d_tile_ids, count, steps,
+                                                      grid_w, grid_h, unpack);
     else
-        k_union_tiles<float><<<blocks, 256, 0, st>>>((float *)d_union, (float *)d_packed, d_tile_ids, count, grid_w,
-                                                     grid_h, unpack);
+        k_union_tiles<float><<<blocks, 256, 0, st>>>((float *)d_union, (float *)d_packed, d_tile_ids, count, steps,
+                                                     grid_w, grid_h, unpack);
     count_launch();
     return cuda_check(cudaGetLastError(), "k_union_tiles launch");
 }
