@@ -50,6 +50,18 @@ def main():
     eng.prime(sc.warmup_track[0])
     eng.stage(sc.warmup_track[1], buf=0)
     eng.run_cycle(buf=0, chunks=3)
+    # tile-sparse publication into a pinned host stack, and the sparse-reduce gather/scatter
+    host = torch.zeros(eng.unions[0].shape, dtype=eng.unions[0].dtype).pin_memory()
+    eng_p = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec,
+                        EngineConfig(n=2048, steps=16, dt=sc.dt, mode="production"))
+    eng_p.prime(sc.warmup_track[0])
+    eng_p.stage(sc.warmup_track[1], buf=0)
+    eng_p.run_cycle(buf=0, chunks=2, d2h=host, copy_stream=torch.cuda.Stream())
+    from paper_2603_01122_b200.engine import union_tiles
+    ids = torch.nonzero(eng_p.utile[0].reshape(-1)).reshape(-1).to(torch.int32)
+    packed = torch.empty((len(ids), 32, 32), dtype=eng_p.unions[0].dtype, device="cuda")
+    union_tiles(eng_p.unions[0], ids, packed, unpack=False)
+    union_tiles(eng_p.unions[0], ids, packed, unpack=True)
     eng_i = CycleEngine(sc.control_set, sc.q, sc.spaces, sc.spec,
                         EngineConfig(n=1024, steps=8, dt=sc.dt, mode="reference", union_mode="independent"))
     eng_i.prime(sc.warmup_track[0])
