@@ -143,8 +143,11 @@ __global__ void __launch_bounds__(ENT) k_epilogue(const EParams P) {
 // outputs are not written (the outputs are zero-filled), and the union-tile flags are
 // OR-reduced per CTA (at most 4 union tiles per output tile) instead of one byte store per
 // nonzero cell.  Same arithmetic as k_epilogue: identical results.
+#ifndef GC_K3_MIN_CTAS
+#define GC_K3_MIN_CTAS 6  // 40 registers, 6 CTAs/SM: K3 -14 % vs the unbounded 48 (5 CTAs/SM)
+#endif
 template <int RAD>
-__global__ void __launch_bounds__(ENT) k_epilogue_r(const EParams P) {
+__global__ void __launch_bounds__(ENT, GC_K3_MIN_CTAS) k_epilogue_r(const EParams P) {
     constexpr int E = ET + 2 * RAD;          // input tile edge
     constexpr int NW = ENT / 32;             // warps
     constexpr int LR = (E + NW - 1) / NW;    // input rows per warp
