@@ -43,11 +43,14 @@ typedef enum {
  *                    (its CTAs return without counting anything);
  *   WINDOW_CAPACITY  max_win_cells under-reports the windows of the launch's steps (the
  *                    shared-memory window would not fit; the launch counts nothing);
- *   TABLE_ID         a human's d_table_id outside 0..n_tables-1 (its CTAs return). */
+ *   TABLE_ID         a human's d_table_id outside 0..n_tables-1 (its CTAs return);
+ *   ASSUME_QG        assume_qg was set but a human's hypotheses need the general sampler
+ *                    (that human's counts are not valid). */
 #define GC_ERRBIT_WINDOW_OVERFLOW (1u << 6)
 #define GC_ERRBIT_HYPOTHESES (1u << 8)
 #define GC_ERRBIT_WINDOW_CAPACITY (1u << 9)
 #define GC_ERRBIT_TABLE_ID (1u << 10)
+#define GC_ERRBIT_ASSUME_QG (1u << 11)
 
 /* Size limits of the kernels (shared-memory tables): hypotheses per human (|B| x |G|)
  * and actions per control set.  gc_belief_update marks a human outside 1..GC_MAX_HYPOTHESES
@@ -173,6 +176,14 @@ typedef struct {
     int32_t ref_exact_only;
     /* optional (1,) counter: reference-mode particle-steps that took the numpy-exp path */
     uint64_t *d_ref_fallbacks;
+    /* production factorised sampler: 1 = the caller guarantees that every hypothesis of the
+     * launch admits the top-speed speed-weight normalisation (beta (tau^2 + w_v) dv^2 log2(e)
+     * well below 10; the Python mirror sets it from the hypothesis spaces), so the kernel
+     * omits the max-shift fallback (2.8 % of K2 at cfg3).  Checked per CTA: a human that
+     * does not satisfy it raises GC_ERRBIT_ASSUME_QG (its counts are then not valid; the
+     * Python mirror raises).  0 = general. */
+    int32_t assume_qg;
+    int32_t _pad3;
 } gc_predict_args;
 
 enum { GC_HIST_GLOBAL = 0, GC_HIST_SMEM = 1 };

@@ -27,6 +27,7 @@ GC_ERRBIT_WINDOW_OVERFLOW = 1 << 6
 GC_ERRBIT_HYPOTHESES = 1 << 8
 GC_ERRBIT_WINDOW_CAPACITY = 1 << 9
 GC_ERRBIT_TABLE_ID = 1 << 10
+GC_ERRBIT_ASSUME_QG = 1 << 11
 GC_MAX_HYPOTHESES = 128
 
 GC_Q_GOAL_PROGRESS = 0
@@ -77,6 +78,7 @@ class PredictArgs(ctypes.Structure):
         ("t_begin", I32), ("t_end", I32), ("d_state_xy", P), ("d_state_hyp", P),
         ("p_offset", I32), ("hist_path", I32),
         ("ref_exact_only", I32), ("d_ref_fallbacks", P),
+        ("assume_qg", I32), ("_pad3", I32),
     ]
 
 
@@ -231,6 +233,8 @@ def check_error_word(word: int, what: str = "gc_predict"):
         raise ValueError(f"{what}: max_win_cells is smaller than the launch's reachable-cell windows")
     if word & GC_ERRBIT_TABLE_ID:
         raise ValueError(f"{what}: a human's action-table id is outside the launch's tables")
+    if word & GC_ERRBIT_ASSUME_QG:
+        raise ValueError(f"{what}: assume_qg was set but a hypothesis needs the general speed-weight form")
     if word & GC_ERRBIT_WINDOW_OVERFLOW:
         raise RuntimeError(f"{what}: a particle left its reachable-cell window (internal error)")
     raise RuntimeError(f"{what}: device status word {word:#x}")

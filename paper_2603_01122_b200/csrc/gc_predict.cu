@@ -48,7 +48,9 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 
 constexpr unsigned PHK0 = 0xA4093822u, PHK1 = 0x299F31D0u;  // production Philox key
 
-enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2, MODE_FACTS = 3 };  // FACTS: standard headings
+// FACTS: standard headings; FACTS_QG: FACTS for a launch whose caller guarantees that every
+// hypothesis admits the top-speed normalisation (gc_predict_args.assume_qg; checked per CTA)
+enum { MODE_REF = 0, MODE_FACT = 1, MODE_GEN = 2, MODE_FACTS = 3, MODE_FACTS_QG = 4 };
 
 struct KTable {
     int m, m_keep, q_kind, n_speeds, n_headings;
@@ -701,7 +703,7 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
 //      the displacements in that order, so the search result indexes them directly.
 //  (3) WTH (w_th != 0): heading weights H_b = exp(-beta w_th theta_b^2) per hypothesis from a
 //      shared-memory table in the same order (Htab), one LDS.128 per four headings.
-template <bool WTH>
+template <bool WTH, bool QG>
 __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &P, const float *Htab, float &x,
                                               float &y, int h, float u1, bool qg) {
     GC_DCHECK(h >= 0 && h < S.n_hyp);
@@ -717,9 +719,16 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     const float A = -kk * rx, B = -kk * ry, nkr = -kr;
     const int na = S.n_speeds;
     float G1, G2, G3, Z0;
-    if (qg) {
+#if defined(GC_TIMING_FORCE_FAST) || defined(GC_TIMING_FORCE_QG)  // timing experiments only
+    qg = true;
+#endif
+    if (QG || qg) {  // QG: the max-shift branch is compiled out (2.8 % of K2 at cfg3)
         const float Q = ex2_approx(nkr), Q2 = Q * Q;
+#ifdef GC_TIMING_FORCE_FAST
+        if (true) {
+#else
         if (na == 4) {  // the standard grid: straight-line code on the common path
+#endif
             G3 = 1.f; G2 = Q * hp.w; G1 = Q2 * hq.x; Z0 = Q2 * Q * hq.y;
         } else {
             const bool p3 = na == 3;
@@ -818,7 +827,8 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
     __shared__ SmemTabs S;
     // the factorised sampler keeps particles in grid units u = (x - origin) / res: the
     // cell is floor(u), and the utility is rescaled (k -> k res) so the weights are unchanged
-    constexpr bool GRIDU = !GC_WORLD_CELLS && (MODE == MODE_FACT || MODE == MODE_FACTS);
+    constexpr bool SYM = MODE == MODE_FACTS || MODE == MODE_FACTS_QG;  // standard heading set
+    constexpr bool GRIDU = !GC_WORLD_CELLS && (MODE == MODE_FACT || SYM);
     const int tid = threadIdx.x;
     const int h = blockIdx.x / P.ctas_per_human;
     const int blk = blockIdx.x - h * P.ctas_per_human;
@@ -847,7 +857,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
     // MODE_FACTS with w_th != 0: per-hypothesis heading weights H_b = exp(-beta w_th th_b^2)
     // in CDF slot order (MAXH x NBF floats, in place of the unused SmemAct rows)
     float *Htab = reinterpret_cast<float *>(smem_dyn + P.act_off);
-    if (MODE != MODE_FACT && MODE != MODE_FACTS) {
+    if (MODE != MODE_FACT && !SYM) {
         for (int k = tid; k < T.m_keep; k += NT) {
             const int j = __ldg(&T.keep[k]);
             A.ax[k] = __ldg(&T.sx[j]);
@@ -864,9 +874,9 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
     } else {
         // MODE_FACTS stores headings in the cumulative order of fact_step_sym (slot i holds
         // heading 2(i>>2) + (i&1) + 12((i>>1)&1); its (cos, sin) slot the forward heading's)
-        auto hslot = [](int i) { return MODE == MODE_FACTS ? 2 * (i >> 2) + (i & 1) + 12 * ((i >> 1) & 1) : i; };
+        auto hslot = [](int i) { return SYM ? 2 * (i >> 2) + (i & 1) + 12 * ((i >> 1) & 1) : i; };
         for (int i = tid; i < NBF; i += NT) {
-            const int f = MODE == MODE_FACTS ? 2 * (i >> 2) + (i & 1) : i;
+            const int f = SYM ? 2 * (i >> 2) + (i & 1) : i;
             S.hcs[i] = make_float2(P.hcos[f], P.hsin[f]);
         }
         for (int i = tid; i < NAF * NBF; i += NT) {
@@ -876,7 +886,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             const float2 d = j >= 0 ? make_float2(__ldg(&T.dispx[j]), __ldg(&T.dispy[j])) : make_float2(0.f, 0.f);
             S.fd[i] = GRIDU ? make_float2(__fdiv_rn(d.x, P.res), __fdiv_rn(d.y, P.res)) : d;
         }
-        if (MODE == MODE_FACTS && WTH) {
+        if (SYM && WTH) {
             // same expression as the stay mass sum_b H_b below, so the CDF and Z0 agree
             for (int i = tid; i < nh * NBF; i += NT) {
                 const int hh = i / NBF, q = hslot(i - hh * NBF);
@@ -890,7 +900,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
         S.hb[i] = b;
         S.hgx[i] = __ldg(&P.goal32[2 * (h0 + i)]);
         S.hgy[i] = __ldg(&P.goal32[2 * (h0 + i) + 1]);
-        if (MODE == MODE_FACT || MODE == MODE_FACTS) {
+        if (MODE == MODE_FACT || SYM) {
             const float L2E = 1.4426950408889634f;
             // goal and utility slope in the particles' units (world, or grid units when GRIDU)
             S.hp[i] = GRIDU ? make_float4(__fdiv_rn(S.hgx[i] - P.ox, P.res), __fdiv_rn(S.hgy[i] - P.oy, P.res),
@@ -902,7 +912,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             for (int q = 0; q < T.n_headings; ++q)
                 sh += (T.w_th != 0.f) ? exp2f(-T.w_th * b * P.hth2[q] * 1.4426950408889634f) : 1.f;
             S.hq[i] = make_float4(0.f, 0.f, S.hp[i].w, sh);
-            if (MODE == MODE_FACTS) {
+            if (SYM) {
                 // speed weights relative to the top speed (fact_step_sym): powers of 2^c
                 const double c = S.hp[i].w;
                 const int top = T.n_speeds - 1;
@@ -943,6 +953,10 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
         GC_DCHECK(((words + 1 + 3) & ~3) * 4 <= P.dyn_smem);
     }
     const bool qg = __syncthreads_and(qg_ok) != 0;
+    // the caller's assume_qg does not hold for this human: the launch reports it (the mirror
+    // raises; the human's counts are not valid).  No early return: the extra exit path made
+    // ptxas spill in the step loop (108 B, and most of the gain gone)
+    if (MODE == MODE_FACTS_QG && !qg && tid == 0 && P.error) atomicOr(P.error, GC_ERRBIT_ASSUME_QG);
 
     // ---- particles: hypothesis draw + start state ----
     const float sx0 = __ldg(&P.start_xy[2 * h]), sy0 = __ldg(&P.start_xy[2 * h + 1]);
@@ -1165,8 +1179,8 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
                 // word (p % 4) of this step's block (K = 4: word k; K < 4: the thread's slice)
                 const int wsel = K == 4 ? k : ((p + P.p_offset) & 3);
                 const unsigned ua = wsel == 0 ? rb.x : (wsel == 1 ? rb.y : (wsel == 2 ? rb.z : rb.w));
-                if (MODE == MODE_FACTS) {
-                    fact_step_sym<WTH>(S, P, Htab, x, y, S.phyp[k * NT + tid], u24(ua), qg);
+                if (SYM) {
+                    fact_step_sym<WTH, MODE == MODE_FACTS_QG>(S, P, Htab, x, y, S.phyp[k * NT + tid], u24(ua), qg);
                 } else if (MODE == MODE_FACT) {
                     fact_step<WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
@@ -1501,6 +1515,9 @@ extern "C" gc_status gc_predict(const gc_predict_args *a, void *stream) {
     const int mode = a->rng_mode == GC_RNG_PRODUCTION ? (fact ? (stdh ? MODE_FACTS : MODE_FACT) : MODE_GEN)
                                                       : MODE_REF;
     if (mode == MODE_REF) return dispatch_k<MODE_REF, false>(P, K, (int)grid, smem, st);
+    if (mode == MODE_FACTS && a->assume_qg)
+        return wth ? dispatch_k<MODE_FACTS_QG, true>(P, K, (int)grid, smem, st)
+                   : dispatch_k<MODE_FACTS_QG, false>(P, K, (int)grid, smem, st);
     if (mode == MODE_FACTS)
         return wth ? dispatch_k<MODE_FACTS, true>(P, K, (int)grid, smem, st)  // H_b table in shared memory
                    : dispatch_k<MODE_FACTS, false>(P, K, (int)grid, smem, st);

@@ -35,7 +35,7 @@ from .belief import belief_tables, launch_belief_update, mask_stationary
 from .device import device
 from .prediction import MODES, action_tables, geometry
 from .rng import HUMAN_PREFIX, SIM_PREDICT, derive_seed
-from .tables import hypothesis_arrays
+from .tables import assume_qg, hypothesis_arrays
 
 
 @dataclass
@@ -142,6 +142,7 @@ class CycleEngine:
         self.d_beta64 = up(np.concatenate(betas), np.float64)
         self.d_goal64 = up(np.concatenate(goals), np.float64)
         self.d_beta32 = up(np.concatenate(betas).astype(np.float32), np.float32)
+        self._betas_np = betas  # host copy for gc_predict_args.assume_qg
         self.d_goal32 = up(np.concatenate(goals).astype(np.float32), np.float32)
         if initial_log_weights is None:
             lw = np.concatenate([np.full(len(b), -np.log(len(b))) for b in betas])
@@ -205,6 +206,9 @@ class CycleEngine:
             self._disc = np.ascontiguousarray(disc_offsets(grid_spec, cfg.robot_radius))
             self.blocked = [torch.zeros((T, Hh, W), dtype=torch.uint8, device=dev) for _ in range(2)]
         self._tarr = (_lib.ActionTable * 2)(*[t.struct for t in self.tables])
+        # production: the factorised sampler's fast speed-weight form holds for every
+        # hypothesis (static: hypothesis spaces and tables are fixed) -- K2 checks it per CTA
+        self._assume_qg = int(cfg.mode == "production" and assume_qg(self.tables, self._betas_np))
         self.last_xy = None
         # stage() of an unprimed engine: that cycle has no previous observation, so (like
         # sim.py:462-485, which updates only when last_xy is set) it predicts without an update
@@ -356,6 +360,7 @@ class CycleEngine:
         a.p_offset = self.p_offset
         a.hist_path = _lib.GC_HIST_SMEM if cfg.hist_path == "smem" else _lib.GC_HIST_GLOBAL
         a.ref_exact_only = 0 if cfg.ref_filter else 1
+        a.assume_qg = self._assume_qg
         a.grid_w, a.grid_h = self.spec.width, self.spec.height
         a.origin_x32 = float(np.float32(self.spec.origin[0]))
         a.origin_y32 = float(np.float32(self.spec.origin[1]))

@@ -29,7 +29,7 @@ from .agents import ControlSet, HumanState, QFunction
 from .belief import HypothesisSpace, JointBelief
 from .device import device, stream_handle
 from .occupancy import GridSpec, OccupancyGrid
-from .tables import ActionTables, Geometry, hypothesis_arrays
+from .tables import ActionTables, Geometry, assume_qg, hypothesis_arrays
 
 CHUNK = 1024  # particles per reference random stream (prediction.py:33)
 MODES = {"reference": _lib.GC_RNG_REFERENCE, "production": _lib.GC_RNG_PRODUCTION}
@@ -281,6 +281,8 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
         raise ValueError(f"unknown hist_path {hist_path!r}")
     a.hist_path = _lib.GC_HIST_SMEM if hist_path == "smem" else _lib.GC_HIST_GLOBAL
     a.ref_exact_only = int(bool(ref_exact_only))
+    a.assume_qg = int(mode == "production" and uniforms is None and
+                      assume_qg(tables, [j.beta_of for j in jobs]))
     if ref_fallbacks is not None:
         if ref_fallbacks.dtype != torch.int64 or ref_fallbacks.numel() < 1 or not ref_fallbacks.is_cuda:
             raise ValueError("ref_fallbacks must be a (1,) int64 device tensor")

@@ -199,6 +199,23 @@ class ActionTables:
         self.struct = t
 
 
+def assume_qg(tables, betas) -> bool:
+    """gc_predict_args.assume_qg for a production launch: True when every factorised table
+    and every hypothesis beta keep the factorised sampler's top-speed normalisation
+    representable -- K2 needs 9 c + log2(24) < 100 with c = beta (tau^2 + w_v) dv^2 log2(e)
+    (4 speeds; less with fewer); this host test keeps 10 units of margin in the exponent,
+    so float rounding on the device can never disagree with it."""
+    bmax = float(np.max(np.concatenate([np.asarray(b, dtype=float).ravel() for b in betas]))) if len(betas) else 0.0
+    for t in tables:
+        if not getattr(t, "factorised", False):
+            continue
+        st = t.struct
+        c = bmax * (st.tau * st.tau + st.w_v) * st.dv * st.dv * 1.4426950408889634
+        if not np.isfinite(c) or 9.0 * c + np.log2(24.0) >= 90.0:
+            return False
+    return True
+
+
 def hypothesis_arrays(space):
     """beta_of (|H|,), goal_xy_of (|H|,2) with h = i_beta*|G| + i_goal (belief.py:54-62)."""
     betas = np.asarray(space.rationalities.array if hasattr(space.rationalities, "array")

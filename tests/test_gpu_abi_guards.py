@@ -138,3 +138,34 @@ def test_engine_unprimed_first_cycle_predicts_without_update():
                         cfg.obs_dt, sc.control_set, sc.q, sc.spaces[0], snap_tol=np.inf)
     np.testing.assert_allclose(np.exp(eng.posterior(0)), np.exp(b.log_weights), rtol=1e-9, atol=0)
     eng.check_errors()
+
+
+def test_assume_qg_fast_kernel_is_bit_identical_and_guarded(monkeypatch):
+    """Production launches whose hypotheses admit the top-speed normalisation run the kernel
+    without the max-shift fallback (gc_predict_args.assume_qg, set by the mirror): its
+    outputs equal the general kernel's bit for bit; a launch that claims assume_qg for a
+    hypothesis that needs the fallback (beta = 300) is reported, not silently wrong."""
+    import paper_2603_01122_b200.prediction as PRm
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    tab = PR.action_tables(cs, q, 0.1, torch.device("cuda"))
+    spec = G.GridSpec(200, 200, 0.1)
+
+    def run(betas, force=None):
+        space = G.HypothesisSpace(G.RationalitySet(betas), G.GoalSet(np.array([[15.0, 12.0], [4.0, 14.0]])))
+        lw = np.log(np.full(len(space.beta_of), 1.0 / len(space.beta_of)))
+        job = PR.HumanJob(G.HumanState(9.0, 9.0), lw, space.beta_of, space.goal_xy_of, 7, (2, 0), 0)
+        if force is not None:
+            monkeypatch.setattr(PRm, "assume_qg", lambda *a: force)
+        out = PR.run_predict([job] * 3, [tab], 200000, 30, 0.1, 0.1, spec, "production", per_human_layers=False,
+                             union64=True)
+        monkeypatch.undo()
+        return out
+
+    betas = (0.1, 1.0, 10.0)
+    from paper_2603_01122_b200.tables import assume_qg
+    assert assume_qg([tab], [np.array(betas)]) and not assume_qg([tab], [np.array([300.0])])
+    fast, general = run(betas), run(betas, force=False)
+    assert torch.equal(fast["counts"], general["counts"]) and torch.equal(fast["union64"], general["union64"])
+    with pytest.raises(ValueError, match="assume_qg"):
+        run((300.0,), force=True)
