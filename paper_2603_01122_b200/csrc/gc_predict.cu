@@ -160,6 +160,7 @@ struct SmemTabs {
     float hb[MAXH], hgx[MAXH], hgy[MAXH];
     int n_hyp, m_keep, q_kind, n_speeds;
     int ref_rows;  // MODE_REF: KTable.grid_rows of this CTA's table
+    float gsmax, gatmin;  // MODE_GEN: max_k |(sx, sy)_k| and min_k at_k (or pen_k) of the kept actions
     float wth;
     unsigned char phyp[4 * 256];  // hypothesis index of particle slot k*NT+tid (frees registers)
 };
@@ -559,6 +560,95 @@ __device__ __forceinline__ int gen_pick(const SmemTabs &H, const SmemAct &S, flo
     return k < mk - 1 ? k : mk - 1;
 }
 
+// The generic sampler for a compile-time utility kind and block size (m_keep == 12 B: the
+// 96 actions of a 4 x 24 set or 48 of them), one pass: instead of a max pass it shifts the
+// logits by an analytic upper bound of their max -- by Cauchy-Schwarz, -2 rel.s_k - at_k <=
+// 2 |rel| max_k|s_k| - min_k at_k (and -d2 - pen_k <= -d2 - min_k pen_k for q_default) -- so
+// every weight is <= 1; the bound is loose by the angle to the nearest action and the action
+// term (a few log2 units for the standard sets), and a total below 2^-60 (a bound so loose
+// that the weights underflow, e.g. beta ~ 300) takes the two-pass gen_pick.  Then the
+// 12-block running sum, the block holding r and a rescan of it, fully unrolled, action pairs
+// from one LDS.128.  Same distribution as gen_pick (the shift cancels in the normalisation).
+template <int QK, int B>
+__device__ __forceinline__ int gen_fast_spec(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
+    constexpr int NBLK = 12;
+    const float rx = x - H.hgx[h], ry = y - H.hgy[h];
+    const float d2 = fmaf(rx, rx, ry * ry);
+    const float bl = H.hb[h] * 1.4426950408889634f;
+    float bound;
+    if (QK == GC_Q_DEFAULT) {
+        bound = -d2 - H.gatmin;
+    } else {
+        float rs;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(fmaxf(d2, 1e-30f)));
+        bound = fmaf(2.f * d2 * rs * 1.0001f, H.gsmax, -H.gatmin);  // 2 |rel| max|s| - min at
+        if (QK == GC_Q_GOAL_PROGRESS_FULL) bound -= d2;
+    }
+    const float2 nM = make_float2(-bl * bound, -bl * bound);
+    const float2 BL = make_float2(bl, bl);
+    auto w2 = [&](int k) {
+        const float2 at = *reinterpret_cast<const float2 *>(&S.aat[k]);
+        float2 q;
+        if (QK == GC_Q_DEFAULT) {
+            q = __fadd2_rn(make_float2(-d2, -d2), make_float2(-at.x, -at.y));
+        } else {
+            const float4 a = S.axy[k >> 1];
+            const float2 t = __ffma2_rn(make_float2(ry, ry), make_float2(a.z, a.w),
+                                        __fmul2_rn(make_float2(rx, rx), make_float2(a.x, a.y)));
+            q = __ffma2_rn(make_float2(-2.f, -2.f), t, make_float2(-at.x, -at.y));
+            if (QK == GC_Q_GOAL_PROGRESS_FULL) q = __fadd2_rn(q, make_float2(-d2, -d2));
+        }
+        const float2 e = __ffma2_rn(q, BL, nM);
+        return make_float2(ex2_approx(e.x), ex2_approx(e.y));
+    };
+    float blk[NBLK];
+    float c = 0.f;
+#pragma unroll
+    for (int j = 0; j < NBLK; ++j) {
+#pragma unroll
+        for (int i = 0; i < B; i += 2) {
+            const float2 w = w2(j * B + i);
+            c += w.x + w.y;
+        }
+        blk[j] = c;
+    }
+    if (!(c >= 0x1p-60f)) return -1;  // the bound was far too loose (or NaN): two-pass sampler
+    const float r = u * c;
+    int jb = 0;
+    float cc = 0.f;
+#pragma unroll
+    for (int j = 0; j < NBLK - 1; ++j) {
+        if (blk[j] <= r) { jb = j + 1; cc = blk[j]; }
+    }
+    int i = 0;
+#pragma unroll
+    for (; i < B; i += 2) {
+        const float2 w = w2(jb * B + i);
+        cc += w.x;
+        if (cc > r) break;
+        cc += w.y;
+        if (cc > r) { ++i; break; }
+    }
+    const int k = jb * B + i;
+    return k < NBLK * B - 1 ? k : NBLK * B - 1;
+}
+
+// production generic sampler: the unrolled one-pass form for the common action counts
+__device__ __forceinline__ int gen_sample(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
+    const int mk = H.m_keep, qk = H.q_kind;
+    int a = -1;
+    if (mk == 96) {
+        if (qk == GC_Q_GOAL_PROGRESS) a = gen_fast_spec<GC_Q_GOAL_PROGRESS, 8>(H, S, x, y, h, u);
+        else if (qk == GC_Q_GOAL_PROGRESS_FULL) a = gen_fast_spec<GC_Q_GOAL_PROGRESS_FULL, 8>(H, S, x, y, h, u);
+        else if (qk == GC_Q_DEFAULT) a = gen_fast_spec<GC_Q_DEFAULT, 8>(H, S, x, y, h, u);
+    } else if (mk == 48) {
+        if (qk == GC_Q_GOAL_PROGRESS) a = gen_fast_spec<GC_Q_GOAL_PROGRESS, 4>(H, S, x, y, h, u);
+        else if (qk == GC_Q_GOAL_PROGRESS_FULL) a = gen_fast_spec<GC_Q_GOAL_PROGRESS_FULL, 4>(H, S, x, y, h, u);
+        else if (qk == GC_Q_DEFAULT) a = gen_fast_spec<GC_Q_DEFAULT, 4>(H, S, x, y, h, u);
+    }
+    return a >= 0 ? a : gen_pick(H, S, x, y, h, u);
+}
+
 // ---- production factorised sampler (grid control set x goal-progress utility) --------
 // logit(a,b) = beta*(-2 tau a dv d_b - (tau^2 + w_v) a^2 dv^2 - w_th theta_b^2) + const,
 // d_b = rel . (cos th_b, sin th_b).  With k = 2 beta tau dv, r = |rel|:
@@ -862,7 +952,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             const int j = __ldg(&T.keep[k]);
             A.ax[k] = __ldg(&T.sx[j]);
             A.ay[k] = __ldg(&T.sy[j]);
-            if (MODE == MODE_REF) {
+            if (MODE == MODE_REF || MODE == MODE_GEN) {
                 float *axyf = reinterpret_cast<float *>(A.axy);
                 axyf[(k >> 1) * 4 + (k & 1)] = A.ax[k];
                 axyf[(k >> 1) * 4 + 2 + (k & 1)] = A.ay[k];
@@ -870,6 +960,21 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
             A.aat[k] = (T.q_kind == GC_Q_DEFAULT) ? __ldg(&T.pen[j]) : __ldg(&T.at[j]);
             A.adx[k] = __ldg(&T.dispx[j]);
             A.ady[k] = __ldg(&T.dispy[j]);
+        }
+        if (MODE == MODE_GEN) {  // the logit bound of gen_fast_spec: max |s_k|, min at_k
+            __syncthreads();
+            if (tid < 32) {
+                float sm = 0.f, am = __int_as_float(0x7f800000);
+                for (int k = tid; k < T.m_keep; k += 32) {
+                    sm = fmaxf(sm, fmaf(A.ax[k], A.ax[k], A.ay[k] * A.ay[k]));
+                    am = fminf(am, A.aat[k]);
+                }
+                for (int o = 16; o; o >>= 1) {
+                    sm = fmaxf(sm, __shfl_xor_sync(0xffffffffu, sm, o));
+                    am = fminf(am, __shfl_xor_sync(0xffffffffu, am, o));
+                }
+                if (tid == 0) { S.gsmax = sqrtf(sm) * 1.0001f; S.gatmin = am; }
+            }
         }
     } else {
         // MODE_FACTS stores headings in the cumulative order of fact_step_sym (slot i holds
@@ -1184,7 +1289,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PR
                 } else if (MODE == MODE_FACT) {
                     fact_step<WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
-                    const int a = gen_pick(S, A, x, y, S.phyp[k * NT + tid], u24(ua));
+                    const int a = gen_sample(S, A, x, y, S.phyp[k * NT + tid], u24(ua));
                     x = __fadd_rn(x, A.adx[a]);
                     y = __fadd_rn(y, A.ady[a]);
                 }

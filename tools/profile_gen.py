@@ -44,6 +44,7 @@ def main():
     r = np.random.default_rng(0)
     acts = [G.ControlAction(float(v), float(t)) for v, t in zip(r.uniform(0, 1.4, 96), r.uniform(-math.pi, math.pi, 96))]
     time_k2(G.ControlSet(acts), q, "96 random actions")
+    time_k2(G.ControlSet.grid(4, 24, 1.4), G.q_default((0.3, 0.1)), "grid(4, 24, 1.4), q_default")
 
 
 if __name__ == "__main__":
