@@ -634,7 +634,7 @@ __device__ __forceinline__ int gen_fast_spec(const SmemTabs &H, const SmemAct &S
 }
 
 // production generic sampler: the unrolled one-pass form for the common action counts
-__device__ __forceinline__ int gen_sample(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
+static __device__ __noinline__ int gen_sample(const SmemTabs &H, const SmemAct &S, float x, float y, int h, float u) {
     const int mk = H.m_keep, qk = H.q_kind;
     int a = -1;
     if (mk == 96) {
