@@ -42,6 +42,9 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 #ifndef GC_REF_MIN_CTAS
 #define GC_REF_MIN_CTAS 3  // resident CTAs per SM of the reference-arithmetic K2 (79 regs, no spills; 44.7 ms at cfg3 vs 47.8 at 2, 48.6 at 4)
 #endif
+#ifndef GC_GEN_MIN_CTAS
+#define GC_GEN_MIN_CTAS 4  // resident CTAs per SM of the production generic-sampler K2
+#endif
 #ifndef GC_WORLD_CELLS
 #define GC_WORLD_CELLS 1  // production particles in float32 world coordinates, exact cells
 #endif
@@ -912,7 +915,7 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
 // shared-memory window: u16 counters packed two per u32 word (a CTA holds < 65536
 // particles, so a per-CTA cell count cannot overflow its half-word)
 template <int MODE, int K, bool WTH, bool HSM>
-__global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : GC_PROD_MIN_CTAS) k_predict(const KParams P) {
+__global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : (MODE == MODE_GEN ? GC_GEN_MIN_CTAS : GC_PROD_MIN_CTAS)) k_predict(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ SmemTabs S;
     // the factorised sampler keeps particles in grid units u = (x - origin) / res: the
