@@ -34,8 +34,8 @@ def exact_action_probs(z, belief, cs, q, space):
 
 
 def one_step_tv(q_factory, n=1 << 22, weights=None, mask_v=None, goals=((0.5, 0.3), (0.1, 0.15)),
-                speeds=4, betas=(0.3, 2.0, 9.0), origin=(0.0, 0.0), shape=(400, 400)):
-    cs = G.ControlSet.grid(speeds, 24, 1.4)
+                speeds=4, betas=(0.3, 2.0, 9.0), origin=(0.0, 0.0), shape=(400, 400), cs=None):
+    cs = G.ControlSet.grid(speeds, 24, 1.4) if cs is None else cs
     q = q_factory()
     if mask_v is not None:
         q = G.mask_stationary(q, cs, mask_v)
@@ -101,6 +101,28 @@ def test_generic_sampler_one_step():
     tv, fact = one_step_tv(lambda: G.q_default((0.3, 2.0)))
     assert not fact
     assert tv < 0.006, tv
+
+
+def _random_actions(m, seed=0):
+    r = np.random.default_rng(seed)
+    return G.ControlSet([G.ControlAction(float(v), float(t))
+                         for v, t in zip(r.uniform(0.05, 1.4, m), r.uniform(-np.pi, np.pi, m))])
+
+
+@pytest.mark.parametrize("m,mask_v,betas", [
+    (96, None, (0.3, 2.0, 9.0)),     # one-pass generic sampler, goal-progress utility
+    (96, 0.5, (0.3, 2.0, 9.0)),      # masked (the FULL utility) over the kept actions
+    (48, None, (0.3, 2.0, 9.0)),     # the 48-action instantiation
+    (60, None, (0.3, 2.0, 9.0)),     # an action count without an instantiation: two-pass form
+    (96, None, (0.3, 2.0, 900.0)),   # a bound so loose the weights underflow: two-pass fallback
+])
+def test_generic_sampler_non_grid_sets(m, mask_v, betas):
+    """The production generic sampler (round 2: one pass with an analytic bound of the max
+    logit, compiled for 96 / 48 actions; two passes otherwise or when the bound underflows)
+    is exact in distribution on control sets that are not speed x heading grids."""
+    cs = _random_actions(m)
+    tv, fact = one_step_tv(lambda: G.q_goal_progress(0.5), cs=cs, mask_v=mask_v, betas=betas)
+    assert not fact and tv < 0.006, tv
 
 
 def test_far_goal_high_beta_no_overflow():
