@@ -91,3 +91,38 @@ def test_filter_uniforms_mode_matches_exact():
         outs.append(o)
     assert torch.equal(outs[0]["counts"], outs[1]["counts"])
     assert torch.equal(outs[0]["xy"].view(torch.int32), outs[1]["xy"].view(torch.int32))
+
+
+def test_filter_error_budget_holds_on_this_gpu(tmp_path):
+    """The filter's proof assumes |ex2.approx(fl(x log2e)) - e^x| <= 3e-7 e^x + 1e-9 for every
+    float32 x in [-104, 0]: checked exhaustively on this GPU (tools/cuda_checks/ex2_filter_err.cu)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "ex2_filter_err")
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "--fmad=false", "-I",
+                    os.path.join(root, "paper_2603_01122_b200", "csrc"),
+                    os.path.join(root, "tools", "cuda_checks", "ex2_filter_err.cu"), "-o", exe],
+                   check=True, capture_output=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "violations 0" in out.stdout, out.stdout + out.stderr
+
+
+def test_filter_numpy_exp_error_bound():
+    """... and that numpy's float32 exp (which the device exp_np reproduces bit for bit,
+    test_gpu_exp_packed.py) is within 2.2e-7 relative of e^x on every float32 in [-104, 0]
+    with a normal result (subnormal results: absolute error < 1e-44): EPS_W = 6e-7 >= 3e-7 +
+    2.2e-7 in gc_predict.cu."""
+    lo, hi = 0x80000000, 0xC2D00000
+    worst_rel, worst_abs = 0.0, 0.0
+    step = 1 << 25
+    for s in range(lo, hi + 1, step):
+        x = np.arange(s, min(s + step, hi + 1), dtype=np.uint64).astype(np.uint32).view(np.float32)
+        y = np.exp(x).astype(np.float64)
+        t = np.exp(x.astype(np.float64))
+        err = np.abs(y - t)
+        normal = t > 1.2e-38
+        worst_rel = max(worst_rel, float((err[normal] / t[normal]).max(initial=0.0)))
+        worst_abs = max(worst_abs, float(err[~normal].max(initial=0.0)))
+    assert worst_rel <= 2.2e-7, worst_rel
+    assert worst_abs < 1e-44, worst_abs
