@@ -82,3 +82,28 @@ def test_sparse_merge_of_human_shards_equals_one_engine():
     assert torch.equal(merged, full.unions[0])
     assert torch.equal(flags, full.utile[0])
     assert 0 < len(ids) < flags.numel()
+
+
+@pytest.mark.parametrize("sigma", [0.03, 0.05, 0.1, 0.13, 0.2])
+def test_epilogue_radii_match_the_standalone_smoother(sigma):
+    """K3 for every radius the dispatch distinguishes (k_epilogue_r<1..3>, the runtime-radius
+    kernel for 4 and 6): the fused epilogue's layers equal the standalone smoother
+    (gc_smooth_layers, itself pinned to the reference's smooth_values) applied to the
+    unsmoothed layers of the same predict, and the max union equals the max of the layers."""
+    import paper_2603_01122_b200 as G
+    from paper_2603_01122_b200 import prediction as PR
+    from paper_2603_01122_b200.occupancy import smooth_values
+    cs, q = G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5)
+    tab = PR.action_tables(cs, q, 0.1, torch.device("cuda"))
+    spec = G.GridSpec(90, 70, 0.1)
+    space = G.HypothesisSpace(G.RationalitySet((0.5, 3.0)), G.GoalSet(np.array([[7.0, 5.0], [1.0, 1.0]])))
+    lw = np.log(np.array([0.4, 0.1, 0.3, 0.2]))
+    jobs = [PR.HumanJob(G.HumanState(4.0 + i, 3.0), lw, space.beta_of, space.goal_xy_of, 11, (2, i), 0)
+            for i in range(2)]
+    raw = PR.run_predict(jobs, [tab], 20000, 12, 0.1, 0.0, spec, "production")["layers"].cpu().numpy()
+    out = PR.run_predict(jobs, [tab], 20000, 12, 0.1, sigma, spec, "production", union64=True)
+    lay = out["layers"].cpu().numpy()
+    for h in range(2):
+        for t in (0, 5, 11):
+            np.testing.assert_allclose(lay[h, t], smooth_values(raw[h, t], spec, sigma), rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(out["union64"].cpu().numpy(), lay.max(axis=0))
