@@ -812,16 +812,9 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     const float A = -kk * rx, B = -kk * ry, nkr = -kr;
     const int na = S.n_speeds;
     float G1, G2, G3, Z0;
-#if defined(GC_TIMING_FORCE_FAST) || defined(GC_TIMING_FORCE_QG)  // timing experiments only
-    qg = true;
-#endif
     if (QG || qg) {  // QG: the max-shift branch is compiled out (2.8 % of K2 at cfg3)
         const float Q = ex2_approx(nkr), Q2 = Q * Q;
-#ifdef GC_TIMING_FORCE_FAST
-        if (true) {
-#else
         if (na == 4) {  // the standard grid: straight-line code on the common path
-#endif
             G3 = 1.f; G2 = Q * hp.w; G1 = Q2 * hq.x; Z0 = Q2 * Q * hq.y;
         } else {
             const bool p3 = na == 3;
