@@ -21,6 +21,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 #include "gc_common.cuh"
 #include "gc_internal.h"
@@ -796,7 +797,7 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
 //      the displacements in that order, so the search result indexes them directly.
 //  (3) WTH (w_th != 0): heading weights H_b = exp(-beta w_th theta_b^2) per hypothesis from a
 //      shared-memory table in the same order (Htab), one LDS.128 per four headings.
-template <bool WTH, bool QG>
+template <bool WTH, bool QG, bool NA4>
 __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &P, const float *Htab, float &x,
                                               float &y, int h, float u1, bool qg) {
     GC_DCHECK(h >= 0 && h < S.n_hyp);
@@ -814,7 +815,7 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     float G1, G2, G3, Z0;
     if (QG || qg) {  // QG: the max-shift branch is compiled out (2.8 % of K2 at cfg3)
         const float Q = ex2_approx(nkr), Q2 = Q * Q;
-        if (na == 4) {  // the standard grid: straight-line code on the common path
+        if (NA4 || na == 4) {  // the standard grid: straight-line code on the common path
             G3 = 1.f; G2 = Q * hp.w; G1 = Q2 * hq.x; Z0 = Q2 * Q * hq.y;
         } else {
             const bool p3 = na == 3;
@@ -897,7 +898,7 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
     const float w1 = G1 * eh, w2 = G2 * e * eh;
     const float res = t - lo;
     int a = 1 + ((w1 <= res) ? 1 : 0) + ((w1 + w2 <= res) ? 1 : 0);
-    a = a < na - 1 ? a : na - 1;
+    if (!NA4) a = a < na - 1 ? a : na - 1;  // (4 speeds: a <= 3 already)
     a = (rr < Z0) ? 0 : a;  // stay: row 0 of fd is (0, 0)
     GC_DCHECK(a >= 0 && a < NAF && b >= 0 && b < NBF);
     const float2 d = S.fd[a * NBF + b];
@@ -1230,6 +1231,11 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : (MODE
             px[k] = q.x; py[k] = q.y;
         }
     } else {
+    // the production step loop, instantiated twice for the standard heading set: once for
+    // CTAs whose table has the 4 speeds of ControlSet.grid (no speed-count selects), once
+    // for the rest (2 or 3 speeds, e.g. mask_stationary's table) -- CTA-uniform choice
+    auto prod_loop = [&](auto na4_tag) {
+    constexpr bool NA4 = decltype(na4_tag)::value;
     const float yres = recip_nr(P.res);  // production cell map: the quotient's reciprocal
     U4 rbk = U4{0u, 0u, 0u, 0u};  // K < 4: the block this lane drew for its turn (see below)
     for (int t = P.t_begin; t < P.t_end; ++t) {
@@ -1281,7 +1287,7 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : (MODE
                 const int wsel = K == 4 ? k : ((p + P.p_offset) & 3);
                 const unsigned ua = wsel == 0 ? rb.x : (wsel == 1 ? rb.y : (wsel == 2 ? rb.z : rb.w));
                 if (SYM) {
-                    fact_step_sym<WTH, MODE == MODE_FACTS_QG>(S, P, Htab, x, y, S.phyp[k * NT + tid], u24(ua), qg);
+                    fact_step_sym<WTH, MODE == MODE_FACTS_QG, NA4>(S, P, Htab, x, y, S.phyp[k * NT + tid], u24(ua), qg);
                 } else if (MODE == MODE_FACT) {
                     fact_step<WTH>(S, P, x, y, S.phyp[k * NT + tid], u24(ua));
                 } else {
@@ -1352,6 +1358,13 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : (MODE
             }
             __syncthreads();
         }
+    }
+    };
+    if constexpr (SYM) {
+        if (S.n_speeds == 4) prod_loop(std::true_type{});
+        else prod_loop(std::false_type{});
+    } else {
+        prod_loop(std::false_type{});
     }
     }  // production step loop
     if (overflow && P.error) atomicOr(P.error, GC_ERRBIT_WINDOW_OVERFLOW);
