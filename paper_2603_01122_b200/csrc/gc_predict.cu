@@ -757,8 +757,9 @@ __device__ __forceinline__ void fact_step(const SmemTabs &S, const KParams &P, f
         lo = p ? cum[2] : lo;
 #pragma unroll
         for (int i = 0; i < 3; ++i) cum[i] = p ? cum[i + 3] : cum[i];
+        // the last three entries: cum is non-decreasing, so p2 implies p1 implies p0
         const bool p0 = cum[0] <= t, p1 = cum[1] <= t, p2 = cum[2] <= t;
-        b += (p0 ? 1 : 0) + (p1 ? 1 : 0) + (p2 ? 1 : 0);
+        b += p2 ? 3 : (p1 ? 2 : (p0 ? 1 : 0));
         lo = p2 ? cum[2] : (p1 ? cum[1] : (p0 ? cum[0] : lo));
     }
     b = b < NBF - 1 ? b : NBF - 1;
@@ -884,8 +885,9 @@ __device__ __forceinline__ void fact_step_sym(const SmemTabs &S, const KParams &
         lo = p ? cum[2] : lo;
 #pragma unroll
         for (int i = 0; i < 3; ++i) cum[i] = p ? cum[i + 3] : cum[i];
+        // the last three entries: cum is non-decreasing, so p2 implies p1 implies p0
         const bool p0 = cum[0] <= t, p1 = cum[1] <= t, p2 = cum[2] <= t;
-        b += (p0 ? 1 : 0) + (p1 ? 1 : 0) + (p2 ? 1 : 0);
+        b += p2 ? 3 : (p1 ? 2 : (p0 ? 1 : 0));
         lo = p2 ? cum[2] : (p1 ? cum[1] : (p0 ? cum[0] : lo));
     }
     b = b < NBF - 1 ? b : NBF - 1;  // b is the cumulative-order index i
