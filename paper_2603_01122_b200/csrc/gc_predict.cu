@@ -41,7 +41,7 @@ constexpr int NAF = 4;         // max speeds of the factorised sampler
 #define GC_PROD_MIN_CTAS 4  // resident CTAs per SM of the production K2 (64 registers)
 #endif
 #ifndef GC_REF_MIN_CTAS
-#define GC_REF_MIN_CTAS 3  // resident CTAs per SM of the reference-arithmetic K2 (79 regs, no spills; 44.7 ms at cfg3 vs 47.8 at 2, 48.6 at 4)
+#define GC_REF_MIN_CTAS 4  // resident CTAs per SM of the reference-arithmetic K2 (64 regs): after the specialised filter 9.24 ms (T = 100, cfg3) vs 9.58 at 2 and 9.67 at 3
 #endif
 #ifndef GC_GEN_MIN_CTAS
 #define GC_GEN_MIN_CTAS 4  // resident CTAs per SM of the production generic-sampler K2
