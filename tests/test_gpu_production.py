@@ -202,3 +202,36 @@ def test_production_streams_independent_of_launch_shape():
     multi = PR.run_predict([job] + others, [tab], n, T, 0.1, 0.0, spec, "production")["layers"][0].cpu().numpy()
     assert alone.sum() > 0
     np.testing.assert_array_equal(alone, multi)
+
+
+def test_mixed_tables_in_one_launch():
+    """One launch with humans on the 4-speed grid table and on mask_stationary's 2-speed
+    table (the engine's moving / stationary humans): K2 picks the step-loop instance per CTA
+    (4-speed tables without the speed-count selects, the rest general), and each human's
+    one-step occupancy matches its own exact distribution."""
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    qm = G.mask_stationary(q, cs, 0.5)
+    dev = torch.device("cuda")
+    tabs = [PR.action_tables(cs, q, 0.1, dev), PR.action_tables(cs, qm, 0.1, dev)]
+    assert tabs[0].struct.n_speeds == 4 and tabs[1].struct.n_speeds == 2
+    space = G.HypothesisSpace(G.RationalitySet((0.3, 2.0, 9.0)), G.GoalSet(np.array([[0.5, 0.3], [0.1, 0.15]])))
+    b = G.JointBelief.from_probs(np.full(space.size, 1.0 / space.size))
+    spec = G.GridSpec(400, 400, 0.001)
+    z = G.HumanState(0.2005, 0.2005)
+    jobs = [PR.HumanJob(z, b.log_weights, space.beta_of, space.goal_xy_of, 12345, (), t) for t in (1, 0, 1)]
+    n = 1 << 21
+    out = PR.run_predict(jobs, tabs, n, 1, 0.1, 0.0, spec, "production")
+    layers = out["layers"][:, 0].cpu().numpy()
+    disp = cs.displacements(0.1).astype(np.float32)
+    x = np.float32(z.x) + disp[:, 0]
+    y = np.float32(z.y) + disp[:, 1]
+    inv = np.float32(1.0) / np.float32(0.001)
+    ix = np.clip(np.floor(x * inv).astype(int), 0, 399)
+    iy = np.clip(np.floor(y * inv).astype(int), 0, 399)
+    for hi, qq in zip(range(3), (qm, q, qm)):
+        p = exact_action_probs(z, b, cs, qq, space)
+        exact = np.zeros((400, 400))
+        np.add.at(exact, (iy, ix), p)
+        tv = 0.5 * np.abs(layers[hi] - exact).sum()
+        assert tv < 0.006, (hi, tv)
