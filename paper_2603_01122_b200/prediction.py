@@ -197,6 +197,27 @@ class HumanJob:
     table: int = 0
 
 
+_TORCH_DT = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+             np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.int32, np.dtype(np.uint64): torch.int64}
+
+
+def _upload_packed(dev, arrays):
+    """Copy several small host arrays to the device in one transfer; returns device views
+    (16-byte aligned, same shapes; unsigned types are viewed as their signed twins, which
+    the C ABI reads as the unsigned bits)."""
+    arrays = [np.ascontiguousarray(a) for a in arrays]
+    offs, total = [], 0
+    for a in arrays:
+        total = (total + 15) // 16 * 16
+        offs.append(total)
+        total += a.nbytes
+    host = np.zeros((total + 15) // 16 * 16 or 16, dtype=np.uint8)
+    for a, o in zip(arrays, offs):
+        host[o:o + a.nbytes] = a.reshape(-1).view(np.uint8)
+    d = torch.as_tensor(host, device=dev)
+    return [d[o:o + a.nbytes].view(_TORCH_DT[a.dtype]).view(a.shape) for a, o in zip(arrays, offs)]
+
+
 def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int, steps: int, dt: float,
                 sigma: float, spec: GridSpec, mode: str, per_human_layers: bool = True,
                 union64: bool = False, union32: bool = False, time_union: bool = False,
@@ -233,23 +254,26 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
         if len(j.beta_of) > 128:
             raise NotImplementedError("at most 128 hypotheses per human")
         hyp_off[i + 1] = hyp_off[i] + len(j.beta_of)
-    up = lambda a, dt_: torch.as_tensor(np.array(a, dtype=dt_, order="C"), device=dev)
-    d_start = up([[np.float32(j.z0.x), np.float32(j.z0.y)] for j in jobs], np.float32)
-    d_hyp_off = up(hyp_off, np.int32)
-    d_beta = up(np.concatenate([j.beta_of for j in jobs]).astype(np.float32), np.float32)
-    d_goal = up(np.concatenate([j.goal_xy_of for j in jobs]).astype(np.float32), np.float32)
-    d_cdf = up(np.concatenate([host_cdf(j.log_weights) for j in jobs]), np.float64)
-    d_seed = up([int(j.seed) & _MASK64 for j in jobs], np.uint64)
     pre = np.zeros((H, 4), dtype=np.uint32)
     plen = np.zeros(H, dtype=np.int32)
     for i, j in enumerate(jobs):
         w = _prefix_words(j.prefix)
         pre[i, :len(w)] = w
         plen[i] = len(w)
-    d_pre, d_plen = up(pre, np.uint32), up(plen, np.int32)
-    d_tid = up([j.table for j in jobs], np.int32)
+    # every per-call input in ONE host-to-device copy (the small per-array uploads cost a
+    # copy each -- most of a small predict's latency)
+    (d_start, d_hyp_off, d_beta, d_goal, d_cdf, d_seed, d_pre, d_plen, d_tid, err) = _upload_packed(dev, [
+        np.array([[j.z0.x, j.z0.y] for j in jobs], dtype=np.float32),
+        hyp_off,
+        np.concatenate([j.beta_of for j in jobs]).astype(np.float32),
+        np.concatenate([j.goal_xy_of for j in jobs]).astype(np.float32),
+        np.concatenate([host_cdf(j.log_weights) for j in jobs]).astype(np.float64),
+        np.array([int(j.seed) & _MASK64 for j in jobs], dtype=np.uint64),
+        pre, plen,
+        np.array([j.table for j in jobs], dtype=np.int32),
+        np.zeros(1, dtype=np.int32),  # the device status word
+    ])
     counts = torch.zeros(H * geo.human_stride, dtype=torch.int32, device=dev)
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
     out = {}
     if want_hyp:
         out["hyp"] = torch.empty((H, n), dtype=torch.int32, device=dev)
