@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .agents import ControlAction, ControlSet, GoalSet, HumanState, QFunction, RationalitySet
-from .device import device, stream_handle
+from .device import device, stream_handle, upload_packed
 from .tables import f64_tables, hypothesis_arrays, recognise_q
 
 LOG_WEIGHT_FLOOR = -745.0
@@ -229,13 +229,16 @@ def update_belief(belief: JointBelief, z_t: HumanState, z_next: HumanState, dt: 
     if bt.kind == _lib.GC_Q_TABLE:
         xy = np.tile(np.array([[z_t.x, z_t.y]], dtype=float), (H, 1))
         d_qtable = up(np.asarray(q.table(xy, goal_of, control_set), dtype=float), np.float64)
-    d_prior = up(prior, np.float64)
+    # every per-call input in one host-to-device copy (a copy each costs most of a small
+    # update's latency)
+    (d_prior, d_off, d_beta, d_goal, d_obs, d_fb, d_status) = upload_packed(dev, [
+        np.asarray(prior, dtype=np.float64), np.array([0, H], dtype=np.int32),
+        np.asarray(beta_of, dtype=np.float64), np.asarray(goal_of, dtype=np.float64),
+        np.array([z_t.x, z_t.y, z_next.x, z_next.y], dtype=np.float64),
+        np.array([fallback_theta], dtype=np.float64), np.zeros(1, dtype=np.int32)])
     d_post = torch.empty_like(d_prior)
-    d_status = torch.zeros(1, dtype=torch.int32, device=dev)
     tol = bt.snap_tol if snap_tol is None else float(snap_tol)
-    launch_belief_update(bt, up([0, H], np.int32), up(beta_of, np.float64), up(goal_of, np.float64),
-                         up([z_t.x, z_t.y, z_next.x, z_next.y], np.float64),
-                         up([fallback_theta], np.float64), d_prior, d_post, d_status, dt,
+    launch_belief_update(bt, d_off, d_beta, d_goal, d_obs, d_fb, d_prior, d_post, d_status, dt,
                          tol if not math.isinf(tol) else math.inf, 0, 1, d_qtable=d_qtable)
     status = int(d_status.item())
     _lib.check(status, "update_belief")

@@ -27,7 +27,7 @@ import torch
 from . import _lib
 from .agents import ControlSet, HumanState, QFunction
 from .belief import HypothesisSpace, JointBelief
-from .device import device, stream_handle
+from .device import device, stream_handle, upload_packed
 from .occupancy import GridSpec, OccupancyGrid
 from .tables import ActionTables, Geometry, assume_qg, hypothesis_arrays
 
@@ -197,27 +197,6 @@ class HumanJob:
     table: int = 0
 
 
-_TORCH_DT = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
-             np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.int32, np.dtype(np.uint64): torch.int64}
-
-
-def _upload_packed(dev, arrays):
-    """Copy several small host arrays to the device in one transfer; returns device views
-    (16-byte aligned, same shapes; unsigned types are viewed as their signed twins, which
-    the C ABI reads as the unsigned bits)."""
-    arrays = [np.ascontiguousarray(a) for a in arrays]
-    offs, total = [], 0
-    for a in arrays:
-        total = (total + 15) // 16 * 16
-        offs.append(total)
-        total += a.nbytes
-    host = np.zeros((total + 15) // 16 * 16 or 16, dtype=np.uint8)
-    for a, o in zip(arrays, offs):
-        host[o:o + a.nbytes] = a.reshape(-1).view(np.uint8)
-    d = torch.as_tensor(host, device=dev)
-    return [d[o:o + a.nbytes].view(_TORCH_DT[a.dtype]).view(a.shape) for a, o in zip(arrays, offs)]
-
-
 def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int, steps: int, dt: float,
                 sigma: float, spec: GridSpec, mode: str, per_human_layers: bool = True,
                 union64: bool = False, union32: bool = False, time_union: bool = False,
@@ -262,7 +241,7 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
         plen[i] = len(w)
     # every per-call input in ONE host-to-device copy (the small per-array uploads cost a
     # copy each -- most of a small predict's latency)
-    (d_start, d_hyp_off, d_beta, d_goal, d_cdf, d_seed, d_pre, d_plen, d_tid, err) = _upload_packed(dev, [
+    (d_start, d_hyp_off, d_beta, d_goal, d_cdf, d_seed, d_pre, d_plen, d_tid, err) = upload_packed(dev, [
         np.array([[j.z0.x, j.z0.y] for j in jobs], dtype=np.float32),
         hyp_off,
         np.concatenate([j.beta_of for j in jobs]).astype(np.float32),
