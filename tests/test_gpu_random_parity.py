@@ -1,0 +1,87 @@
+"""GPU: randomized differential parity of the drop-in predict() (reference RNG mode) against
+the pinned oracle (tests/test_oracle_golden.py pins the oracle to the live reference).
+
+Eighty random scenes, each drawing: a speed x heading grid (2-4 speeds, 8/12/24 headings --
+the 4 x 24 grid takes the specialised filter, the others the generic one) or a set of
+random actions; q_goal_progress (random tau and action weights) or q_default, optionally
+mask_stationary; 1-5 rationality values x 1-4 goals with a random belief; a random grid
+(size, resolution, origin) with the start anywhere in it (edge clamping); ragged particle
+counts, horizons, time steps, seeds and stream prefixes.  Every per-step occupancy layer
+must equal the oracle's bit for bit (sigma = 0: counts / n exactly).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_01122_b200 as G  # noqa: E402
+from oracle import model  # noqa: E402
+from oracle import predict as OP  # noqa: E402
+
+
+def scene(seed):
+    r = np.random.default_rng(1000 + seed)
+    if r.random() < 0.6:
+        ns, nh = int(r.integers(2, 5)), int(r.choice([8, 12, 24]))
+        if seed % 5 == 0:
+            ns, nh = 4, 24  # the standard grid: the specialised reference filter
+        v, th = model.control_grid(ns, nh, float(r.uniform(0.5, 2.0)))
+    else:
+        m = int(r.integers(6, 81))
+        v, th = r.uniform(0.0, 1.8, m), r.uniform(-math.pi, math.pi, m)
+        v[0] = 0.0  # a stay action
+    cs = G.ControlSet([G.ControlAction(float(a), float(b)) for a, b in zip(v, th)])
+    v, th = np.asarray(cs.v, float), np.asarray(cs.theta, float)  # the wrapped values
+    wv, wth = (float(r.uniform(0, 0.5)), float(r.uniform(0, 0.3))) if r.random() < 0.5 else (0.0, 0.0)
+    thr = float(r.uniform(0.3, 1.2)) if r.random() < 0.3 else None
+    if r.random() < 0.75:
+        tau = float(r.uniform(0.2, 1.0))
+        q = G.q_goal_progress(tau, (wv, wth))
+        qs = model.QSpec("goal_progress", tau, wv, wth, thr)
+    else:
+        wv = wv or 0.3
+        q = G.q_default((wv, wth))
+        qs = model.QSpec("default", 0.5, wv, wth, thr)
+    if thr is not None:
+        if not np.any(v <= thr):
+            thr = None
+            qs.v_threshold = None
+        else:
+            q = G.mask_stationary(q, cs, thr)
+    W, H = int(r.integers(20, 91)), int(r.integers(20, 91))
+    res = float(r.choice([0.05, 0.1, 0.2]))
+    origin = (float(r.uniform(-3, 3)), float(r.uniform(-3, 3)))
+    spec = G.GridSpec(W, H, res, origin)
+    start = (origin[0] + float(r.uniform(0, W * res)), origin[1] + float(r.uniform(0, H * res)))
+    nb = int(r.integers(1, 6))
+    betas = tuple(sorted(set(float(b) for b in np.round(np.geomspace(0.05, 30, 12)[r.choice(12, nb, replace=False)], 6))))
+    k = int(r.integers(1, 5))
+    goals = np.stack([start[0] + r.uniform(-4, 4, k), start[1] + r.uniform(-4, 4, k)], 1)
+    space = G.HypothesisSpace(G.RationalitySet(betas), G.GoalSet(goals))
+    w = r.dirichlet(np.ones(space.size))
+    belief = G.JointBelief.from_probs(w)
+    n, T = int(r.integers(100, 5001)), int(r.integers(1, 13))
+    dt = float(r.uniform(0.05, 0.4))
+    seed_p = int(r.integers(0, 2**31))
+    prefix = tuple(int(x) for x in r.integers(0, 50, int(r.integers(0, 3))))
+    return cs, q, qs, v, th, spec, start, space, belief, n, T, dt, seed_p, prefix
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_random_scene_reference_mode_bit_exact(seed):
+    cs, q, qs, v, th, spec, start, space, belief, n, T, dt, seed_p, prefix = scene(seed)
+    cfg = G.PredictionConfig(n=n, steps=T, dt=dt, smoothing_sigma=0.0, seed=seed_p)
+    st = G.predict(G.HumanState(*start), belief, cfg, cs, q, space, spec, prefix=prefix)
+    tables = model.make_tables(v, th, dt, qs)
+    o = OP.predict(start, belief.log_weights, n, T, dt, 0.0, seed_p, tables, space.beta_of, space.goal_xy_of,
+                   OP.Grid(spec.width, spec.height, spec.resolution, spec.origin), prefix=prefix)
+    got = st.layers
+    assert got.shape == o["layers"].shape
+    bad = np.argwhere(got != o["layers"])
+    assert len(bad) == 0, (f"scene {seed}: {len(bad)} cells differ, first {bad[:3].tolist()}; "
+                           f"m={len(v)} q={qs} n={n} T={T}")
+    torch.cuda.synchronize()
