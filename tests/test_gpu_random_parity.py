@@ -1,5 +1,6 @@
-"""GPU: randomized differential parity of the drop-in predict() (reference RNG mode) against
-the pinned oracle (tests/test_oracle_golden.py pins the oracle to the live reference).
+"""GPU: randomized differential parity of the drop-in predict() (reference RNG mode) and
+update_belief() against the pinned oracle (tests/test_oracle_golden.py pins the oracle to
+the live reference), and of production mode against the exact one-step mixture.
 
 Eighty random scenes, each drawing: a speed x heading grid (2-4 speeds, 8/12/24 headings --
 the 4 x 24 grid takes the specialised filter, the others the generic one) or a set of
@@ -85,3 +86,50 @@ def test_random_scene_reference_mode_bit_exact(seed):
     assert len(bad) == 0, (f"scene {seed}: {len(bad)} cells differ, first {bad[:3].tolist()}; "
                            f"m={len(v)} q={qs} n={n} T={T}")
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_belief_update_matches_oracle(seed):
+    """update_belief (K1) on random scenes -- random control sets, utilities (masked or not),
+    hypothesis spaces and priors, an observed move along a random action (with a little
+    noise, snapped back by the reference's tolerance) -- against the oracle's float64
+    restatement of belief.py:159-198: posteriors within 1e-9 relative (north star: 1e-5)."""
+    cs, q, qs, v, th, spec, start, space, belief, n, T, dt, seed_p, prefix = scene(seed)
+    r = np.random.default_rng(5000 + seed)
+    a = int(r.integers(0, len(v)))
+    if qs.v_threshold is not None and v[a] > qs.v_threshold:
+        a = int(np.flatnonzero(v <= qs.v_threshold)[0])
+    z_t = G.HumanState(*start)
+    z_n = G.HumanState(start[0] + v[a] * math.cos(th[a]) * dt + float(r.normal(0, 1e-6)),
+                       start[1] + v[a] * math.sin(th[a]) * dt + float(r.normal(0, 1e-6)))
+    post = G.update_belief(belief, z_t, z_n, dt, cs, q, space, fallback_theta=float(th[a]))
+    want, _ = OP.belief_update(belief.log_weights, (z_t.x, z_t.y), (z_n.x, z_n.y), dt, v, th, qs,
+                               space.beta_of, space.goal_xy_of, fallback_theta=float(th[a]))
+    np.testing.assert_allclose(np.exp(post.log_weights), np.exp(want), rtol=1e-9, atol=1e-300)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_production_one_step_exact_in_distribution(seed):
+    """Production mode on the random scenes' control sets, utilities and beliefs (the
+    factorised sampler for 24-heading grids with goal-progress utility, the one-pass /
+    two-pass generic sampler otherwise): one step of 2^21 particles on a 1 mm grid, where
+    every action lands in its own cell, against the float64 Boltzmann mixture -- total
+    variation within the Monte-Carlo noise."""
+    cs, q, qs, v, th, spec, start, space, belief, n, T, dt, seed_p, prefix = scene(seed)
+    z = G.HumanState(0.5005, 0.5005)
+    space = G.HypothesisSpace(space.rationalities, G.GoalSet(np.asarray(space.goals.positions) - np.array(start) + 0.5))
+    grid = G.GridSpec(1000, 1000, 0.001)
+    cfg = G.PredictionConfig(n=1 << 21, steps=1, dt=0.2, smoothing_sigma=0.0, seed=seed_p, mode="production")
+    layer = G.predict(z, belief, cfg, cs, q, space, grid).layers[0]
+    p = np.zeros(len(cs))
+    for h, (b, g) in enumerate(zip(space.beta_of, space.goal_xy_of)):
+        p += belief.probs()[h] * G.boltzmann_policy(z, b, g, cs, q)
+    disp = cs.displacements(0.2).astype(np.float32)
+    x = np.float32(z.x) + disp[:, 0]
+    y = np.float32(z.y) + disp[:, 1]
+    ix = np.clip(np.floor(x / np.float32(0.001)).astype(int), 0, 999)
+    iy = np.clip(np.floor(y / np.float32(0.001)).astype(int), 0, 999)
+    exact = np.zeros((1000, 1000))
+    np.add.at(exact, (iy, ix), p)
+    tv = 0.5 * np.abs(layer - exact).sum()
+    assert tv < 0.008, (seed, tv, len(cs))
