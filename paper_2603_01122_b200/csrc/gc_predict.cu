@@ -264,7 +264,8 @@ static __device__ __noinline__ int ref_pick_exact(const SmemAct &S, float rx, fl
 // so |w~_k - w_k| <= EPS_W w_k + A_W.  A sequential float32 sum is within 2^-24 sum_{j<=k} c_j
 // of the exact sum of its terms (each add rounds by at most 2^-24 of its result, the
 // first term is exact), so with T~_k = sum_{j<=k} c~_j (bounded from the block sums: every
-// c~_j of block b is <= blk[b]) the two chains differ at index k by at most
+// c~_j of block b is <= blk[b]; the specialised filter bounds the blocks before the one
+// holding r by jb B blk[jb - 1]) the two chains differ at index k by at most
 //   D_k = 2^-23 T~_k + EPS_W c~_k + (k + 1) A_W,
 // and r = fl(u c_N) differs from r~ = fl(u c~_N) by at most D_r = u D_N + 2^-23 r~.  If the
 // filter's pick k has r~ - c~_{k-1} > D_{k-1} + D_r and c~_k - r~ > D_k + D_r, then
@@ -372,12 +373,13 @@ __device__ __forceinline__ int ref_fast_spec(const SmemAct &S, float rx, float r
     if (lm != M) { M = lm; return -1; }
     const float r = __fmul_rn(u, c);
     int jb = 0;
-    float cc = 0.f, tpre = 0.f, tall = blk[NBLK - 1];
+    float cc = 0.f, tall = blk[NBLK - 1];
 #pragma unroll
     for (int j = 0; j < NBLK - 1; ++j) {
         tall = __fadd_rn(tall, blk[j]);
-        if (blk[j] < r) { jb = j + 1; cc = blk[j]; tpre = __fadd_rn(tpre, blk[j]); }
+        if (blk[j] < r) { jb = j + 1; cc = blk[j]; }
     }
+    const float tpre = (float)jb * cc;  // >= the earlier block ends' sum (each <= cc)
     // rescan the block holding r with the same operations (the same chain values)
     float lower = cc;
     int i = 0;
