@@ -1154,6 +1154,15 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : (MODE
         // u32 halves of words (j0 >> 1) .. of ONE Philox4x64 block: one block per thread-step
         const int pg0 = pbase + tid * K + P.p_offset;
         const int j0 = pg0 & 1023;
+        // K = 4: the 8 draws of one Philox4x64 block feed the particles of two adjacent
+        // threads (lanes 2m, 2m + 1 when the CTA's first particle is 8-aligned).  Instead of
+        // both computing it every step, the pair takes turns: at the first step of every
+        // step pair the even lane computes step t's block and the odd lane step t + 1's, and
+        // each hands the other the two words it needs by shuffle -- one block and one key
+        // derivation per lane per two steps.  The draws are unchanged (bit-identical).
+        const bool turns = K == 4 && !P.uniforms && ((pbase + P.p_offset) & 7) == 0;
+        const bool qodd = (tid & 1) != 0;
+        uint64_t tb[4] = {0, 0, 0, 0};  // turns: this lane's block (step t or t + 1)
         for (int t = P.t_begin; t < P.t_end; ++t) {
             const int R = __ldg(&P.step_r[t - 1]);
             const int x0 = max(0, cx - R), x1 = min(P.grid_w - 1, cx + R);
@@ -1162,13 +1171,37 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : (MODE
             unsigned *gcount = P.counts + hbase + __ldg(&P.step_off[t - 1]);
             GC_DCHECK(__ldg(&P.step_off[t - 1]) + (long long)ww * wh <= P.human_stride);
             uint64_t blkw[4] = {0, 0, 0, 0};
-            if (!P.uniforms) {
+            uint64_t w01[2] = {0, 0};  // K = 4: this thread's two words of step t's block
+            if (turns) {
+                if (((t - P.t_begin) & 1) == 0) {
+                    SSPool s = pool_step;
+                    ss_absorb(s, (unsigned)(qodd ? t + 1 : t));
+                    ss_absorb(s, (unsigned)(pg0 >> 10));
+                    uint64_t sk0, sk1;
+                    ss_key(s, sk0, sk1);
+                    philox4x64((uint64_t)(j0 >> 3) + 1, sk0, sk1, tb);
+                    const uint64_t x2 = __shfl_xor_sync(0xffffffffu, tb[2], 1);
+                    const uint64_t x3 = __shfl_xor_sync(0xffffffffu, tb[3], 1);
+                    w01[0] = qodd ? x2 : tb[0];
+                    w01[1] = qodd ? x3 : tb[1];
+                } else {
+                    const uint64_t y0 = __shfl_xor_sync(0xffffffffu, tb[0], 1);
+                    const uint64_t y1 = __shfl_xor_sync(0xffffffffu, tb[1], 1);
+                    w01[0] = qodd ? tb[2] : y0;
+                    w01[1] = qodd ? tb[3] : y1;
+                }
+            } else if (!P.uniforms) {
                 SSPool s = pool_step;
                 ss_absorb(s, (unsigned)t);
                 ss_absorb(s, (unsigned)(pg0 >> 10));
                 uint64_t sk0, sk1;
                 ss_key(s, sk0, sk1);
                 philox4x64((uint64_t)(j0 >> 3) + 1, sk0, sk1, blkw);
+                if (K == 4) {
+                    const int w = (j0 >> 1) & 3;  // 0 or 2
+                    w01[0] = w == 0 ? blkw[0] : blkw[2];
+                    w01[1] = w == 0 ? blkw[1] : blkw[3];
+                }
             }
 #pragma unroll 1
             for (int k = 0; k < K; ++k) {
@@ -1180,6 +1213,10 @@ __global__ void __launch_bounds__(NT, MODE == MODE_REF ? GC_REF_MIN_CTAS : (MODE
                     float u;
                     if (P.uniforms) {
                         u = __ldg(&P.uniforms[((long long)h * P.steps + (t - 1)) * P.n + p]);
+                    } else if (K == 4) {  // draw j0 + k: half k & 1 of the thread's word k >> 1
+                        const uint64_t wd = (k >> 1) ? w01[1] : w01[0];
+                        const uint32_t u32 = (k & 1) ? (uint32_t)(wd >> 32) : (uint32_t)wd;
+                        u = (float)(u32 >> 8) * (1.0f / 16777216.0f);  // random(dtype=float32)
                     } else {
                         const int j = j0 + k, w = (j >> 1) & 3;
                         const uint64_t wd = w == 0 ? blkw[0] : (w == 1 ? blkw[1] : (w == 2 ? blkw[2] : blkw[3]));
