@@ -19,9 +19,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pr
     -o gpurun_out/k2_cfg3 python tools/profile_predict.py --steps 250 --cycles 2 > gpurun_out/ncu_k2.log 2>&1
 fi
 [ "$PART" = a ] && exit 0
-python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/plain_ref.log 2>&1 && \
+python tools/profile_predict.py --mode reference --steps 20 --cycles 2 > gpurun_out/plain_ref.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_predict -s 1 -c 1 \
-    -o gpurun_out/k2_refmode python tools/profile_predict.py --mode reference --steps 20 --humans 1 --n 65536 --cycles 2 > gpurun_out/ncu_ref.log 2>&1
+    -o gpurun_out/k2_refmode python tools/profile_predict.py --mode reference --steps 20 --cycles 2 > gpurun_out/ncu_ref.log 2>&1
 python tools/profile_extras.py > gpurun_out/plain_extras.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_collision|k_mppi|k_exact" -s 2 -c 6 \
     -o gpurun_out/extras python tools/profile_extras.py > gpurun_out/ncu_extras.log 2>&1

@@ -124,9 +124,9 @@ def main():
     ref = os.path.join(src, "k2_refmode.ncu-rep")
     if os.path.exists(ref):
         open(os.path.join(prof, f"{a.tag}_ncu_k2_reference_mode.txt"), "w").write(
-            "# ncu --set full of the REFERENCE-arithmetic kernel k_predict<0,1,0> (1 human x 65536 particles x 20 "
-            "steps)\n" + capture(ncu_summary.main, ref) + "\n# dynamic SASS opcode mix (lane-instructions per "
-            "particle-step)\n" + capture(ncu_opmix.main, ref, 65536 * 20))
+            "# ncu --set full of the REFERENCE-arithmetic kernel k_predict<0,4,0,0> at the cfg3 launch shape (8 humans x "
+            "262144 particles x 20 steps, K = 4 particles per thread)\n" + capture(ncu_summary.main, ref) + "\n# dynamic SASS opcode mix (lane-instructions per "
+            "particle-step)\n" + capture(ncu_opmix.main, ref, 8 * 262144 * 20))
     ext = os.path.join(src, "extras.ncu-rep")
     if os.path.exists(ext):
         open(os.path.join(prof, f"{a.tag}_ncu_frows.txt"), "w").write(
