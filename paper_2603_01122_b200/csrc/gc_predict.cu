@@ -360,9 +360,9 @@ __device__ __forceinline__ int ref_fast_spec(const SmemAct &S, float rx, float r
 #pragma unroll
         for (int i = 0; i < B; i += 2) {
             const float2 q = ref_q2<QK>(S, j * B + i, rx, ry, d2);
-            const float2 L = make_float2(__fmul_rn(q.x, beta), __fmul_rn(q.y, beta));
+            const float2 L = px_mul(q, px2(beta));
             lm = fmaxf(lm, fmaxf(L.x, L.y));
-            const float2 t = px_mul(px_add(L, nM), px2(L2E));
+            const float2 t = px_mul(px_sub_after_mul(L, nM), px2(L2E));
             c = __fadd_rn(c, ex2_approx(t.x));
             c = __fadd_rn(c, ex2_approx(t.y));
         }
