@@ -45,6 +45,21 @@ def test_library_is_sm100a(L):
     assert "sm_100a" in out
 
 
+def test_reference_kernels_have_no_contracted_beta_products(L):
+    """The reference-arithmetic kernels (k_predict<0, ...>) compute fl(fl(beta Q') - M) with two
+    roundings; ptxas can fold a packed product into the following add as one FFMA2 with a
+    scalar multiplier and a negated scalar addend (seen when the product had no other use).
+    No such FFMA2 may appear in their SASS (the GPU bit-exact tests are the final guard)."""
+    so = os.path.join(ROOT, "paper_2603_01122_b200", "_lib", "libgridcast_b200.so")
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s*Function : ", sass)
+    ref = [f for f in funcs if re.match(r"_ZN2gc9k_predictILi0E", f)]
+    assert len(ref) >= 6, len(ref)  # K = 1 / 2 / 4, two histogram paths
+    pat = re.compile(r"FFMA2 R\d+, R\d+\.F32x2\.HI_LO, R\d+\.F32, -R\d+\.F32 ")
+    for f in ref:
+        assert not pat.search(f), f.splitlines()[0]
+
+
 def test_abi_version(L):
     assert L.gc_abi_version() == 3
 
