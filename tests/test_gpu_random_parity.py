@@ -1,4 +1,5 @@
-"""GPU: randomized differential parity of the drop-in predict() (reference RNG mode) and
+"""GPU: randomized differential parity of the drop-in predict() (reference RNG mode, also at
+the K = 2 / K = 4 launch shapes by replicating a scene's human) and
 update_belief() against the pinned oracle (tests/test_oracle_golden.py pins the oracle to
 the live reference), and of production mode against the exact one-step mixture.
 
@@ -133,3 +134,38 @@ def test_random_production_one_step_exact_in_distribution(seed):
     np.add.at(exact, (iy, ix), p)
     tv = 0.5 * np.abs(layer - exact).sum()
     assert tv < 0.008, (seed, tv, len(cs))
+
+
+# random scenes at the K = 2 / K = 4 launch shapes: one human replicated until the launch
+# takes k particles per thread (the headline's K = 4 instantiation, with the lane-pair
+# Philox turns and, for ragged particle counts, CTAs whose first particle is not
+# 8-aligned), every replica bit-identical and equal to the oracle's counts
+K_SEEDS = [2, 3, 7, 15, 19, 20, 23, 32, 36, 37, 43, 45, 53, 65, 70, 73]  # n >= 2500: <= 243 replicas
+
+
+@pytest.mark.parametrize("k", [2, 4])
+@pytest.mark.parametrize("seed", K_SEEDS)
+def test_random_scene_reference_mode_replicated_at_k(seed, k):
+    from paper_2603_01122_b200 import prediction as PR
+    cs, q, qs, v, th, spec, start, space, belief, n, T, dt, seed_p, prefix = scene(seed)
+    thr = 256 * (k // 2) * 2 * 4 * 148  # smallest launch gc_predict runs with k particles per thread
+    humans = -(-thr // n)
+    dev = torch.device("cuda")
+    tab = PR.action_tables(cs, q, dt, dev)
+    job = PR.HumanJob(G.HumanState(*start), belief.log_weights, space.beta_of, space.goal_xy_of, seed_p, prefix, 0)
+    out = PR.run_predict([job] * humans, [tab], n, T, dt, 0.0, spec, "reference", per_human_layers=False)
+    geo = out["geometry"]
+    rows = out["counts"].view(humans, geo.human_stride)
+    assert bool((rows == rows[0]).all()), f"scene {seed}: replicas differ"
+    row = rows[0].cpu().numpy().view(np.uint32).astype(np.int64)
+    tables = model.make_tables(v, th, dt, qs)
+    o = OP.predict(start, belief.log_weights, n, T, dt, 0.0, seed_p, tables, space.beta_of, space.goal_xy_of,
+                   OP.Grid(spec.width, spec.height, spec.resolution, spec.origin), prefix=prefix)
+    start32 = (np.float32(start[0]), np.float32(start[1]))
+    got = np.zeros((T, spec.height, spec.width), dtype=np.int64)
+    for t in range(T):
+        x0, y0, w, hh = geo.window(start32, t)
+        got[t, y0:y0 + hh, x0:x0 + w] = row[geo.step_off[t]:geo.step_off[t] + w * hh].reshape(hh, w)
+    want = np.asarray(o["counts"], dtype=np.int64)
+    bad = np.argwhere(got != want)
+    assert len(bad) == 0, f"scene {seed} k={k} humans={humans}: {len(bad)} cells differ, first {bad[:3].tolist()}"
