@@ -55,7 +55,7 @@ typedef enum {
 /* Size limits of the kernels (shared-memory tables): hypotheses per human (|B| x |G|)
  * and actions per control set.  gc_belief_update marks a human outside 1..GC_MAX_HYPOTHESES
  * with GC_BAD_ARG in d_status; gc_predict raises GC_ERRBIT_HYPOTHESES. */
-#define GC_MAX_HYPOTHESES 128
+#define GC_MAX_HYPOTHESES 256
 #define GC_MAX_ACTIONS 256
 
 /* Utility families (agents.py:245-296).  *_FULL = the reference's `base` (with the

@@ -221,8 +221,8 @@ def update_belief(belief: JointBelief, z_t: HumanState, z_next: HumanState, dt: 
     if transition is not None:
         prior = np.asarray(transition(prior), dtype=float)
     H = len(beta_of)
-    if H > 128:
-        raise NotImplementedError("at most 128 hypotheses per human")
+    if H > _lib.GC_MAX_HYPOTHESES:
+        raise NotImplementedError(f"at most {_lib.GC_MAX_HYPOTHESES} hypotheses per human")
     # np.array copies: the belief's log weights are read-only (immutable snapshots)
     up = lambda a, dt_: torch.as_tensor(np.array(a, dtype=dt_, order="C"), device=dev)  # noqa: E731
     d_qtable = None

@@ -18,7 +18,7 @@
 namespace gc {
 
 constexpr int BT = 256;      // one CTA (8 warps) per human
-constexpr int BMAXH = 128;   // hypotheses per human (4 per lane)
+constexpr int BMAXH = 256;   // hypotheses per human (8 per lane)
 
 struct BParams {
     int n_humans, m, q_kind, clamp;

@@ -131,8 +131,8 @@ class CycleEngine:
         betas, goals, off = [], [], [0]
         for sp in spaces:
             b, g = hypothesis_arrays(sp)
-            if len(b) > 128:
-                raise NotImplementedError("at most 128 hypotheses per human")
+            if len(b) > _lib.GC_MAX_HYPOTHESES:
+                raise NotImplementedError(f"at most {_lib.GC_MAX_HYPOTHESES} hypotheses per human")
             betas.append(b)
             goals.append(g)
             off.append(off[-1] + len(b))

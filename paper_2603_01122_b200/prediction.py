@@ -230,8 +230,8 @@ def run_predict(jobs: Sequence[HumanJob], tables: Sequence[ActionTables], n: int
     geo = geometry(spec, steps, max_step, float(sigma), dev)
     hyp_off = np.zeros(H + 1, dtype=np.int32)
     for i, j in enumerate(jobs):
-        if len(j.beta_of) > 128:
-            raise NotImplementedError("at most 128 hypotheses per human")
+        if len(j.beta_of) > _lib.GC_MAX_HYPOTHESES:
+            raise NotImplementedError(f"at most {_lib.GC_MAX_HYPOTHESES} hypotheses per human")
         hyp_off[i + 1] = hyp_off[i] + len(j.beta_of)
     pre = np.zeros((H, 4), dtype=np.uint32)
     plen = np.zeros(H, dtype=np.int32)

@@ -54,11 +54,12 @@ def _run(a, keep):
     return int(keep["err"].item()) & 0xFFFFFFFF, int(keep["counts"].sum().item())
 
 
-def test_predict_rejects_hypothesis_counts_outside_1_to_128():
-    a, keep = _args([4, 4])
-    word, total = _run(a, keep)
-    assert word == 0 and total == 2 * 512 * 6
-    for bad in ([4, 0], [129, 4]):
+def test_predict_rejects_hypothesis_counts_outside_1_to_256():
+    for ok in ([4, 4], [256, 1]):  # both ends of the range
+        a, keep = _args(ok)
+        word, total = _run(a, keep)
+        assert word == 0 and total == 2 * 512 * 6
+    for bad in ([4, 0], [257, 4]):
         a, keep = _args(bad)
         word, _ = _run(a, keep)
         assert word & _lib.GC_ERRBIT_HYPOTHESES
@@ -105,7 +106,7 @@ def test_belief_update_rejects_too_many_hypotheses():
     dev = torch.device("cuda")
     cs = G.ControlSet.grid(4, 24, 1.4)
     btab = belief_tables(cs, G.q_goal_progress(0.5), dev)
-    nh = 130
+    nh = _lib.GC_MAX_HYPOTHESES + 2
     off = torch.tensor([0, nh], dtype=torch.int32, device=dev)
     beta = torch.ones(nh, dtype=torch.float64, device=dev)
     goal = torch.full((nh, 2), 5.0, dtype=torch.float64, device=dev)

@@ -169,3 +169,35 @@ def test_random_scene_reference_mode_replicated_at_k(seed, k):
     want = np.asarray(o["counts"], dtype=np.int64)
     bad = np.argwhere(got != want)
     assert len(bad) == 0, f"scene {seed} k={k} humans={humans}: {len(bad)} cells differ, first {bad[:3].tolist()}"
+
+
+@pytest.mark.parametrize("nb,ng", [(9, 16), (12, 21), (16, 16)])
+def test_many_hypotheses_reference_mode_and_update(nb, ng):
+    """|B| x |G| up to the 256-hypothesis limit (128-256): predict() in reference mode bit
+    for bit against the oracle, and the belief update against its float64 restatement."""
+    r = np.random.default_rng(nb * 100 + ng)
+    cs = G.ControlSet.grid(4, 24, 1.4)
+    q = G.q_goal_progress(0.5)
+    qs = model.QSpec("goal_progress", 0.5, 0.0, 0.0, None)
+    v, th = np.asarray(cs.v, float), np.asarray(cs.theta, float)
+    betas = tuple(float(b) for b in np.round(np.geomspace(0.05, 30, nb), 6))
+    start = (2.0, 3.0)
+    goals = np.stack([start[0] + r.uniform(-4, 4, ng), start[1] + r.uniform(-4, 4, ng)], 1)
+    space = G.HypothesisSpace(G.RationalitySet(betas), G.GoalSet(goals))
+    assert 128 < space.size <= 256
+    belief = G.JointBelief.from_probs(r.dirichlet(np.ones(space.size)))
+    spec = G.GridSpec(50, 50, 0.1)
+    n, T, dt, seed_p = 3000, 6, 0.2, 11
+    cfg = G.PredictionConfig(n=n, steps=T, dt=dt, smoothing_sigma=0.0, seed=seed_p)
+    st = G.predict(G.HumanState(*start), belief, cfg, cs, q, space, spec, prefix=(2, 1))
+    tables = model.make_tables(v, th, dt, qs)
+    o = OP.predict(start, belief.log_weights, n, T, dt, 0.0, seed_p, tables, space.beta_of, space.goal_xy_of,
+                   OP.Grid(spec.width, spec.height, spec.resolution, spec.origin), prefix=(2, 1))
+    assert np.array_equal(st.layers, o["layers"])
+    a = 30
+    z_t = G.HumanState(*start)
+    z_n = G.HumanState(start[0] + v[a] * math.cos(th[a]) * dt, start[1] + v[a] * math.sin(th[a]) * dt)
+    post = G.update_belief(belief, z_t, z_n, dt, cs, q, space, fallback_theta=float(th[a]))
+    want, _ = OP.belief_update(belief.log_weights, (z_t.x, z_t.y), (z_n.x, z_n.y), dt, v, th, qs,
+                               space.beta_of, space.goal_xy_of, fallback_theta=float(th[a]))
+    np.testing.assert_allclose(np.exp(post.log_weights), np.exp(want), rtol=1e-9, atol=1e-300)
