@@ -56,6 +56,8 @@ typedef enum {
  * and actions per control set.  gc_belief_update marks a human outside 1..GC_MAX_HYPOTHESES
  * with GC_BAD_ARG in d_status; gc_predict raises GC_ERRBIT_HYPOTHESES. */
 #define GC_MAX_HYPOTHESES 256
+/* smoothing radius ceil(3 sigma / res) in cells (gc_grid_epilogue, gc_smooth_layers) */
+#define GC_MAX_SMOOTH_RADIUS 56
 #define GC_MAX_ACTIONS 256
 
 /* Utility families (agents.py:245-296).  *_FULL = the reference's `base` (with the

@@ -20,7 +20,7 @@ namespace gc {
 
 constexpr int ET = 32;    // output tile edge
 constexpr int ENT = 256;  // threads per CTA
-constexpr int MAXRAD = 16;
+constexpr int MAXRAD = GC_MAX_SMOOTH_RADIUS;  // max smoothing radius (cells): the runtime-radius tile, (32 + 2R)^2 + 32 (32 + 2R) doubles, fits 227 KB
 
 struct EParams {
     int n_humans, n, steps, grid_w, grid_h, radius, n_tiles, time_union;

@@ -253,8 +253,8 @@ class Geometry:
             self.radius = int(np.ceil(3.0 * sc))
             offs = np.arange(-self.radius, self.radius + 1)
             k = np.exp(-0.5 * (offs / sc) ** 2)
-        if self.radius > 16:
-            raise NotImplementedError("smoothing radius above 16 cells is not implemented")
+        if self.radius > _lib.GC_MAX_SMOOTH_RADIUS:
+            raise NotImplementedError(f"smoothing radius above {_lib.GC_MAX_SMOOTH_RADIUS} cells is not implemented")
         self.kernel = k
 
         def zmass(size):

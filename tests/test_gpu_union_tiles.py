@@ -107,3 +107,33 @@ def test_epilogue_radii_match_the_standalone_smoother(sigma):
         for t in (0, 5, 11):
             np.testing.assert_allclose(lay[h, t], smooth_values(raw[h, t], spec, sigma), rtol=0, atol=1e-15)
     np.testing.assert_array_equal(out["union64"].cpu().numpy(), lay.max(axis=0))
+
+
+@pytest.mark.parametrize("sigma", [0.13, 0.186])
+def test_large_smoothing_radii_match_the_reference_operator(sigma):
+    """Radii far above the bench's 3 cells (39 and 56 = GC_MAX_SMOOTH_RADIUS on a 1 cm grid):
+    the fused epilogue's layers and the standalone smoother both equal the oracle's dense
+    restatement of smooth_values (bit-identical to the reference, tests/test_oracle_golden.py)
+    within 1e-15; one radius more raises NotImplementedError like any unsupported input."""
+    import paper_2603_01122_b200 as G
+    from paper_2603_01122_b200 import prediction as PR
+    from paper_2603_01122_b200.occupancy import smooth_layers_device
+    from oracle import predict as OP
+    cs, q = G.ControlSet.grid(4, 24, 1.4), G.q_goal_progress(0.5)
+    tab = PR.action_tables(cs, q, 0.05, torch.device("cuda"))
+    spec = G.GridSpec(200, 160, 0.01)
+    space = G.HypothesisSpace(G.RationalitySet((0.5, 3.0)), G.GoalSet(np.array([[1.7, 1.2], [0.2, 0.3]])))
+    lw = np.log(np.array([0.4, 0.1, 0.3, 0.2]))
+    jobs = [PR.HumanJob(G.HumanState(1.0, 0.8), lw, space.beta_of, space.goal_xy_of, 5, (2, 0), 0)]
+    raw = PR.run_predict(jobs, [tab], 20000, 4, 0.05, 0.0, spec, "production")["layers"]
+    out = PR.run_predict(jobs, [tab], 20000, 4, 0.05, sigma, spec, "production", union64=True)
+    lay = out["layers"].cpu().numpy()
+    alone = smooth_layers_device(raw[0].contiguous(), spec, sigma).cpu().numpy()
+    g = OP.Grid(spec.width, spec.height, spec.resolution)
+    for t in range(4):
+        want = OP.smooth_dense(raw[0, t].cpu().numpy(), g, sigma)
+        np.testing.assert_allclose(lay[0, t], want, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(alone[t], want, rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(out["union64"].cpu().numpy(), lay.max(axis=0))
+    with pytest.raises(NotImplementedError):
+        smooth_layers_device(raw[0].contiguous(), spec, 0.19)
