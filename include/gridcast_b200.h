@@ -58,7 +58,7 @@ typedef enum {
 #define GC_MAX_HYPOTHESES 256
 /* smoothing radius ceil(3 sigma / res) in cells (gc_grid_epilogue, gc_smooth_layers) */
 #define GC_MAX_SMOOTH_RADIUS 56
-#define GC_MAX_ACTIONS 256
+#define GC_MAX_ACTIONS 512
 
 /* Utility families (agents.py:245-296).  *_FULL = the reference's `base` (with the
  * row-constant -|rel|^2), used when a stationary mask dropped base_policy (belief.py:222). */

@@ -47,6 +47,9 @@ __device__ __forceinline__ double wrap_angle(double th) {
     return pymod(th + PI, TWO_PI) - PI;
 }
 
+// SPL actions per lane (m <= 32 SPL): 8 for up to 256 actions, 16 for up to GC_MAX_ACTIONS;
+// the extra slots of the wider instance are empty for m <= 256 (no change in any sum's order)
+template <int SPL>
 __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
     // one CTA per human: every warp recovers/snaps the control (identical results), then
     // warp w takes hypotheses w, w + NW, ...; warp 0 normalises from shared memory
@@ -94,11 +97,11 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
         if (threadIdx.x == 0) P.status[h] = GC_BAD_ARG;
         return;
     }
-    // per-action tables of this lane's actions, loaded once (<= 8 per lane)
-    double ax[8], ay[8], aat[8];
-    bool amask[8];
+    // per-action tables of this lane's actions, loaded once (<= SPL per lane)
+    double ax[SPL], ay[SPL], aat[SPL];
+    bool amask[SPL];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int s = 0; s < SPL; ++s) {
         const int j = lane + 32 * s;
         const bool ok = j < P.m;
         amask[s] = !ok || (P.masked && P.masked[j]);
@@ -114,10 +117,10 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
         const double rx = zx - P.goal[2 * (h0 + i)];
         const double ry = zy - P.goal[2 * (h0 + i) + 1];
         const double d2 = __dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry));
-        double Lj[8];  // m <= 256 actions: 8 per lane
+        double Lj[SPL];  // m <= 32 SPL actions
         double mx = NEG_INF;
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
+        for (int s = 0; s < SPL; ++s) {
             const int j = lane + 32 * s;
             double L = NEG_INF;
             if (!amask[s]) {
@@ -144,13 +147,13 @@ __global__ void __launch_bounds__(BT) k_belief(const BParams P) {
         }
         double ssum = 0.0;
 #pragma unroll
-        for (int s = 0; s < 8; ++s) if (Lj[s] > NEG_INF) ssum += exp(Lj[s] - mx);
+        for (int s = 0; s < SPL; ++s) if (Lj[s] > NEG_INF) ssum += exp(Lj[s] - mx);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
         // the observed action's logit lives in lane idx % 32, slot idx / 32
         double Lmine = NEG_INF;
 #pragma unroll
-        for (int s = 0; s < 8; ++s) if (s == (idx >> 5)) Lmine = Lj[s];
+        for (int s = 0; s < SPL; ++s) if (s == (idx >> 5)) Lmine = Lj[s];
         const double Li = __shfl_sync(0xffffffffu, Lmine, idx & 31);
         const double ll = (Li > NEG_INF) ? (Li - mx) - log(ssum) : NEG_INF;
         if (lane == 0) {
@@ -197,7 +200,8 @@ using namespace gc;
 
 extern "C" gc_status gc_belief_update(const gc_belief_args *a, void *stream) {
     GC_CHECK_ARG(a != nullptr, "gc_belief_update: null args");
-    GC_CHECK_ARG(a->n_humans >= 1 && a->m >= 1 && a->m <= 256, "gc_belief_update: 1..256 actions");
+    GC_CHECK_ARG(a->n_humans >= 1 && a->m >= 1 && a->m <= GC_MAX_ACTIONS, "gc_belief_update: 1..%d actions",
+                 GC_MAX_ACTIONS);
     GC_CHECK_ARG(a->d_v && a->d_theta && a->d_hyp_off && a->d_beta && a->d_goal && a->d_obs &&
                  a->d_fallback_theta && a->d_prior && a->d_post && a->d_status,
                  "gc_belief_update: missing device buffers");
@@ -212,7 +216,8 @@ extern "C" gc_status gc_belief_update(const gc_belief_args *a, void *stream) {
     P.beta = a->d_beta; P.goal = a->d_goal; P.obs = a->d_obs; P.fallback = a->d_fallback_theta;
     P.dt = a->dt; P.snap_tol = a->snap_tol; P.prior = a->d_prior; P.post = a->d_post;
     P.status = a->d_status; P.action = a->d_action;
-    k_belief<<<a->n_humans, BT, 0, (cudaStream_t)stream>>>(P);
+    if (a->m <= 256) k_belief<8><<<a->n_humans, BT, 0, (cudaStream_t)stream>>>(P);
+    else k_belief<GC_MAX_ACTIONS / 32><<<a->n_humans, BT, 0, (cudaStream_t)stream>>>(P);
     count_launch();
     return cuda_check(cudaGetLastError(), "k_belief launch");
 }

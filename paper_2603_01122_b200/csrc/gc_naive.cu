@@ -13,7 +13,7 @@
 namespace gc {
 
 constexpr int NB_T = 128;
-constexpr int NB_MAXM = 256;
+constexpr int NB_MAXM = GC_MAX_ACTIONS;
 
 struct NParams {
     int n, steps, m_keep, q_kind, grid_w, grid_h, prefix_len;

@@ -29,7 +29,7 @@
 namespace gc {
 
 constexpr int NT = 256;        // threads per CTA
-constexpr int MAXM = 256;      // max actions per control set
+constexpr int MAXM = GC_MAX_ACTIONS;  // max actions per control set (512)
 constexpr int MAXH = 256;      // max hypotheses per human (the per-slot index is a byte)
 constexpr int NBF = 24;        // headings of the factorised sampler (ControlSet.grid default)
 constexpr int NAF = 4;         // max speeds of the factorised sampler

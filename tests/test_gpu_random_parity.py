@@ -201,3 +201,56 @@ def test_many_hypotheses_reference_mode_and_update(nb, ng):
     want, _ = OP.belief_update(belief.log_weights, (z_t.x, z_t.y), (z_n.x, z_n.y), dt, v, th, qs,
                                space.beta_of, space.goal_xy_of, fallback_theta=float(th[a]))
     np.testing.assert_allclose(np.exp(post.log_weights), np.exp(want), rtol=1e-9, atol=1e-300)
+
+
+@pytest.mark.parametrize("kind", ["grid", "random"])
+def test_many_actions_reference_mode_update_and_production(kind):
+    """Control sets above 256 actions (up to GC_MAX_ACTIONS = 512): a 6 x 60 grid and 420
+    random actions -- reference-mode predict() bit for bit against the oracle, the belief
+    update against its float64 restatement, and one production step against the exact
+    Boltzmann mixture (the generic sampler)."""
+    r = np.random.default_rng(7 if kind == "grid" else 8)
+    if kind == "grid":
+        v, th = model.control_grid(6, 60, 1.8)
+    else:
+        v, th = r.uniform(0.0, 1.8, 420), r.uniform(-math.pi, math.pi, 420)
+        v[0] = 0.0
+    cs = G.ControlSet([G.ControlAction(float(a), float(b)) for a, b in zip(v, th)])
+    assert 256 < len(cs) <= 512
+    v, th = np.asarray(cs.v, float), np.asarray(cs.theta, float)
+    q = G.q_goal_progress(0.5, (0.2, 0.1))
+    qs = model.QSpec("goal_progress", 0.5, 0.2, 0.1, None)
+    start = (2.0, 3.0)
+    goals = np.stack([start[0] + r.uniform(-4, 4, 3), start[1] + r.uniform(-4, 4, 3)], 1)
+    space = G.HypothesisSpace(G.RationalitySet((0.3, 2.0, 9.0)), G.GoalSet(goals))
+    belief = G.JointBelief.from_probs(r.dirichlet(np.ones(space.size)))
+    spec = G.GridSpec(60, 60, 0.1)
+    n, T, dt, seed_p = 2500, 5, 0.2, 3
+    st = G.predict(G.HumanState(*start), belief, G.PredictionConfig(n=n, steps=T, dt=dt, smoothing_sigma=0.0,
+                   seed=seed_p), cs, q, space, spec, prefix=(2, 4))
+    tables = model.make_tables(v, th, dt, qs)
+    o = OP.predict(start, belief.log_weights, n, T, dt, 0.0, seed_p, tables, space.beta_of, space.goal_xy_of,
+                   OP.Grid(spec.width, spec.height, spec.resolution, spec.origin), prefix=(2, 4))
+    assert np.array_equal(st.layers, o["layers"])
+    a = 301
+    z_t = G.HumanState(*start)
+    z_n = G.HumanState(start[0] + v[a] * math.cos(th[a]) * dt, start[1] + v[a] * math.sin(th[a]) * dt)
+    post = G.update_belief(belief, z_t, z_n, dt, cs, q, space, fallback_theta=float(th[a]))
+    want, _ = OP.belief_update(belief.log_weights, (z_t.x, z_t.y), (z_n.x, z_n.y), dt, v, th, qs,
+                               space.beta_of, space.goal_xy_of, fallback_theta=float(th[a]))
+    np.testing.assert_allclose(np.exp(post.log_weights), np.exp(want), rtol=1e-9, atol=1e-300)
+    # production, one step of 2^21 particles on a 1 mm grid (every action its own cell)
+    z = G.HumanState(0.5005, 0.5005)
+    sp2 = G.HypothesisSpace(space.rationalities, G.GoalSet(goals - np.array(start) + 0.5))
+    grid = G.GridSpec(1000, 1000, 0.001)
+    cfg = G.PredictionConfig(n=1 << 21, steps=1, dt=0.2, smoothing_sigma=0.0, seed=seed_p, mode="production")
+    layer = G.predict(z, belief, cfg, cs, q, sp2, grid).layers[0]
+    p = np.zeros(len(cs))
+    for h, (b, g) in enumerate(zip(sp2.beta_of, sp2.goal_xy_of)):
+        p += belief.probs()[h] * G.boltzmann_policy(z, b, g, cs, q)
+    disp = cs.displacements(0.2).astype(np.float32)
+    ix = np.clip(np.floor((np.float32(z.x) + disp[:, 0]) / np.float32(0.001)).astype(int), 0, 999)
+    iy = np.clip(np.floor((np.float32(z.y) + disp[:, 1]) / np.float32(0.001)).astype(int), 0, 999)
+    exact = np.zeros((1000, 1000))
+    np.add.at(exact, (iy, ix), p)
+    assert 0.5 * np.abs(layer - exact).sum() < 0.01
