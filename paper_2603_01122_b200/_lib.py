@@ -30,6 +30,7 @@ GC_ERRBIT_TABLE_ID = 1 << 10
 GC_ERRBIT_ASSUME_QG = 1 << 11
 GC_MAX_HYPOTHESES = 256
 GC_MAX_SMOOTH_RADIUS = 56  # include/gridcast_b200.h
+GC_MAX_ACTIONS = 512
 
 GC_Q_GOAL_PROGRESS = 0
 GC_Q_GOAL_PROGRESS_FULL = 1

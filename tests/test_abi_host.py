@@ -64,6 +64,22 @@ def test_abi_version(L):
     assert L.gc_abi_version() == 3
 
 
+def test_header_constants_match_the_python_mirror():
+    """Every GC_* integer constant the Python mirror restates equals the header's #define
+    (status codes, error bits, RNG modes, size limits...)."""
+    from paper_2603_01122_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "gridcast_b200.h")).read()
+    defs = dict(re.findall(r"^#define (GC_\w+) \(?([0-9u <]+)\)?\s*(?:/\*.*)?$", src, flags=re.M))
+    checked = 0
+    for name, expr in defs.items():
+        if hasattr(_lib, name):
+            val = eval(expr.replace("u", ""))  # noqa: S307 -- literal ints and shifts only
+            assert getattr(_lib, name) == val, (name, getattr(_lib, name), val)
+            checked += 1
+    assert checked >= 8, checked
+    assert {"GC_MAX_HYPOTHESES", "GC_MAX_ACTIONS", "GC_MAX_SMOOTH_RADIUS"} <= set(defs)
+
+
 def test_abi_rng_matches_reference_streams(L):
     from paper_2603_01122_b200 import rng
     z = golden_io.load("philox.npz")
