@@ -170,3 +170,20 @@ def test_assume_qg_fast_kernel_is_bit_identical_and_guarded(monkeypatch):
     assert torch.equal(fast["counts"], general["counts"]) and torch.equal(fast["union64"], general["union64"])
     with pytest.raises(ValueError, match="assume_qg"):
         run((300.0,), force=True)
+
+
+def test_predict_and_update_reject_control_sets_above_the_action_limit():
+    """GC_MAX_ACTIONS + 1 actions: gc_predict and gc_belief_update refuse the launch with
+    GC_BAD_ARG (a ValueError in the mirror) instead of overrunning the shared tables."""
+    m = _lib.GC_MAX_ACTIONS + 1
+    r = np.random.default_rng(0)
+    cs = G.ControlSet([G.ControlAction(float(v), float(t))
+                       for v, t in zip(r.uniform(0.1, 1.5, m), r.uniform(-3.1, 3.1, m))])
+    q = G.q_goal_progress(0.5)
+    space = G.HypothesisSpace(G.RationalitySet((1.0,)), G.GoalSet(np.array([[5.0, 5.0]])))
+    belief = G.init_belief(space)
+    cfg = G.PredictionConfig(n=256, steps=2, dt=0.1, smoothing_sigma=0.0, seed=0, mode="production")
+    with pytest.raises(ValueError, match="512 actions"):
+        G.predict(G.HumanState(1.0, 1.0), belief, cfg, cs, q, space, G.GridSpec(40, 40, 0.1))
+    with pytest.raises(ValueError, match="512 actions"):
+        G.update_belief(belief, G.HumanState(1.0, 1.0), G.HumanState(1.05, 1.0), 0.1, cs, q, space)
