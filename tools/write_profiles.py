@@ -150,9 +150,9 @@ def main():
     import sass_extract
     import sass_summary
     so = os.path.join(ROOT, "paper_2603_01122_b200", "_lib", "libgridcast_b200.so")
-    for name, fn in (("k_predict_production", "_ZN2gc9k_predictILi3ELi4ELb0ELb0EEEvNS_7KParamsE"),
-                     ("k_epilogue", "_ZN2gc10k_epilogueILi3EEEvNS_7EParamsE"),
-                     ("k_belief", "_ZN2gc8k_beliefENS_7BParamsE")):
+    for name, fn in (("k_predict_production", "_ZN2gc9k_predictILi4ELi4ELb0ELb0EEEvNS_7KParamsE"),
+                     ("k_epilogue", "_ZN2gc12k_epilogue_rILi3EEEvNS_7EParamsE"),
+                     ("k_belief", "_ZN2gc8k_beliefILi8EEEvNS_7BParamsE")):
         open(os.path.join(prof, f"{a.tag}_sass_{name}.txt"), "w").write(sass_extract.extract(so, fn) + "\n")
     open(os.path.join(prof, f"{a.tag}_sass_summary_all_kernels.txt"), "w").write(capture(sass_summary.main, so))
 
